@@ -1,0 +1,461 @@
+"""bench.py — batched FFT / CZT / Zoom FFT throughput on B200 (BASELINE.json metric).
+
+Headline workload (configs[1]): Bluestein CZT of 4096 THz-TDS trace pairs (8192 real traces,
+N=1024, M=2048 over 0.1-3 THz, L=4096), fp64, inputs resident in HBM. A "step" is one pass of the
+fused CZT kernel over the whole batch. Traces are independent, so N GPUs run weak-scaled batches
+with no data-path collective. Extra keys report the other configs (fp32 CZT, cfg3 zoom,
+cfg4 H cube, cfg1 latency) measured the same way.
+
+  python bench.py [--gpus N --steps K --warmup W]          our CUDA path
+  python bench.py --impl reference [...]                    the reference CPU path (oracle/_ref)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "traces/sec & achieved HBM GB/s (% of roofline) for batched FFT / CZT / Zoom FFT"
+UNIT = "traces/s"
+
+
+def peaks():
+    p = {"hbm_gbs": 6540.2, "source": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p["hbm_gbs"] = float(m["hbm_gbs"])
+        p["source"] = "MEASURED_PEAKS.json"
+    except Exception:
+        pass
+    return p
+
+
+# ---- algorithmic counts ----------------------------------------------------------
+def czt_counts(n, m, s):
+    L = 1 << math.ceil(math.log2(n + m - 1))
+    return {"bytes": n * s + m * 2 * s, "flops": 2 * 5 * L * math.log2(L) + 6 * (n + L + m), "L": L}
+
+
+def zoom_counts(n, D, T, n_fft, nb, s):
+    usable = (n // D) * D
+    blk = usable // D
+    return {"bytes": n * s + nb * 2 * s,
+            "flops": 2 * usable + 4 * T * blk + 5 * n_fft * math.log2(n_fft) + 8 * nb}
+
+
+def h_counts(n, L, s):
+    return {"bytes": n * s + (L // 2 + 1) * 2 * s, "flops": 2.5 * L * math.log2(L) + 6 * (L // 2 + 1)}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for i, nm in enumerate(names):
+                if len(r) > 4 + i and r[4 + i].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def dist_init():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def time_device(fn, steps, warmup, world, flush=None):
+    """W untimed steps, then K steps bracketed by barrier + synchronize; CUDA events on the
+    launching (current) stream; returns the max-over-ranks seconds for the K steps and the
+    per-step event times."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(st)
+    for a, b in evs:
+        if flush is not None:
+            flush()
+        a.record(st)
+        fn()
+        b.record(st)
+    t1.record(st)
+    torch.cuda.synchronize()
+    barrier(world)
+    per = [a.elapsed_time(b) * 1e-3 for a, b in evs]
+    kernel_total = max_over_ranks(sum(per), world)
+    return kernel_total, per
+
+
+def fp_peak_tflops(dtype):
+    """In-run measured CUDA-core FMA peak: cuBLAS {D,S}GEMM 8192^3 (TF32 off), best of 5 —
+    the same method MEASURED_PEAKS.json uses for bf16 (there is no fp64/fp32 entry there)."""
+    import torch
+    torch.backends.cuda.matmul.allow_tf32 = False
+    n = 8192 if dtype == torch.float32 else 4096
+    a = torch.randn(n, n, dtype=dtype, device="cuda")
+    b = torch.randn(n, n, dtype=dtype, device="cuda")
+    for _ in range(2):
+        a @ b
+    torch.cuda.synchronize()
+    best = 1e9
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        a @ b
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1) * 1e-3)
+    return 2 * n ** 3 / best / 1e12
+
+
+# ---- CPU baseline (the reference on this host's cores) -----------------------------------------
+def cpu_czt_baseline(x, a, w, m, seconds=4.0, threads=None):
+    import ctypes as C
+
+    import oracle
+    threads = threads or os.cpu_count() or 1
+    n = x.shape[1]
+    R = oracle.ref()
+    kind = "reference" if R is not None else "port"
+    xs = np.ascontiguousarray(x)
+    if R is not None:
+        p = R.skr_czt_plan_create(n, a.real, a.imag, w.real, w.imag, m)
+
+        def run(cnt):
+            return R.skr_czt_batch(p, oracle._p(xs), n, cnt, threads, None)
+    else:
+        plan = oracle.CztPlan(n, a, w, m)
+
+        def run(cnt):
+            return oracle.port().sko_bench_czt(plan._h, oracle._p(xs), n, cnt, threads, None)
+    run(min(len(xs), threads))   # warm-up (page in, thread start)
+    cnt = min(len(xs), threads * 4)
+    dt = run(cnt)
+    while dt < seconds / 4 and cnt < len(xs):
+        cnt = min(len(xs), cnt * 4)
+        dt = run(cnt)
+    if R is not None:
+        R.skr_czt_plan_free(p)
+    return {"value": cnt / dt, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{cnt} of the {len(xs)} cfg2 traces, plan reuse (CztPlan::execute), {threads} threads, "
+                      f"{dt:.2f} s wall"}
+
+
+# ---- our path ---------------------------------------------------------------------------------
+def bench_ours(args):
+    import torch
+
+    import paper_2108_03948_b200 as sk
+    from paper_2108_03948_b200 import workloads as W
+    rank, world, local = dist_init()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pk = peaks()
+    info = sk.device_info()
+    K, Wm = args.steps, args.warmup
+
+    # ---- headline: cfg2 CZT fp64 -----------------------------------------------------------
+    pairs = args.pairs
+    x_host = W.cfg2_batch(pairs, 1024).astype(np.float64)      # 8192 x 1024 (refs then samples)
+    B = x_host.shape[0]
+    a, w = W.cfg2_czt_params(2048)
+    plan = sk.CztPlanGPU(1024, a, w, 2048, sk.SKG_F64)
+    xd = torch.from_numpy(x_host).to(dev)
+    out = torch.empty((B, 2048), dtype=torch.complex128, device=dev)
+    fn = lambda: plan.execute(xd, out=out)  # noqa: E731
+    fn()
+    torch.cuda.synchronize()
+    l0 = sk.launch_count()
+    fn()
+    per_step_launches = sk.launch_count() - l0
+    with ClockSampler(local) as clk:
+        total, per = time_device(fn, K, Wm, world)
+    launches = per_step_launches * K
+    ms = total / K * 1e3
+    value = world * B * K / total
+    c = czt_counts(1024, 2048, 8)
+    fp64_peak = fp_peak_tflops(torch.float64)
+    kern_s = float(np.mean(per))
+    achieved_tf = c["flops"] * B / kern_s / 1e12
+    hbm_gbs = c["bytes"] * B / kern_s / 1e9
+    roof_t = max(c["bytes"] * B / (pk["hbm_gbs"] * 1e9), c["flops"] * B / (fp64_peak * 1e12))
+
+    # ---- e2e: host buffers through the C ABI, H2D + kernel + D2H per step ---------------------
+    xh = torch.from_numpy(x_host).pin_memory()
+    oh = torch.empty((B, 2048), dtype=torch.complex128).pin_memory()
+    chunks = 8
+    cs = B // chunks
+    s_copy = torch.cuda.Stream()
+    s_out = torch.cuda.Stream()
+    evs_in = [torch.cuda.Event() for _ in range(chunks)]
+    evs_k = [torch.cuda.Event() for _ in range(chunks)]
+
+    def e2e_step():
+        cur = torch.cuda.current_stream()
+        for i in range(chunks):
+            sl = slice(i * cs, (i + 1) * cs)
+            with torch.cuda.stream(s_copy):
+                xd[sl].copy_(xh[sl], non_blocking=True)
+                evs_in[i].record(s_copy)
+            cur.wait_event(evs_in[i])
+            plan.execute(xd[sl], out=out[sl])
+            evs_k[i].record(cur)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(evs_k[i])
+                oh[sl].copy_(out[sl], non_blocking=True)
+        cur.wait_stream(s_out)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(max(2, K // 2)):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_dt = max_over_ranks(time.perf_counter() - t0, world)
+    e2e_val = world * B * max(2, K // 2) / e2e_dt
+    # spot-check the e2e result against the device-resident result
+    ok_e2e = bool(torch.allclose(oh[:4].to(dev), out[:4]))
+
+    extra = {}
+    if not args.quick:
+        extra = bench_extras(args, sk, W, dev, world, pk)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": Wm,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded THz-TDS pulse pairs, SURVEY §8d)",
+        "config": {"workload": "cfg2: Bluestein CZT, 4096 pairs = 8192 real traces, N=1024, M=2048, "
+                               "0.1-3 THz, L=4096, fp64", "global_batch": B * world, "per_gpu_batch": B,
+                   "parallelism": f"dp{world} (independent traces, no collective)",
+                   "l2": "inputs 64 MiB + outputs 256 MiB per step > 126 MB L2 (no flush needed)"},
+        "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": fp64_peak, "unit": "TFLOP/s",
+                     "frac": achieved_tf / fp64_peak, "traffic": None,
+                     "peak_source": "in-run cuBLAS DGEMM 4096^3 (no fp64 entry in MEASURED_PEAKS.json)",
+                     "kernel": "skg::k_czt<double,12,4,8>", "kernel_ms": kern_s * 1e3,
+                     "flops_per_trace": c["flops"], "bytes_per_trace": c["bytes"],
+                     "hbm_achieved_gbs": hbm_gbs, "hbm_peak_gbs": pk["hbm_gbs"], "hbm_frac": hbm_gbs / pk["hbm_gbs"],
+                     "roof_frac": roof_t / kern_s},
+        "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(B * 1024 * 8),
+                "d2h_bytes_per_step": int(B * 2048 * 16), "chunks": chunks, "matches_device_result": ok_e2e},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "device": info,
+    }
+    if extra:
+        line["extra"] = extra
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_czt_baseline(x_host, a, w, 2048, seconds=args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def bench_extras(args, sk, W, dev, world, pk):
+    import torch
+    res = {}
+    K = max(3, args.steps // 2)
+    Wm = 3
+    fp32_peak = fp_peak_tflops(torch.float32)
+    # cfg2 fp32
+    x = W.cfg2_batch(args.pairs, 1024)
+    a, w = W.cfg2_czt_params(2048)
+    p32 = sk.CztPlanGPU(1024, a, w, 2048, sk.SKG_F32)
+    xd = torch.from_numpy(x.astype(np.float32)).to(dev)
+    out = torch.empty((x.shape[0], 2048), dtype=torch.complex64, device=dev)
+    t, per = time_device(lambda: p32.execute(xd, out=out), K, Wm, world)
+    c = czt_counts(1024, 2048, 4)
+    ks = float(np.mean(per))
+    res["cfg2_czt_f32"] = {"traces_per_s": x.shape[0] * K / t, "kernel_ms": ks * 1e3,
+                           "tflops": c["flops"] * x.shape[0] / ks / 1e12, "fp32_peak_tflops": fp32_peak,
+                           "frac_fp32": c["flops"] * x.shape[0] / ks / 1e12 / fp32_peak,
+                           "hbm_gbs": c["bytes"] * x.shape[0] / ks / 1e9}
+    del xd, out
+    # cfg3 zoom (reference sizing n_fft 512, and the 2048 text variant), fp64 + fp32
+    x3 = W.cfg3_batch(4096, 4096)
+    for prec, dt, s in (("f64", torch.float64, 8), ("f32", torch.float32, 4)):
+        xd = torch.from_numpy(x3).to(dt).to(dev)
+        for nf in (0, 2048):
+            zp = sk.ZoomPlanGPU(4096, 0.4e12, 1.2e12, W.FS, sk.SKG_F64 if prec == "f64" else sk.SKG_F32, n_fft=nf,
+                                decimation=8, num_taps=65)
+            out = torch.empty((4096, zp.bins), dtype=torch.complex128 if prec == "f64" else torch.complex64,
+                              device=dev)
+            t, per = time_device(lambda: zp.execute(xd, out=out), K, Wm, world)
+            ks = float(np.mean(per))
+            cc = zoom_counts(4096, 8, 65, zp.n_fft, zp.bins, s)
+            res[f"cfg3_zoom_nfft{zp.n_fft}_{prec}"] = {
+                "traces_per_s": 4096 * K / t, "kernel_ms": ks * 1e3, "hbm_gbs": cc["bytes"] * 4096 / ks / 1e9,
+                "hbm_frac": cc["bytes"] * 4096 / ks / 1e9 / pk["hbm_gbs"], "tflops": cc["flops"] * 4096 / ks / 1e12}
+        del xd
+    # cfg4 cube: 65536 px x 2048 fp32 -> |H|, arg H on 4097 bins
+    cube, ref = W.cfg4_cube(256, 256, 2048)
+    tp = sk.TransferPlanGPU(ref, 8192, sk.SKG_F32)
+    cd = torch.from_numpy(cube).to(dev)
+    mag = torch.empty((cube.shape[0], tp.bins), dtype=torch.float32, device=dev)
+    ph = torch.empty_like(mag)
+    t, per = time_device(lambda: tp.execute(cd, mag, ph), K, Wm, world)
+    ks = float(np.mean(per))
+    hc = h_counts(2048, 8192, 4)
+    res["cfg4_cube_H_f32"] = {"pixels_per_s": cube.shape[0] * K / t, "kernel_ms": ks * 1e3,
+                              "hbm_gbs": hc["bytes"] * cube.shape[0] / ks / 1e9,
+                              "hbm_frac": hc["bytes"] * cube.shape[0] / ks / 1e9 / pk["hbm_gbs"]}
+    del cd, mag, ph
+    # cfg1 latency: one pair, fp64, FFT 4096 + H (device-resident) and through the C ABI (host)
+    r1, s1 = W.cfg1_pair()
+    tp1 = sk.TransferPlanGPU(r1, 4096, sk.SKG_F64)
+    sd = torch.from_numpy(s1[None]).to(dev)
+    t, per = time_device(lambda: tp1.execute(sd), 20, 5, world)
+    t0 = time.perf_counter()
+    for _ in range(20):
+        sk.fft_spectrum(s1, W.FS, 4096)
+    res["cfg1_pair_f64"] = {"device_us_per_pair_H": float(np.median(per)) * 1e6,
+                            "c_abi_us_per_fft_spectrum": (time.perf_counter() - t0) / 20 * 1e6}
+    return res
+
+
+# ---- reference arm ----------------------------------------------------------------------------
+def bench_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import oracle
+    from paper_2108_03948_b200 import workloads as W
+    threads = os.cpu_count() or 1
+    R = oracle.ref()
+    kind = "reference" if R is not None else "port"
+    x = W.cfg2_batch(args.pairs, 1024)
+    a, w = W.cfg2_czt_params(2048)
+    n, m = 1024, 2048
+    xs = np.ascontiguousarray(x)
+    if R is not None:
+        p = R.skr_czt_plan_create(n, a.real, a.imag, w.real, w.imag, m)
+        run = lambda cnt: R.skr_czt_batch(p, oracle._p(xs), n, cnt, threads, None)  # noqa: E731
+    else:
+        plan = oracle.CztPlan(n, a, w, m)
+        run = lambda cnt: oracle.port().sko_bench_czt(plan._h, oracle._p(xs), n, cnt, threads, None)  # noqa: E731
+    # size one step to ~`ref_step_s` seconds of wall time
+    dt = run(threads)
+    per_trace = dt / threads
+    cnt = int(min(len(xs), max(threads, args.ref_step_s / max(per_trace, 1e-9) * threads)))
+    for _ in range(args.warmup):
+        run(cnt)
+    tot = 0.0
+    for _ in range(args.steps):
+        tot += run(cnt)
+    value = cnt * args.steps / tot
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded THz-TDS pulse pairs)",
+            "config": {"workload": "cfg2: Bluestein CZT, N=1024, M=2048, 0.1-3 THz, L=4096, fp64 "
+                                   f"(bounded sample of {cnt} traces per step)", "global_batch": cnt,
+                       "parallelism": f"{threads} host threads"},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                             "sample": f"{cnt} traces per step, CztPlan::execute plan reuse, shared plan"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--pairs", type=int, default=4096)
+    ap.add_argument("--quick", action="store_true", help="headline only")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=4.0)
+    ap.add_argument("--ref-step-s", type=float, default=3.0)
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_ours(args)
+
+
+if __name__ == "__main__":
+    main()

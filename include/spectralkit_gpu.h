@@ -1,0 +1,98 @@
+/* spectralkit_gpu.h — batched, device-resident extension of the spectralkit C ABI.
+ *
+ * The reference has no batch interface: every sk_* call transforms one trace held in host
+ * memory. These entry points run the same transforms on a batch of traces that
+ * already lives in GPU memory (device pointers from cudaMalloc, torch, CuPy, ...), enqueue on
+ * the caller's CUDA stream and return without synchronising. Plans hold the precomputed
+ * twiddle / chirp / filter tables on the device and are immutable after creation, so one plan
+ * may be shared by concurrent streams (the reference's plan rule, numerics.hpp:24-26).
+ *
+ * Layouts: traces are real rows of `n` samples, row stride `x_stride` elements; complex outputs
+ * are interleaved (re, im) — the std::complex layout of the reference's ComplexBuffer —
+ * with row stride in complex elements. precision: SKG_F64 (double / complex128 buffers) or
+ * SKG_F32 (float / complex64 buffers; tables are rounded from fp64).
+ */
+#ifndef SPECTRALKIT_GPU_H
+#define SPECTRALKIT_GPU_H
+
+#include "spectralkit.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum skg_precision { SKG_F64 = 0, SKG_F32 = 1 } skg_precision;
+
+/* device facts of the current CUDA device */
+SK_API sk_status skg_device_info(int* device, int* sm_count, size_t* smem_optin, size_t* l2_bytes);
+/* number of kernels this library has launched in the process (evidence counter) */
+SK_API uint64_t skg_launch_count(void);
+/* cudaStreamSynchronize(stream) with the library's error reporting */
+SK_API sk_status skg_synchronize(void* stream);
+
+/* Complex-to-complex FFT of `batch` rows of n points (power of two); inverse applies 1/n
+ * (numerics.cpp:73-100). d_in == d_out is allowed. */
+SK_API sk_status skg_fft_batch(size_t n, int inverse, int precision, const void* d_in,
+                               size_t in_stride, void* d_out, size_t out_stride, size_t batch,
+                               void* stream);
+
+/* Zero-padded spectrum of real traces (fft_spectrum, spectra.cpp:21-38). transform_len 0 =
+ * next_pow2(n). layout SKG_FULL: transform_len bins on [0, fs) (the reference layout);
+ * SKG_HALF: transform_len/2 + 1 bins on [0, fs/2]. Non-power-of-two transform_len runs the
+ * chirp route (dft_any, czt.cpp:144-153) and supports SKG_FULL only. */
+#define SKG_FULL 0
+#define SKG_HALF 1
+SK_API sk_status skg_fft_spectrum_batch(size_t n, size_t transform_len, int precision, int layout,
+                                        const void* d_x, size_t x_stride, size_t batch,
+                                        void* d_out, size_t out_stride, void* stream);
+
+/* Chirp-z transform plan (CztPlan, czt.cpp:85-137). */
+typedef struct skg_czt_plan skg_czt_plan;
+SK_API sk_status skg_czt_plan_create(size_t n, double a_re, double a_im, double w_re, double w_im,
+                                     size_t m, int precision, skg_czt_plan** out);
+SK_API void skg_czt_plan_free(skg_czt_plan* p);
+SK_API size_t skg_czt_plan_conv_size(const skg_czt_plan* p);
+/* x: real (x_complex = 0) or interleaved complex rows of n; out: rows of m complex bins */
+SK_API sk_status skg_czt_execute(const skg_czt_plan* p, const void* d_x, int x_complex,
+                                 size_t x_stride, size_t batch, void* d_out, size_t out_stride,
+                                 void* stream);
+
+/* Transfer function H(f) = X_sample(f) / X_ref(f) against one shared reference trace, fused
+ * into the FFT store epilogue: per trace, transform_len/2 + 1 bins of |H| and arg H (radians,
+ * atan2 convention) and optionally the complex H. */
+typedef struct skg_transfer_plan skg_transfer_plan;
+SK_API sk_status skg_transfer_plan_create(const double* ref_samples, size_t n, size_t transform_len,
+                                          int precision, skg_transfer_plan** out);
+SK_API void skg_transfer_plan_free(skg_transfer_plan* p);
+SK_API size_t skg_transfer_plan_bins(const skg_transfer_plan* p);
+/* copies X_ref (bins complex, fp64) to host */
+SK_API sk_status skg_transfer_plan_reference(const skg_transfer_plan* p, double* xr_interleaved);
+SK_API sk_status skg_transfer_execute(const skg_transfer_plan* p, const void* d_x, size_t x_stride,
+                                      size_t batch, void* d_mag, void* d_phase, size_t mp_stride,
+                                      void* d_h, size_t h_stride, void* stream);
+
+/* Zoom FFT plan (make_zoom_plan + zoom_fft, zoomfft.cpp:106-239). `ext` (may be NULL) carries
+ * knobs the reference struct lacks: an explicit short-FFT length n_fft (>= decimated block;
+ * the reference derives next_pow2(block)) and an explicit filter (any length, including the
+ * even 64-tap design of the cfg3 text; the reference designs odd Hamming-sinc filters only). */
+typedef struct skg_zoom_ext {
+    size_t n_fft;          /* 0 = reference sizing */
+    const double* taps;    /* NULL = reference design */
+    size_t num_taps;
+} skg_zoom_ext;
+typedef struct skg_zoom_plan skg_zoom_plan;
+SK_API sk_status skg_zoom_plan_create(size_t input_len, double f1_hz, double f2_hz,
+                                      double sample_rate_hz, const sk_zoom_options* opts,
+                                      const skg_zoom_ext* ext, int precision, skg_zoom_plan** out);
+SK_API void skg_zoom_plan_free(skg_zoom_plan* p);
+SK_API sk_status skg_zoom_plan_info(const skg_zoom_plan* p, size_t* bins, double* f_start_hz,
+                                    double* f_step_hz, size_t* n_fft, size_t* decimation,
+                                    size_t* num_taps);
+SK_API sk_status skg_zoom_execute(const skg_zoom_plan* p, const void* d_x, size_t x_stride,
+                                  size_t batch, void* d_out, size_t out_stride, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPECTRALKIT_GPU_H */

@@ -1,0 +1,512 @@
+"""paper_2108_03948_b200 — B200-native batched FFT / CZT / Zoom FFT for THz-TDS traces.
+
+The product is the C-ABI shared library ``lib/libspectralkit_b200.so`` (CUDA C++ for sm_100a,
+sources in ``csrc/``). This module is the Python mirror of the reference's transform API
+(/root/reference/proj/include/spectralkit.h and src/*.hpp) over that C ABI:
+
+* single-trace, host-memory calls with the reference's names and semantics
+  (``fft``, ``ifft``, ``czt``, ``fft_spectrum``, ``czt_spectrum``, ``ZoomPlan`` ...), each one a
+  host->device->host round trip through the ``sk_*`` entry points;
+* batched, device-resident calls on torch CUDA tensors (``fft_batch``, ``fft_spectrum_batch``,
+  ``CztPlanGPU``, ``TransferPlanGPU``, ``ZoomPlanGPU``) through the ``skg_*`` extension, enqueued on
+  the current torch stream.
+
+Errors raise :class:`SkError` carrying the ``sk_status`` code and ``sk_last_error()`` text
+(the reference maps C++ exceptions to the same codes, capi.cpp:48-78). There is no CPU fallback:
+if the shared library is missing or no GPU is present the calls fail loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libspectralkit_b200.so")
+
+SK_OK, SK_ERR_INVALID_ARGUMENT, SK_ERR_INTERNAL = 0, 1, 6
+SKG_F64, SKG_F32 = 0, 1
+SKG_FULL, SKG_HALF = 0, 1
+
+_lib = None
+dp = C.POINTER(C.c_double)
+sz = C.c_size_t
+vp = C.c_void_p
+
+
+class SkError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"[{status}] {message}")
+        self.status = status
+        self.message = message
+
+
+class SkZoomOptions(C.Structure):
+    """sk_zoom_options (spectralkit.h:170-179 layout)."""
+    _fields_ = [("center_hz", C.c_double), ("center_set", C.c_int), ("decimation", sz),
+                ("cutoff_hz", C.c_double), ("num_taps", sz), ("circular", C.c_int),
+                ("trim_transient", C.c_int), ("pad_pow2", C.c_int)]
+
+
+class SkgZoomExt(C.Structure):
+    _fields_ = [("n_fft", sz), ("taps", dp), ("num_taps", sz)]
+
+
+def _declare(L):
+    st = C.c_int
+    sig = {
+        "sk_status_name": (C.c_char_p, [st]),
+        "sk_last_error": (C.c_char_p, []),
+        "sk_version": (C.c_char_p, []),
+        "sk_fft": (st, [dp, dp, sz]),
+        "sk_ifft": (st, [dp, dp, sz]),
+        "sk_dft_naive": (st, [dp, dp, sz, dp, dp]),
+        "sk_czt": (st, [dp, dp, sz, C.c_double, C.c_double, C.c_double, C.c_double, sz, dp, dp]),
+        "sk_czt_direct": (st, [dp, dp, sz, C.c_double, C.c_double, C.c_double, C.c_double, sz, dp, dp]),
+        "sk_czt_params_for_band": (st, [C.c_double, C.c_double, C.c_double, sz, dp, dp, dp, dp]),
+        "sk_next_pow2": (sz, [sz]),
+        "sk_trace_create": (st, [dp, sz, C.c_double, C.c_double, C.POINTER(vp)]),
+        "sk_trace_free": (None, [vp]),
+        "sk_trace_size": (sz, [vp]),
+        "sk_trace_sample_rate": (C.c_double, [vp]),
+        "sk_trace_t0": (C.c_double, [vp]),
+        "sk_trace_samples": (dp, [vp]),
+        "sk_fft_spectrum": (st, [vp, sz, C.POINTER(vp)]),
+        "sk_czt_spectrum": (st, [vp, C.c_double, C.c_double, sz, C.POINTER(vp)]),
+        "sk_spectrum_create": (st, [dp, dp, sz, C.c_double, C.c_double, C.POINTER(vp)]),
+        "sk_spectrum_free": (None, [vp]),
+        "sk_spectrum_size": (sz, [vp]),
+        "sk_spectrum_f_start": (C.c_double, [vp]),
+        "sk_spectrum_f_step": (C.c_double, [vp]),
+        "sk_spectrum_frequency": (C.c_double, [vp, sz]),
+        "sk_spectrum_source_n": (sz, [vp]),
+        "sk_spectrum_bin": (st, [vp, sz, dp, dp]),
+        "sk_spectrum_magnitude_db": (st, [vp, sz, dp]),
+        "sk_spectrum_copy_data": (st, [vp, dp, dp]),
+        "sk_spectrum_slice_band": (st, [vp, C.c_double, C.c_double, C.POINTER(vp)]),
+        "sk_zoom_options_defaults": (None, [C.POINTER(SkZoomOptions)]),
+        "sk_zoom_plan_create": (st, [sz, C.c_double, C.c_double, C.c_double, C.POINTER(SkZoomOptions),
+                                     C.POINTER(vp)]),
+        "sk_zoom_plan_free": (None, [vp]),
+        "sk_zoom_plan_decimation": (sz, [vp]),
+        "sk_zoom_plan_n_fft": (sz, [vp]),
+        "sk_zoom_plan_filter_len": (sz, [vp]),
+        "sk_zoom_plan_f_step": (C.c_double, [vp]),
+        "sk_zoom_spectrum": (st, [vp, vp, C.POINTER(vp)]),
+        "skg_device_info": (st, [C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(sz), C.POINTER(sz)]),
+        "skg_launch_count": (C.c_uint64, []),
+        "skg_synchronize": (st, [vp]),
+        "skg_fft_batch": (st, [sz, C.c_int, C.c_int, vp, sz, vp, sz, sz, vp]),
+        "skg_fft_spectrum_batch": (st, [sz, sz, C.c_int, C.c_int, vp, sz, sz, vp, sz, vp]),
+        "skg_czt_plan_create": (st, [sz, C.c_double, C.c_double, C.c_double, C.c_double, sz, C.c_int,
+                                     C.POINTER(vp)]),
+        "skg_czt_plan_free": (None, [vp]),
+        "skg_czt_plan_conv_size": (sz, [vp]),
+        "skg_czt_execute": (st, [vp, vp, C.c_int, sz, sz, vp, sz, vp]),
+        "skg_transfer_plan_create": (st, [dp, sz, sz, C.c_int, C.POINTER(vp)]),
+        "skg_transfer_plan_free": (None, [vp]),
+        "skg_transfer_plan_bins": (sz, [vp]),
+        "skg_transfer_plan_reference": (st, [vp, dp]),
+        "skg_transfer_execute": (st, [vp, vp, sz, sz, vp, vp, sz, vp, sz, vp]),
+        "skg_zoom_plan_create": (st, [sz, C.c_double, C.c_double, C.c_double, C.POINTER(SkZoomOptions),
+                                      C.POINTER(SkgZoomExt), C.c_int, C.POINTER(vp)]),
+        "skg_zoom_plan_free": (None, [vp]),
+        "skg_zoom_plan_info": (st, [vp, C.POINTER(sz), dp, dp, C.POINTER(sz), C.POINTER(sz), C.POINTER(sz)]),
+        "skg_zoom_execute": (st, [vp, vp, sz, sz, vp, sz, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    return L
+
+
+def lib():
+    """Load the CUDA shared library (raises if it was not built — no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (make -C csrc)")
+        _lib = _declare(C.CDLL(LIB_PATH))
+    return _lib
+
+
+def exported_symbols():
+    """Names declared SK_API in include/*.h (used by the export test)."""
+    import re
+    names = []
+    inc = os.path.join(os.path.dirname(HERE), "include")
+    for fn in sorted(os.listdir(inc)):
+        if fn.endswith(".h"):
+            src = open(os.path.join(inc, fn)).read()
+            names += re.findall(r"SK_API\s+[\w\s\*]+?\b(sk\w+)\s*\(", src)
+    return names
+
+
+def _chk(status):
+    if status != SK_OK:
+        raise SkError(status, lib().sk_last_error().decode())
+
+
+def _p(a):
+    return a.ctypes.data_as(dp)
+
+
+def last_error() -> str:
+    return lib().sk_last_error().decode()
+
+
+def launch_count() -> int:
+    return int(lib().skg_launch_count())
+
+
+def device_info():
+    d, s = C.c_int(), C.c_int()
+    smem, l2 = sz(), sz()
+    _chk(lib().skg_device_info(C.byref(d), C.byref(s), C.byref(smem), C.byref(l2)))
+    return {"device": d.value, "sm_count": s.value, "smem_optin": smem.value, "l2_bytes": l2.value}
+
+
+# ---- single-trace host API (reference C ABI semantics) ---------------------------------------
+
+def _split(x):
+    x = np.asarray(x, dtype=np.complex128)
+    return np.ascontiguousarray(x.real), np.ascontiguousarray(x.imag)
+
+
+def fft(x):
+    """sk_fft: forward, unnormalised, n power of two (numerics.cpp:102-120)."""
+    re, im = _split(x)
+    _chk(lib().sk_fft(_p(re), _p(im), re.size))
+    return re + 1j * im
+
+
+def ifft(x):
+    re, im = _split(x)
+    _chk(lib().sk_ifft(_p(re), _p(im), re.size))
+    return re + 1j * im
+
+
+def dft_naive(x):
+    re, im = _split(x)
+    orr, oi = np.empty_like(re), np.empty_like(im)
+    _chk(lib().sk_dft_naive(_p(re), _p(im), re.size, _p(orr), _p(oi)))
+    return orr + 1j * oi
+
+
+def czt(x, a, w, m):
+    """sk_czt: X[k] = sum_n x[n] a^-n w^(kn), k < m (Bluestein on the GPU)."""
+    re, im = _split(x)
+    orr, oi = np.empty(m), np.empty(m)
+    a, w = complex(a), complex(w)
+    _chk(lib().sk_czt(_p(re), _p(im), re.size, a.real, a.imag, w.real, w.imag, m, _p(orr), _p(oi)))
+    return orr + 1j * oi
+
+
+def czt_direct(x, a, w, m):
+    re, im = _split(x)
+    orr, oi = np.empty(m), np.empty(m)
+    a, w = complex(a), complex(w)
+    _chk(lib().sk_czt_direct(_p(re), _p(im), re.size, a.real, a.imag, w.real, w.imag, m, _p(orr), _p(oi)))
+    return orr + 1j * oi
+
+
+def czt_params_for_band(f1, f2, fs, m):
+    v = [C.c_double() for _ in range(4)]
+    _chk(lib().sk_czt_params_for_band(f1, f2, fs, m, *[C.byref(t) for t in v]))
+    return complex(v[0].value, v[1].value), complex(v[2].value, v[3].value)
+
+
+def next_pow2(n: int) -> int:
+    return int(lib().sk_next_pow2(n))
+
+
+@dataclass
+class Spectrum:
+    bins: np.ndarray
+    f_start_hz: float
+    f_step_hz: float
+    source_n: int
+
+    def frequency(self, k):
+        return self.f_start_hz + k * self.f_step_hz
+
+
+class Trace:
+    """Owning wrapper of sk_trace (samples, fs, t0)."""
+
+    def __init__(self, samples, sample_rate_hz, t0_s=0.0):
+        s = np.ascontiguousarray(samples, dtype=np.float64)
+        h = vp()
+        _chk(lib().sk_trace_create(_p(s), s.size, sample_rate_hz, t0_s, C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __len__(self):
+        return int(lib().sk_trace_size(self._h))
+
+    @property
+    def sample_rate_hz(self):
+        return float(lib().sk_trace_sample_rate(self._h))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().sk_trace_free(self._h)
+            self._h = None
+
+
+def _take_spectrum(h) -> Spectrum:
+    L = lib()
+    n = int(L.sk_spectrum_size(h))
+    re, im = np.empty(n), np.empty(n)
+    _chk(L.sk_spectrum_copy_data(h, _p(re), _p(im)))
+    s = Spectrum(re + 1j * im, float(L.sk_spectrum_f_start(h)), float(L.sk_spectrum_f_step(h)),
+                 int(L.sk_spectrum_source_n(h)))
+    L.sk_spectrum_free(h)
+    return s
+
+
+def fft_spectrum(samples, sample_rate_hz, transform_len=0) -> Spectrum:
+    """sk_fft_spectrum: full [0, fs) spectrum of a real trace (spectra.cpp:21-38)."""
+    t = Trace(samples, sample_rate_hz)
+    h = vp()
+    _chk(lib().sk_fft_spectrum(t.handle, transform_len, C.byref(h)))
+    return _take_spectrum(h)
+
+
+def czt_spectrum(samples, sample_rate_hz, f1, f2, m) -> Spectrum:
+    t = Trace(samples, sample_rate_hz)
+    h = vp()
+    _chk(lib().sk_czt_spectrum(t.handle, f1, f2, m, C.byref(h)))
+    return _take_spectrum(h)
+
+
+def slice_band(spec: Spectrum, f_lo, f_hi) -> Spectrum:
+    re, im = _split(spec.bins)
+    h = vp()
+    _chk(lib().sk_spectrum_create(_p(re), _p(im), re.size, spec.f_start_hz, spec.f_step_hz, C.byref(h)))
+    out = vp()
+    st = lib().sk_spectrum_slice_band(h, f_lo, f_hi, C.byref(out))
+    lib().sk_spectrum_free(h)
+    _chk(st)
+    s = _take_spectrum(out)
+    s.source_n = spec.source_n
+    return s
+
+
+def zoom_options(**kw) -> SkZoomOptions:
+    o = SkZoomOptions()
+    lib().sk_zoom_options_defaults(C.byref(o))
+    for k, v in kw.items():
+        setattr(o, k, v)
+        if k == "center_hz":
+            o.center_set = 1
+    return o
+
+
+class ZoomPlan:
+    """sk_zoom_plan (make_zoom_plan, zoomfft.cpp:106-181)."""
+
+    def __init__(self, input_len, f1, f2, fs, **opts):
+        o = zoom_options(**opts)
+        h = vp()
+        _chk(lib().sk_zoom_plan_create(input_len, f1, f2, fs, C.byref(o), C.byref(h)))
+        self._h = h
+        self.fs = fs
+
+    @property
+    def decimation(self):
+        return int(lib().sk_zoom_plan_decimation(self._h))
+
+    @property
+    def n_fft(self):
+        return int(lib().sk_zoom_plan_n_fft(self._h))
+
+    @property
+    def filter_len(self):
+        return int(lib().sk_zoom_plan_filter_len(self._h))
+
+    @property
+    def f_step_hz(self):
+        return float(lib().sk_zoom_plan_f_step(self._h))
+
+    def spectrum(self, samples, fs=None) -> Spectrum:
+        t = Trace(samples, self.fs if fs is None else fs)
+        h = vp()
+        _chk(lib().sk_zoom_spectrum(self._h, t.handle, C.byref(h)))
+        return _take_spectrum(h)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().sk_zoom_plan_free(self._h)
+            self._h = None
+
+
+# ---- batched device API (torch CUDA tensors) -------------------------------------------------
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream():
+    torch = _torch()
+    return vp(torch.cuda.current_stream().cuda_stream)
+
+
+def _prec(t):
+    torch = _torch()
+    if t.dtype in (torch.float64, torch.complex128):
+        return SKG_F64
+    if t.dtype in (torch.float32, torch.complex64):
+        return SKG_F32
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def _cdtype(prec):
+    torch = _torch()
+    return torch.complex128 if prec == SKG_F64 else torch.complex64
+
+
+def _rows(x):
+    """(batch, row stride) of a 1-D or 2-D tensor with unit inner stride."""
+    if x.dim() == 1:
+        x = x.unsqueeze(0)
+    assert x.stride(-1) == 1, "rows must be contiguous"
+    return x, x.shape[0], x.stride(0)
+
+
+def fft_batch(x, inverse=False, out=None):
+    """Complex FFT of each row of a complex CUDA tensor (skg_fft_batch)."""
+    x, b, s = _rows(x)
+    prec = _prec(x)
+    out = torch_empty_like_rows(x) if out is None else out
+    _chk(lib().skg_fft_batch(x.shape[-1], int(inverse), prec, vp(x.data_ptr()), s, vp(out.data_ptr()),
+                             out.stride(0) if out.dim() == 2 else 0, b, _stream()))
+    return out
+
+
+def torch_empty_like_rows(x):
+    torch = _torch()
+    return torch.empty(x.shape, dtype=x.dtype, device=x.device)
+
+
+def fft_spectrum_batch(x, transform_len=0, layout=SKG_FULL, out=None):
+    """Zero-padded spectra of real trace rows (skg_fft_spectrum_batch)."""
+    torch = _torch()
+    x, b, s = _rows(x)
+    prec = _prec(x)
+    n = x.shape[-1]
+    L = transform_len or next_pow2(n)
+    nb = L if layout == SKG_FULL else L // 2 + 1
+    if out is None:
+        out = torch.empty((b, nb), dtype=_cdtype(prec), device=x.device)
+    _chk(lib().skg_fft_spectrum_batch(n, L, prec, layout, vp(x.data_ptr()), s, b, vp(out.data_ptr()),
+                                      out.stride(0), _stream()))
+    return out
+
+
+class CztPlanGPU:
+    """Batched Bluestein CZT plan (CztPlan, czt.cpp:85-137) on device tables."""
+
+    def __init__(self, n, a, w, m, precision=SKG_F64):
+        a, w = complex(a), complex(w)
+        h = vp()
+        _chk(lib().skg_czt_plan_create(n, a.real, a.imag, w.real, w.imag, m, precision, C.byref(h)))
+        self._h, self.n, self.m, self.precision = h, n, m, precision
+
+    @property
+    def conv_size(self):
+        return int(lib().skg_czt_plan_conv_size(self._h))
+
+    def execute(self, x, out=None):
+        torch = _torch()
+        x, b, s = _rows(x)
+        is_c = x.is_complex()
+        if out is None:
+            out = torch.empty((b, self.m), dtype=_cdtype(self.precision), device=x.device)
+        _chk(lib().skg_czt_execute(self._h, vp(x.data_ptr()), int(is_c), s, b, vp(out.data_ptr()),
+                                   out.stride(0), _stream()))
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().skg_czt_plan_free(self._h)
+            self._h = None
+
+
+class TransferPlanGPU:
+    """H(f) = X_sample / X_ref fused into the FFT store epilogue (skg_transfer_*)."""
+
+    def __init__(self, ref_samples, transform_len=0, precision=SKG_F64):
+        r = np.ascontiguousarray(ref_samples, dtype=np.float64)
+        h = vp()
+        _chk(lib().skg_transfer_plan_create(_p(r), r.size, transform_len, precision, C.byref(h)))
+        self._h, self.n, self.precision = h, r.size, precision
+        self.bins = int(lib().skg_transfer_plan_bins(h))
+
+    def reference_spectrum(self):
+        out = np.empty(self.bins, np.complex128)
+        _chk(lib().skg_transfer_plan_reference(self._h, _p(out.view(np.float64))))
+        return out
+
+    def execute(self, x, mag=None, phase=None, h=None):
+        torch = _torch()
+        x, b, s = _rows(x)
+        rd = torch.float64 if self.precision == SKG_F64 else torch.float32
+        if mag is None:
+            mag = torch.empty((b, self.bins), dtype=rd, device=x.device)
+        if phase is None:
+            phase = torch.empty((b, self.bins), dtype=rd, device=x.device)
+        _chk(lib().skg_transfer_execute(self._h, vp(x.data_ptr()), s, b, vp(mag.data_ptr()),
+                                        vp(phase.data_ptr()), mag.stride(0),
+                                        vp(h.data_ptr()) if h is not None else None,
+                                        h.stride(0) if h is not None else 0, _stream()))
+        return mag, phase
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().skg_transfer_plan_free(self._h)
+            self._h = None
+
+
+class ZoomPlanGPU:
+    """Batched fused Zoom FFT plan (make_zoom_plan + zoom_fft) with optional n_fft / taps overrides."""
+
+    def __init__(self, input_len, f1, f2, fs, precision=SKG_F64, n_fft=0, taps=None, **opts):
+        o = zoom_options(**opts)
+        ext = SkgZoomExt()
+        ext.n_fft = n_fft
+        self._taps = None
+        if taps is not None:
+            self._taps = np.ascontiguousarray(taps, dtype=np.float64)
+            ext.taps = _p(self._taps)
+            ext.num_taps = self._taps.size
+        h = vp()
+        _chk(lib().skg_zoom_plan_create(input_len, f1, f2, fs, C.byref(o), C.byref(ext), precision, C.byref(h)))
+        self._h, self.precision, self.input_len = h, precision, input_len
+        nb, nf, d, nt = sz(), sz(), sz(), sz()
+        f0, df = C.c_double(), C.c_double()
+        _chk(lib().skg_zoom_plan_info(h, C.byref(nb), C.byref(f0), C.byref(df), C.byref(nf), C.byref(d),
+                                      C.byref(nt)))
+        self.bins, self.f_start_hz, self.f_step_hz = nb.value, f0.value, df.value
+        self.n_fft, self.decimation, self.num_taps = nf.value, d.value, nt.value
+
+    def execute(self, x, out=None):
+        torch = _torch()
+        x, b, s = _rows(x)
+        if out is None:
+            out = torch.empty((b, self.bins), dtype=_cdtype(self.precision), device=x.device)
+        _chk(lib().skg_zoom_execute(self._h, vp(x.data_ptr()), s, b, vp(out.data_ptr()), out.stride(0),
+                                    _stream()))
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().skg_zoom_plan_free(self._h)
+            self._h = None

@@ -1,0 +1,575 @@
+// capi.cpp — the drop-in sk_* C ABI (include/spectralkit.h) and the batched skg_* extension
+// (include/spectralkit_gpu.h). Error convention follows the reference's capi.cpp:44-83:
+// exceptions are mapped to status codes, the message goes to a thread-local string.
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "host.hpp"
+#include "spectralkit.h"
+#include "spectralkit_gpu.h"
+
+namespace skg {
+cudaError_t launch_dft_naive(const void* x, long long n, const void* tw, void* out, cudaStream_t st);
+cudaError_t launch_czt_direct(const void* x, long long n, double a_logm, double a_q, double w_logm, double w_q,
+                              long long m, void* xa_scratch, void* out, cudaStream_t st);
+}  // namespace skg
+
+using skg::cd;
+
+struct sk_trace {
+    std::vector<double> samples;
+    double fs = 0.0, t0 = 0.0;
+};
+struct sk_spectrum {
+    std::vector<cd> bins;
+    double f_start = 0.0, f_step = 0.0;
+    size_t source_n = 0;
+};
+struct sk_zoom_plan {
+    std::unique_ptr<skg::ZoomPlanG> p;
+};
+struct skg_czt_plan {
+    std::unique_ptr<skg::CztPlanG> p;
+    bool f32 = false;
+};
+struct skg_transfer_plan {
+    std::unique_ptr<skg::TransferPlanG> p;
+};
+struct skg_zoom_plan {
+    std::unique_ptr<skg::ZoomPlanG> p;
+    bool f32 = false;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename Fn> sk_status guarded(Fn&& fn) {
+    try {
+        fn();
+        return SK_OK;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return SK_ERR_INVALID_ARGUMENT;
+    } catch (const std::bad_alloc&) {
+        g_err = "out of memory";
+        return SK_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return SK_ERR_INTERNAL;
+    } catch (...) {
+        g_err = "unknown error";
+        return SK_ERR_INTERNAL;
+    }
+}
+
+sk_status bad_arg(const char* msg) {
+    g_err = msg;
+    return SK_ERR_INVALID_ARGUMENT;
+}
+
+// types.cpp:20-27
+void validate_trace(const sk_trace& t) {
+    if (t.samples.empty()) throw std::invalid_argument("trace: no samples");
+    if (!(t.fs > 0.0) || !std::isfinite(t.fs))
+        throw std::invalid_argument("trace: sample rate must be positive and finite");
+    for (double v : t.samples)
+        if (!std::isfinite(v)) throw std::invalid_argument("trace: non-finite sample");
+    if (!std::isfinite(t.t0)) throw std::invalid_argument("trace: non-finite start time");
+}
+
+std::vector<cd> join(const double* re, const double* im, size_t n) {
+    std::vector<cd> x(n);
+    for (size_t i = 0; i < n; ++i) x[i] = cd(re[i], im ? im[i] : 0.0);
+    return x;
+}
+
+void split(const std::vector<cd>& x, double* re, double* im) {
+    for (size_t i = 0; i < x.size(); ++i) {
+        re[i] = x[i].real();
+        im[i] = x[i].imag();
+    }
+}
+
+// one-shot staging: host -> device -> host on the per-thread default stream
+struct Stage {
+    cudaStream_t st = cudaStreamPerThread;
+    skg::DevMem in, out;
+    void put(const void* h, size_t bytes) {
+        skg::require_device();
+        in = skg::DevMem(bytes);
+        skg::check(cudaMemcpyAsync(in.p, h, bytes, cudaMemcpyHostToDevice, st), "H2D");
+    }
+    void alloc_out(size_t bytes) { out = skg::DevMem(bytes); }
+    void get(void* h, size_t bytes) {
+        skg::check(cudaMemcpyAsync(h, out.p, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+        skg::check(cudaStreamSynchronize(st), "sync");
+    }
+};
+
+void fft_inplace(double* re, double* im, size_t n, bool inverse) {   // numerics.cpp:102-120
+    if (n == 0) throw std::invalid_argument("fft: empty input");
+    if (!skg::is_pow2(n))
+        throw std::invalid_argument("fft: length " + std::to_string(n) + " is not a power of two; zero_pad to " +
+                                    std::to_string(skg::next_pow2(n)) + " first");
+    std::vector<cd> x = join(re, im, n);
+    Stage s;
+    s.put(x.data(), n * sizeof(cd));
+    skg::fft_c2c(n, inverse, false, s.in.p, 0, s.in.p, 0, 1, s.st);
+    s.out = std::move(s.in);
+    s.get(x.data(), n * sizeof(cd));
+    split(x, re, im);
+}
+
+std::vector<cd> czt_gpu(const std::vector<cd>& x, cd a, cd w, size_t m) {   // czt.cpp:139-142
+    if (x.empty()) throw std::invalid_argument("czt: empty input");
+    skg::CztPlanG plan(x.size(), a, w, m);
+    Stage s;
+    s.put(x.data(), x.size() * sizeof(cd));
+    s.alloc_out(m * sizeof(cd));
+    plan.execute(s.in.p, true, 0, 1, s.out.p, 0, false, s.st);
+    std::vector<cd> y(m);
+    s.get(y.data(), m * sizeof(cd));
+    return y;
+}
+
+sk_spectrum* fft_spectrum_gpu(const sk_trace& t, size_t transform_len) {   // spectra.cpp:21-38
+    validate_trace(t);
+    const size_t n = t.samples.size();
+    const size_t len = transform_len == 0 ? skg::next_pow2(n) : transform_len;
+    if (len < n) throw std::invalid_argument("fft_spectrum: transform length shorter than the trace");
+    Stage s;
+    s.put(t.samples.data(), n * sizeof(double));
+    s.alloc_out(len * sizeof(cd));
+    skg::fft_spectrum_batch(n, len, false, 0, s.in.p, 0, 1, s.out.p, 0, s.st);
+    auto* out = new sk_spectrum;
+    out->bins.resize(len);
+    s.get(out->bins.data(), len * sizeof(cd));
+    out->f_start = 0.0;
+    out->f_step = t.fs / static_cast<double>(len);
+    out->source_n = len;
+    return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sk_status_name(sk_status status) {
+    switch (status) {
+        case SK_OK: return "ok";
+        case SK_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case SK_ERR_IO: return "io error";
+        case SK_ERR_PARSE: return "parse error";
+        case SK_ERR_FORMAT: return "format error";
+        case SK_ERR_INSUFFICIENT_RESOLUTION: return "insufficient resolution";
+        case SK_ERR_INTERNAL: return "internal error";
+    }
+    return "unknown status";
+}
+
+const char* sk_last_error(void) { return g_err.c_str(); }
+const char* sk_version(void) { return "0.1.0-b200"; }
+
+sk_status sk_fft(double* re, double* im, size_t n) {
+    if (!re || !im) return bad_arg("sk_fft: null buffer");
+    return guarded([&] { fft_inplace(re, im, n, false); });
+}
+
+sk_status sk_ifft(double* re, double* im, size_t n) {
+    if (!re || !im) return bad_arg("sk_ifft: null buffer");
+    return guarded([&] { fft_inplace(re, im, n, true); });
+}
+
+sk_status sk_dft_naive(const double* re, const double* im, size_t n, double* out_re, double* out_im) {
+    if (!re || !im || !out_re || !out_im) return bad_arg("sk_dft_naive: null buffer");
+    return guarded([&] {
+        if (n == 0) throw std::invalid_argument("dft_naive: empty input");
+        std::vector<cd> x = join(re, im, n), tw(n);
+        for (size_t r = 0; r < n; ++r) {   // numerics.cpp:38-42
+            const double ang = -2.0 * M_PI * static_cast<double>(r) / static_cast<double>(n);
+            tw[r] = cd(std::cos(ang), std::sin(ang));
+        }
+        Stage s;
+        s.put(x.data(), n * sizeof(cd));
+        skg::DevMem dtw(n * sizeof(cd));
+        dtw.upload(tw.data(), n * sizeof(cd), s.st);
+        s.alloc_out(n * sizeof(cd));
+        skg::check(skg::launch_dft_naive(s.in.p, (long long)n, dtw.p, s.out.p, s.st), "dft_naive");
+        skg::count_launch();
+        s.get(x.data(), n * sizeof(cd));
+        split(x, out_re, out_im);
+    });
+}
+
+sk_status sk_czt(const double* re, const double* im, size_t n, double a_re, double a_im, double w_re, double w_im,
+                 size_t m, double* out_re, double* out_im) {
+    if (!re || !im || !out_re || !out_im) return bad_arg("sk_czt: null buffer");
+    return guarded([&] { split(czt_gpu(join(re, im, n), cd(a_re, a_im), cd(w_re, w_im), m), out_re, out_im); });
+}
+
+sk_status sk_czt_direct(const double* re, const double* im, size_t n, double a_re, double a_im, double w_re,
+                        double w_im, size_t m, double* out_re, double* out_im) {
+    if (!re || !im || !out_re || !out_im) return bad_arg("sk_czt_direct: null buffer");
+    return guarded([&] {
+        if (m == 0) throw std::invalid_argument("czt: m must be >= 1");
+        const cd a(a_re, a_im), w(w_re, w_im);
+        if (!(std::abs(a) > 0.0) || !(std::abs(w) > 0.0)) throw std::invalid_argument("czt: a and w must be nonzero");
+        if (n == 0) throw std::invalid_argument("czt_direct: empty input");
+        const skg::PolarPow A(a), W(w);
+        std::vector<cd> x = join(re, im, n);
+        Stage s;
+        s.put(x.data(), n * sizeof(cd));
+        skg::DevMem xa(n * sizeof(cd));
+        s.alloc_out(m * sizeof(cd));
+        skg::check(skg::launch_czt_direct(s.in.p, (long long)n, A.log_mag, A.q, W.log_mag, W.q, (long long)m, xa.p,
+                                          s.out.p, s.st),
+                   "czt_direct");
+        skg::count_launch(2);
+        std::vector<cd> y(m);
+        s.get(y.data(), m * sizeof(cd));
+        split(y, out_re, out_im);
+    });
+}
+
+sk_status sk_czt_params_for_band(double f1, double f2, double fs, size_t m, double* a_re, double* a_im,
+                                 double* w_re, double* w_im) {
+    if (!a_re || !a_im || !w_re || !w_im) return bad_arg("sk_czt_params_for_band: null output");
+    return guarded([&] {   // czt.cpp:42-56
+        if (!(fs > 0.0)) throw std::invalid_argument("czt_params_for_band: sample rate must be positive");
+        if (!(f1 >= 0.0) || !(f1 < f2)) throw std::invalid_argument("czt_params_for_band: need 0 <= f1 < f2");
+        if (f2 > fs * (1.0 + 1e-12)) throw std::invalid_argument("czt_params_for_band: f2 exceeds the sample rate");
+        if (m < 2) throw std::invalid_argument("czt_params_for_band: m must be >= 2");
+        const cd a = skg::cis_cycles(f1 / fs, 1.0);
+        const cd w = skg::cis_cycles(-(f2 - f1) / (static_cast<double>(m) * fs), 1.0);
+        *a_re = a.real();
+        *a_im = a.imag();
+        *w_re = w.real();
+        *w_im = w.imag();
+    });
+}
+
+size_t sk_next_pow2(size_t n) {
+    try {
+        return skg::next_pow2(n == 0 ? 1 : n);
+    } catch (...) {
+        return 0;
+    }
+}
+
+// ---- traces ------------------------------------------------------------------------------------
+sk_status sk_trace_create(const double* samples, size_t n, double fs, double t0, sk_trace** out) {
+    if (!samples || !out) return bad_arg("sk_trace_create: null argument");
+    return guarded([&] {
+        auto* t = new sk_trace;
+        t->samples.assign(samples, samples + n);
+        t->fs = fs;
+        t->t0 = t0;
+        try {
+            validate_trace(*t);
+        } catch (...) {
+            delete t;
+            throw;
+        }
+        *out = t;
+    });
+}
+void sk_trace_free(sk_trace* t) { delete t; }
+size_t sk_trace_size(const sk_trace* t) { return t ? t->samples.size() : 0; }
+double sk_trace_sample_rate(const sk_trace* t) { return t ? t->fs : 0.0; }
+double sk_trace_t0(const sk_trace* t) { return t ? t->t0 : 0.0; }
+const double* sk_trace_samples(const sk_trace* t) { return t ? t->samples.data() : nullptr; }
+
+// ---- spectra -----------------------------------------------------------------------------------
+sk_status sk_fft_spectrum(const sk_trace* t, size_t transform_len, sk_spectrum** out) {
+    if (!t || !out) return bad_arg("sk_fft_spectrum: null argument");
+    return guarded([&] { *out = fft_spectrum_gpu(*t, transform_len); });
+}
+
+sk_status sk_czt_spectrum(const sk_trace* t, double f1, double f2, size_t m, sk_spectrum** out) {
+    if (!t || !out) return bad_arg("sk_czt_spectrum: null argument");
+    return guarded([&] {   // czt.cpp:155-175
+        validate_trace(*t);
+        const double nyquist = t->fs / 2.0;
+        if (!(f1 >= 0.0) || !(f1 < f2)) throw std::invalid_argument("czt_spectrum: need 0 <= f1 < f2");
+        if (f2 > nyquist * (1.0 + 1e-12))
+            throw std::invalid_argument("czt_spectrum: band edge " + std::to_string(f2) +
+                                        " Hz exceeds the Nyquist rate " + std::to_string(nyquist) + " Hz");
+        double ar, ai, wr, wi;
+        if (sk_czt_params_for_band(f1, f2, t->fs, m, &ar, &ai, &wr, &wi) != SK_OK)
+            throw std::invalid_argument(g_err);
+        const size_t n = t->samples.size();
+        skg::CztPlanG plan(n, cd(ar, ai), cd(wr, wi), m);
+        Stage s;
+        s.put(t->samples.data(), n * sizeof(double));
+        s.alloc_out(m * sizeof(cd));
+        plan.execute(s.in.p, false, 0, 1, s.out.p, 0, false, s.st);
+        auto* sp = new sk_spectrum;
+        sp->bins.resize(m);
+        s.get(sp->bins.data(), m * sizeof(cd));
+        sp->f_start = f1;
+        sp->f_step = (f2 - f1) / static_cast<double>(m);
+        sp->source_n = n;
+        *out = sp;
+    });
+}
+
+sk_status sk_spectrum_create(const double* re, const double* im, size_t n, double f_start, double f_step,
+                             sk_spectrum** out) {
+    if (!re || !out) return bad_arg("sk_spectrum_create: null argument");
+    return guarded([&] {
+        if (n == 0) throw std::invalid_argument("sk_spectrum_create: empty spectrum");
+        if (!(f_step >= 0.0)) throw std::invalid_argument("sk_spectrum_create: negative step");
+        auto* s = new sk_spectrum;
+        s->bins = join(re, im, n);
+        s->f_start = f_start;
+        s->f_step = f_step;
+        s->source_n = n;
+        *out = s;
+    });
+}
+void sk_spectrum_free(sk_spectrum* s) { delete s; }
+size_t sk_spectrum_size(const sk_spectrum* s) { return s ? s->bins.size() : 0; }
+double sk_spectrum_f_start(const sk_spectrum* s) { return s ? s->f_start : 0.0; }
+double sk_spectrum_f_step(const sk_spectrum* s) { return s ? s->f_step : 0.0; }
+double sk_spectrum_frequency(const sk_spectrum* s, size_t k) {
+    return s ? s->f_start + static_cast<double>(k) * s->f_step : 0.0;
+}
+size_t sk_spectrum_source_n(const sk_spectrum* s) { return s ? s->source_n : 0; }
+
+sk_status sk_spectrum_bin(const sk_spectrum* s, size_t k, double* re, double* im) {
+    if (!s || !re || !im) return bad_arg("sk_spectrum_bin: null argument");
+    if (k >= s->bins.size()) return bad_arg("sk_spectrum_bin: index out of range");
+    *re = s->bins[k].real();
+    *im = s->bins[k].imag();
+    return SK_OK;
+}
+
+sk_status sk_spectrum_magnitude_db(const sk_spectrum* s, size_t k, double* out_db) {
+    if (!s || !out_db) return bad_arg("sk_spectrum_magnitude_db: null argument");
+    if (k >= s->bins.size()) return bad_arg("sk_spectrum_magnitude_db: index out of range");
+    const double mag = std::abs(s->bins[k]);   // types.cpp:13-18
+    *out_db = mag > 1e-15 ? 20.0 * std::log10(mag) : -300.0;
+    return SK_OK;
+}
+
+sk_status sk_spectrum_copy_data(const sk_spectrum* s, double* re, double* im) {
+    if (!s || !re || !im) return bad_arg("sk_spectrum_copy_data: null argument");
+    split(s->bins, re, im);
+    return SK_OK;
+}
+
+sk_status sk_spectrum_slice_band(const sk_spectrum* s, double f_lo, double f_hi, sk_spectrum** out) {
+    if (!s || !out) return bad_arg("sk_spectrum_slice_band: null argument");
+    return guarded([&] {   // spectra.cpp:40-61
+        if (s->bins.empty()) throw std::invalid_argument("slice_band: empty spectrum");
+        if (!(s->f_step > 0.0)) throw std::invalid_argument("slice_band: non-positive step");
+        if (!(f_lo <= f_hi)) throw std::invalid_argument("slice_band: inverted band");
+        const double eps = 0.5 * s->f_step * 1e-9;
+        const double lo = (f_lo - s->f_start) / s->f_step;
+        const double hi = (f_hi - s->f_start) / s->f_step;
+        const long k_lo = static_cast<long>(std::ceil(lo - eps));
+        const long k_hi = static_cast<long>(std::floor(hi + eps));
+        const long last = static_cast<long>(s->bins.size()) - 1;
+        const long a = std::max(k_lo, 0L), b = std::min(k_hi, last);
+        if (a > b) throw std::invalid_argument("slice_band: no bins fall inside the requested band");
+        auto* o = new sk_spectrum;
+        o->bins.assign(s->bins.begin() + a, s->bins.begin() + b + 1);
+        o->f_start = s->f_start + static_cast<double>(a) * s->f_step;
+        o->f_step = s->f_step;
+        o->source_n = s->source_n;
+        *out = o;
+    });
+}
+
+// ---- zoom --------------------------------------------------------------------------------------
+void sk_zoom_options_defaults(sk_zoom_options* o) {
+    if (!o) return;
+    o->center_hz = 0.0;
+    o->center_set = 0;
+    o->decimation = 0;
+    o->cutoff_hz = 0.0;
+    o->num_taps = 0;
+    o->circular = 1;
+    o->trim_transient = 0;
+    o->pad_pow2 = 1;
+}
+
+static skg::ZoomOptionsG to_opts(const sk_zoom_options* o) {
+    skg::ZoomOptionsG g;
+    if (o) {
+        g.center_hz = o->center_hz;
+        g.center_set = o->center_set != 0;
+        g.decimation = o->decimation;
+        g.cutoff_hz = o->cutoff_hz;
+        g.num_taps = o->num_taps;
+        g.circular = o->circular != 0;
+        g.trim_transient = o->trim_transient != 0;
+        g.pad_pow2 = o->pad_pow2 != 0;
+    }
+    return g;
+}
+
+sk_status sk_zoom_plan_create(size_t input_len, double f1, double f2, double fs, const sk_zoom_options* opts,
+                              sk_zoom_plan** out) {
+    if (!out) return bad_arg("sk_zoom_plan_create: null output");
+    return guarded([&] {
+        auto p = std::make_unique<skg::ZoomPlanG>(input_len, f1, f2, fs, to_opts(opts));
+        *out = new sk_zoom_plan{std::move(p)};
+    });
+}
+void sk_zoom_plan_free(sk_zoom_plan* p) { delete p; }
+size_t sk_zoom_plan_decimation(const sk_zoom_plan* p) { return p ? p->p->decimation : 0; }
+size_t sk_zoom_plan_n_fft(const sk_zoom_plan* p) { return p ? p->p->n_fft : 0; }
+size_t sk_zoom_plan_filter_len(const sk_zoom_plan* p) { return p ? p->p->filter_taps.size() : 0; }
+double sk_zoom_plan_f_step(const sk_zoom_plan* p) { return p ? p->p->f_step_hz() : 0.0; }
+
+sk_status sk_zoom_spectrum(const sk_zoom_plan* p, const sk_trace* t, sk_spectrum** out) {
+    if (!p || !t || !out) return bad_arg("sk_zoom_spectrum: null argument");
+    return guarded([&] {   // zoomfft.cpp:183-189 checks, then the fused kernel
+        validate_trace(*t);
+        const skg::ZoomPlanG& z = *p->p;
+        if (t->samples.size() != z.input_len)
+            throw std::invalid_argument("zoom_fft: trace length does not match the plan");
+        if (std::abs(t->fs - z.sample_rate_hz) > 1e-9 * z.sample_rate_hz)
+            throw std::invalid_argument("zoom_fft: trace sample rate does not match the plan");
+        if (z.k_lo > z.k_hi) throw std::invalid_argument("zoom_fft: no transform bins fall inside the band");
+        Stage s;
+        s.put(t->samples.data(), t->samples.size() * sizeof(double));
+        const size_t nb = z.bins();
+        s.alloc_out(nb * sizeof(cd));
+        z.execute(s.in.p, 0, 1, s.out.p, 0, false, s.st);
+        auto* sp = new sk_spectrum;
+        sp->bins.resize(nb);
+        s.get(sp->bins.data(), nb * sizeof(cd));
+        sp->f_start = z.f_start_hz();
+        sp->f_step = z.f_step_hz();
+        sp->source_n = z.n_fft;
+        *out = sp;
+    });
+}
+
+// ---- batched extension -------------------------------------------------------------------------
+sk_status skg_device_info(int* device, int* sm_count, size_t* smem_optin, size_t* l2_bytes) {
+    return guarded([&] {
+        skg::require_device();
+        const int d = skg::current_device();
+        cudaDeviceProp pr;
+        skg::check(cudaGetDeviceProperties(&pr, d), "cudaGetDeviceProperties");
+        if (device) *device = d;
+        if (sm_count) *sm_count = pr.multiProcessorCount;
+        if (smem_optin) *smem_optin = pr.sharedMemPerBlockOptin;
+        if (l2_bytes) *l2_bytes = pr.l2CacheSize;
+    });
+}
+
+uint64_t skg_launch_count(void) { return skg::launch_counter().load(); }
+
+sk_status skg_synchronize(void* stream) {
+    return guarded([&] { skg::check(cudaStreamSynchronize((cudaStream_t)stream), "cudaStreamSynchronize"); });
+}
+
+sk_status skg_fft_batch(size_t n, int inverse, int precision, const void* d_in, size_t in_stride, void* d_out,
+                        size_t out_stride, size_t batch, void* stream) {
+    if (!d_in || !d_out) return bad_arg("skg_fft_batch: null buffer");
+    return guarded([&] {
+        if (n == 0) throw std::invalid_argument("fft: empty input");
+        if (!skg::is_pow2(n))
+            throw std::invalid_argument("fft: length " + std::to_string(n) + " is not a power of two; zero_pad to " +
+                                        std::to_string(skg::next_pow2(n)) + " first");
+        skg::fft_c2c(n, inverse != 0, precision == SKG_F32, d_in, (long long)in_stride, d_out, (long long)out_stride,
+                     (long long)batch, (cudaStream_t)stream);
+    });
+}
+
+sk_status skg_fft_spectrum_batch(size_t n, size_t transform_len, int precision, int layout, const void* d_x,
+                                 size_t x_stride, size_t batch, void* d_out, size_t out_stride, void* stream) {
+    if (!d_x || !d_out) return bad_arg("skg_fft_spectrum_batch: null buffer");
+    return guarded([&] {
+        if (n == 0) throw std::invalid_argument("trace: no samples");
+        skg::fft_spectrum_batch(n, transform_len, precision == SKG_F32, layout, d_x, (long long)x_stride,
+                                (long long)batch, d_out, (long long)out_stride, (cudaStream_t)stream);
+    });
+}
+
+sk_status skg_czt_plan_create(size_t n, double a_re, double a_im, double w_re, double w_im, size_t m, int precision,
+                              skg_czt_plan** out) {
+    if (!out) return bad_arg("skg_czt_plan_create: null output");
+    return guarded([&] {
+        auto p = std::make_unique<skg::CztPlanG>(n, cd(a_re, a_im), cd(w_re, w_im), m);
+        *out = new skg_czt_plan{std::move(p), precision == SKG_F32};
+    });
+}
+void skg_czt_plan_free(skg_czt_plan* p) { delete p; }
+size_t skg_czt_plan_conv_size(const skg_czt_plan* p) { return p ? p->p->conv_size() : 0; }
+
+sk_status skg_czt_execute(const skg_czt_plan* p, const void* d_x, int x_complex, size_t x_stride, size_t batch,
+                          void* d_out, size_t out_stride, void* stream) {
+    if (!p || !d_x || !d_out) return bad_arg("skg_czt_execute: null argument");
+    return guarded([&] {
+        p->p->execute(d_x, x_complex != 0, (long long)x_stride, (long long)batch, d_out, (long long)out_stride, p->f32,
+                      (cudaStream_t)stream);
+    });
+}
+
+sk_status skg_transfer_plan_create(const double* ref, size_t n, size_t transform_len, int precision,
+                                   skg_transfer_plan** out) {
+    if (!ref || !out) return bad_arg("skg_transfer_plan_create: null argument");
+    return guarded([&] {
+        auto p = std::make_unique<skg::TransferPlanG>(ref, n, transform_len, precision == SKG_F32);
+        *out = new skg_transfer_plan{std::move(p)};
+    });
+}
+void skg_transfer_plan_free(skg_transfer_plan* p) { delete p; }
+size_t skg_transfer_plan_bins(const skg_transfer_plan* p) { return p ? p->p->bins() : 0; }
+sk_status skg_transfer_plan_reference(const skg_transfer_plan* p, double* xr) {
+    if (!p || !xr) return bad_arg("skg_transfer_plan_reference: null argument");
+    const auto& v = p->p->reference_spectrum();
+    std::memcpy(xr, v.data(), v.size() * sizeof(cd));
+    return SK_OK;
+}
+sk_status skg_transfer_execute(const skg_transfer_plan* p, const void* d_x, size_t x_stride, size_t batch,
+                               void* d_mag, void* d_phase, size_t mp_stride, void* d_h, size_t h_stride,
+                               void* stream) {
+    if (!p || !d_x || !d_mag || !d_phase) return bad_arg("skg_transfer_execute: null argument");
+    return guarded([&] {
+        p->p->execute(d_x, (long long)x_stride, (long long)batch, d_mag, d_phase, (long long)mp_stride, d_h,
+                      (long long)h_stride, (cudaStream_t)stream);
+    });
+}
+
+sk_status skg_zoom_plan_create(size_t input_len, double f1, double f2, double fs, const sk_zoom_options* opts,
+                               const skg_zoom_ext* ext, int precision, skg_zoom_plan** out) {
+    if (!out) return bad_arg("skg_zoom_plan_create: null output");
+    return guarded([&] {
+        auto p = std::make_unique<skg::ZoomPlanG>(input_len, f1, f2, fs, to_opts(opts), ext ? ext->n_fft : 0,
+                                                  ext ? ext->taps : nullptr, ext ? ext->num_taps : 0);
+        *out = new skg_zoom_plan{std::move(p), precision == SKG_F32};
+    });
+}
+void skg_zoom_plan_free(skg_zoom_plan* p) { delete p; }
+sk_status skg_zoom_plan_info(const skg_zoom_plan* p, size_t* bins, double* f_start, double* f_step, size_t* n_fft,
+                             size_t* decimation, size_t* num_taps) {
+    if (!p) return bad_arg("skg_zoom_plan_info: null plan");
+    const skg::ZoomPlanG& z = *p->p;
+    if (bins) *bins = z.k_hi >= z.k_lo ? z.bins() : 0;
+    if (f_start) *f_start = z.f_start_hz();
+    if (f_step) *f_step = z.f_step_hz();
+    if (n_fft) *n_fft = z.n_fft;
+    if (decimation) *decimation = z.decimation;
+    if (num_taps) *num_taps = z.filter_taps.size();
+    return SK_OK;
+}
+sk_status skg_zoom_execute(const skg_zoom_plan* p, const void* d_x, size_t x_stride, size_t batch, void* d_out,
+                           size_t out_stride, void* stream) {
+    if (!p || !d_x || !d_out) return bad_arg("skg_zoom_execute: null argument");
+    return guarded([&] {
+        p->p->execute(d_x, (long long)x_stride, (long long)batch, d_out, (long long)out_stride, p->f32,
+                      (cudaStream_t)stream);
+    });
+}
+
+}  // extern "C"

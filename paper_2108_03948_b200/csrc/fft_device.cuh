@@ -1,0 +1,268 @@
+// fft_device.cuh — in-register / shared-memory Stockham FFT engine for sm_100a.
+//
+// Replaces the reference's scalar radix-2 DIT loop (FftPlan::run, numerics.cpp:73-97) with a
+// batched, block-cooperative autosort (Stockham) FFT:
+//   * a transform of L = 2^LOG2L points is owned by NT = L/16 threads; thread `tid` always holds
+//     the 16 elements at positions tid + NT*q (q < 16) between passes, so the first pass reads
+//     global memory coalesced and the last pass leaves natural-order results in registers,
+//     ready for a coalesced store or a fused epilogue (CZT kernel product, H(f), ...);
+//   * radix-16 butterflies in registers (4x4 split, constant twiddles folded); the last pass
+//     takes the leftover radix 2/4/8; between passes one shared-memory exchange through a
+//     padded layout (one pad slot per 16 elements) that keeps the strided first-pass writes
+//     conflict-free;
+//   * per-pass twiddles W_{pR}^{jk} come from an fp64-accurate table built on the host with the
+//     reference's exact phase reduction (cis_cycles, numerics.cpp:122-128); fp32 tables are
+//     rounded from fp64, never computed in fp32;
+//   * the first pass can skip known-zero inputs (zero padding is synthesised, never loaded) and
+//     the last pass can skip unneeded outputs (the CZT keeps only m of L bins).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace skg {
+
+template <typename T> struct CxT;
+template <> struct CxT<double> { using type = double2; };
+template <> struct CxT<float> { using type = float2; };
+template <typename T> using cx_t = typename CxT<T>::type;
+
+template <typename C> struct Scalar;
+template <> struct Scalar<double2> { using type = double; };
+template <> struct Scalar<float2> { using type = float; };
+template <typename C> using sc_t = typename Scalar<C>::type;
+
+template <typename C> __device__ __forceinline__ C mk(sc_t<C> a, sc_t<C> b) {
+    C r;
+    r.x = a;
+    r.y = b;
+    return r;
+}
+template <typename C> __device__ __forceinline__ C czero() { return mk<C>(0, 0); }
+template <typename C> __device__ __forceinline__ C cadd(C a, C b) { return mk<C>(a.x + b.x, a.y + b.y); }
+template <typename C> __device__ __forceinline__ C csub(C a, C b) { return mk<C>(a.x - b.x, a.y - b.y); }
+template <typename C> __device__ __forceinline__ C cmul(C a, C b) {
+    return mk<C>(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a * conj(b)
+template <typename C> __device__ __forceinline__ C cmulc(C a, C b) {
+    return mk<C>(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+template <typename C> __device__ __forceinline__ C cconj(C a) { return mk<C>(a.x, -a.y); }
+template <typename C> __device__ __forceinline__ C cscale(C a, sc_t<C> s) { return mk<C>(a.x * s, a.y * s); }
+// real * complex
+template <typename C> __device__ __forceinline__ C rmul(sc_t<C> r, C a) { return mk<C>(r * a.x, r * a.y); }
+// twiddle multiply: forward uses w, inverse uses conj(w)
+template <bool INV, typename C> __device__ __forceinline__ C twmul(C a, C w) {
+    return INV ? cmulc(a, w) : cmul(a, w);
+}
+// multiply by W4 = -i (forward) / +i (inverse)
+template <bool INV, typename C> __device__ __forceinline__ C mul_w4(C a) {
+    return INV ? mk<C>(-a.y, a.x) : mk<C>(a.y, -a.x);
+}
+// multiply by W8^1 = (1 -/+ i)/sqrt2
+template <bool INV, typename C> __device__ __forceinline__ C mul_w8(C a) {
+    const sc_t<C> r = (sc_t<C>)0.70710678118654752440;
+    return INV ? mk<C>((a.x - a.y) * r, (a.x + a.y) * r) : mk<C>((a.x + a.y) * r, (a.y - a.x) * r);
+}
+// multiply by W8^3 = (-1 -/+ i)/sqrt2
+template <bool INV, typename C> __device__ __forceinline__ C mul_w8_3(C a) {
+    const sc_t<C> r = (sc_t<C>)0.70710678118654752440;
+    return INV ? mk<C>(-(a.x + a.y) * r, (a.x - a.y) * r) : mk<C>((a.y - a.x) * r, -(a.x + a.y) * r);
+}
+// multiply by exp(-/+ i theta) given c = cos theta, s = sin theta
+template <bool INV, typename C> __device__ __forceinline__ C mul_cs(C a, sc_t<C> c, sc_t<C> s) {
+    return INV ? mk<C>(a.x * c - a.y * s, a.y * c + a.x * s) : mk<C>(a.x * c + a.y * s, a.y * c - a.x * s);
+}
+
+// ---- small DFTs, natural order in and out.
+// NZ = number of leading inputs that may be nonzero, NO = number of leading outputs needed.
+template <bool INV, int NZ = 4, int NO = 4, typename C>
+__device__ __forceinline__ void dft4(C& a0, C& a1, C& a2, C& a3) {
+    if constexpr (NZ <= 0) {
+        a0 = czero<C>(); a1 = a0; a2 = a0; a3 = a0;
+    } else if constexpr (NZ == 1) {
+        a1 = a0; a2 = a0; a3 = a0;
+    } else if constexpr (NZ == 2) {
+        const C b = mul_w4<INV>(a1);
+        const C x0 = cadd(a0, a1), x2 = csub(a0, a1), x1 = cadd(a0, b), x3 = csub(a0, b);
+        a0 = x0; a1 = x1; a2 = x2; a3 = x3;
+    } else {
+        const C t0 = cadd(a0, a2), t1 = csub(a0, a2);
+        const C t2 = cadd(a1, a3), t3 = mul_w4<INV>(csub(a1, a3));
+        a0 = cadd(t0, t2);
+        if constexpr (NO > 1) a1 = cadd(t1, t3);
+        if constexpr (NO > 2) a2 = csub(t0, t2);
+        if constexpr (NO > 3) a3 = csub(t1, t3);
+    }
+}
+
+template <bool INV, typename C> __device__ __forceinline__ void dft2(C& a0, C& a1) {
+    const C t = a0;
+    a0 = cadd(t, a1);
+    a1 = csub(t, a1);
+}
+
+template <bool INV, typename C> __device__ __forceinline__ void dft8(C (&a)[8]) {
+    dft4<INV>(a[0], a[2], a[4], a[6]);
+    dft4<INV>(a[1], a[3], a[5], a[7]);
+    // now a[2k] = E_k, a[2k+1] = O_k
+    const C o1 = mul_w8<INV>(a[3]), o2 = mul_w4<INV>(a[5]), o3 = mul_w8_3<INV>(a[7]);
+    const C e0 = a[0], e1 = a[2], e2 = a[4], e3 = a[6], o0 = a[1];
+    a[0] = cadd(e0, o0); a[4] = csub(e0, o0);
+    a[1] = cadd(e1, o1); a[5] = csub(e1, o1);
+    a[2] = cadd(e2, o2); a[6] = csub(e2, o2);
+    a[3] = cadd(e3, o3); a[7] = csub(e3, o3);
+}
+
+// 16-point DFT as 4x4 (n = n2 + 4 n1, k = k1 + 4 k2); NZ in {1,2,4,8,16}, NO in {4,8,16}.
+template <bool INV, int NZ = 16, int NO = 16, typename C> __device__ __forceinline__ void dft16(C (&a)[16]) {
+    constexpr sc_t<C> C1 = (sc_t<C>)0.92387953251128675613;  // cos(pi/8)
+    constexpr sc_t<C> S1 = (sc_t<C>)0.38268343236508977173;  // sin(pi/8)
+    // stage 1: column n2 holds a[n2 + 4 n1]
+    constexpr int nz0 = NZ >= 13 ? 4 : NZ >= 9 ? 3 : NZ >= 5 ? 2 : NZ >= 1 ? 1 : 0;
+    constexpr int nz1 = NZ >= 14 ? 4 : NZ >= 10 ? 3 : NZ >= 6 ? 2 : NZ >= 2 ? 1 : 0;
+    constexpr int nz2 = NZ >= 15 ? 4 : NZ >= 11 ? 3 : NZ >= 7 ? 2 : NZ >= 3 ? 1 : 0;
+    constexpr int nz3 = NZ >= 16 ? 4 : NZ >= 12 ? 3 : NZ >= 8 ? 2 : NZ >= 4 ? 1 : 0;
+    constexpr int rows = NZ >= 4 ? 4 : NZ;   // nonzero rows entering stage 2
+    dft4<INV, (nz0 == 3 ? 4 : nz0)>(a[0], a[4], a[8], a[12]);
+    if constexpr (rows > 1) dft4<INV, (nz1 == 3 ? 4 : nz1)>(a[1], a[5], a[9], a[13]);
+    if constexpr (rows > 2) dft4<INV, (nz2 == 3 ? 4 : nz2)>(a[2], a[6], a[10], a[14]);
+    if constexpr (rows > 3) dft4<INV, (nz3 == 3 ? 4 : nz3)>(a[3], a[7], a[11], a[15]);
+    // twiddles W16^{n2 k1}: element a[n2 + 4 k1]
+    if constexpr (rows > 1) {
+        a[5] = mul_cs<INV>(a[5], C1, S1);      // n2=1,k1=1: W16^1
+        a[9] = mul_w8<INV>(a[9]);              // n2=1,k1=2: W16^2
+        a[13] = mul_cs<INV>(a[13], S1, C1);    // n2=1,k1=3: W16^3
+    }
+    if constexpr (rows > 2) {
+        a[6] = mul_w8<INV>(a[6]);              // W16^2
+        a[10] = mul_w4<INV>(a[10]);            // W16^4
+        a[14] = mul_w8_3<INV>(a[14]);          // W16^6
+    }
+    if constexpr (rows > 3) {
+        a[7] = mul_cs<INV>(a[7], S1, C1);      // W16^3
+        a[11] = mul_w8_3<INV>(a[11]);          // W16^6
+        a[15] = mul_cs<INV>(a[15], -C1, -S1);  // W16^9
+    }
+    // stage 2: for each k1, DFT4 over n2 of a[4 k1 + n2] -> X[k1 + 4 k2] lands in a[4 k1 + k2]
+    constexpr int no4 = NO / 4;
+    dft4<INV, rows, no4>(a[0], a[1], a[2], a[3]);
+    dft4<INV, rows, no4>(a[4], a[5], a[6], a[7]);
+    dft4<INV, rows, no4>(a[8], a[9], a[10], a[11]);
+    dft4<INV, rows, no4>(a[12], a[13], a[14], a[15]);
+    // transpose 4x4 so a[k] = X[k]  (pure register renaming)
+    C t[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) t[i] = a[i];
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) a[k1 + 4 * k2] = t[4 * k1 + k2];
+}
+
+template <int R, bool INV, int NZ, int NO, typename C> __device__ __forceinline__ void dft_r(C (&u)[R]) {
+    if constexpr (R == 1) {
+    } else if constexpr (R == 2) {
+        dft2<INV>(u[0], u[1]);
+    } else if constexpr (R == 4) {
+        dft4<INV>(u[0], u[1], u[2], u[3]);
+    } else if constexpr (R == 8) {
+        dft8<INV>(u);
+    } else {
+        static_assert(R == 16, "radix");
+        dft16<INV, NZ, NO>(u);
+    }
+}
+
+// ---- geometry of an L = 2^LOG2L transform ------------------------------------------------
+template <int LOG2L> struct FftGeom {
+    static constexpr int L = 1 << LOG2L;
+    static constexpr int EPT = L < 16 ? L : 16;        // elements per thread
+    static constexpr int NT = L / EPT;                  // threads per transform
+    static constexpr int P = L < 16 ? 1 : (LOG2L + 3) / 4;   // passes
+    static constexpr int RLAST = L < 16 ? L : (1 << (LOG2L - 4 * (P - 1)));
+    static constexpr int SMEM = L < 16 ? 0 : L + (L >> 4);   // padded elements per transform
+    __host__ __device__ static constexpr int radix(int s) { return L < 16 ? L : (s < P - 1 ? 16 : RLAST); }
+    __host__ __device__ static constexpr int pval(int s) { return 1 << (4 * s); }
+    __host__ __device__ static constexpr int tw_off(int s) {
+        int o = 0;
+        for (int t = 1; t < s; ++t) o += (radix(t) - 1) * pval(t);
+        return o;
+    }
+    static constexpr int TW_SIZE = tw_off(P);   // twiddle entries (pass 0 needs none)
+};
+
+__device__ __forceinline__ int pad16(int a) { return a + (a >> 4); }
+
+template <typename C> __device__ __forceinline__ C ldg_c(const C* p) {
+#ifdef SKG_PLAIN_LD
+    return *p;
+#else
+    return __ldg(p);
+#endif
+}
+
+// One Stockham pass. v[q] holds position tid + NT*q on entry and exit.
+template <bool INV, int S, int NZ, int NO, int LOG2L, typename C>
+__device__ __forceinline__ void stockham_pass(C (&v)[FftGeom<LOG2L>::EPT], C* sm, const C* __restrict__ tw,
+                                              int tid, bool active = true) {
+    using G = FftGeom<LOG2L>;
+    constexpr int R = G::radix(S);
+    constexpr int p = G::pval(S);
+    constexpr int B = G::EPT / R;
+    constexpr bool last = (S == G::P - 1);
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+        C u[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) u[j] = v[b + B * j];
+        const int i = tid + G::NT * b;
+        const int k = i & (p - 1);
+        if constexpr (p > 1) {
+            const C* t = tw + G::tw_off(S) + k;
+#pragma unroll
+            for (int j = 1; j < R; ++j) u[j] = twmul<INV>(u[j], ldg_c(t + (j - 1) * p));
+        }
+        dft_r<R, INV, (S == 0 ? NZ : 16), (last ? NO : 16)>(u);
+        if constexpr (last) {
+#pragma unroll
+            for (int j = 0; j < R; ++j) v[b + B * j] = u[j];
+        } else {
+            const int base = (i / p) * p * R + k;
+            if (active) {
+#pragma unroll
+                for (int j = 0; j < R; ++j) sm[pad16(base + j * p)] = u[j];
+            }
+        }
+    }
+    if constexpr (!last) {
+        __syncthreads();
+        if (active) {
+#pragma unroll
+            for (int q = 0; q < G::EPT; ++q) v[q] = sm[pad16(tid + G::NT * q)];
+        }
+        __syncthreads();
+    }
+}
+
+// Full transform: NZ = leading nonzero inputs of the first radix-16 pass (1..16),
+// NO = leading outputs needed from the last radix-16 pass (4, 8 or 16).
+template <bool INV, int LOG2L, int NZ = 16, int NO = 16, typename C>
+__device__ __forceinline__ void block_fft(C (&v)[FftGeom<LOG2L>::EPT], C* sm, const C* __restrict__ tw, int tid,
+                                          bool active = true) {
+    using G = FftGeom<LOG2L>;
+    if constexpr (G::L < 16) {
+        dft_r<G::L, INV, 16, 16>(v);
+    } else {
+        constexpr int nz = G::radix(0) == 16 ? NZ : 16;
+        constexpr int no = G::radix(G::P - 1) == 16 ? NO : 16;
+        stockham_pass<INV, 0, nz, (G::P == 1 ? no : 16), LOG2L>(v, sm, tw, tid, active);
+        if constexpr (G::P > 1) stockham_pass<INV, 1, 16, (G::P == 2 ? no : 16), LOG2L>(v, sm, tw, tid, active);
+        if constexpr (G::P > 2) stockham_pass<INV, 2, 16, (G::P == 3 ? no : 16), LOG2L>(v, sm, tw, tid, active);
+        if constexpr (G::P > 3) stockham_pass<INV, 3, 16, (G::P == 4 ? no : 16), LOG2L>(v, sm, tw, tid, active);
+        static_assert(G::P <= 4, "single-CTA engine handles L <= 65536");
+    }
+}
+
+}  // namespace skg

@@ -1,0 +1,421 @@
+// host.cpp — runtime, table builders and plan objects of the B200 spectral library.
+#include "host.hpp"
+
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <numbers>
+
+#include "fft_device.cuh"
+
+namespace skg {
+
+// ---- errors / device -----------------------------------------------------------------------
+void check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        cudaGetLastError();   // clear sticky-free errors so the next call can proceed
+        throw CudaError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+    }
+}
+
+void require_device() {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        throw CudaError(std::string("no CUDA device available (") +
+                        (e == cudaSuccess ? "0 devices" : cudaGetErrorString(e)) +
+                        "); the B200 spectral library has no CPU fallback");
+    }
+}
+
+int current_device() {
+    int d = 0;
+    check(cudaGetDevice(&d), "cudaGetDevice");
+    return d;
+}
+
+std::atomic<uint64_t>& launch_counter() {
+    static std::atomic<uint64_t> c{0};
+    return c;
+}
+
+// ---- numerics ---------------------------------------------------------------------------------
+bool is_pow2(size_t n) { return n != 0 && (n & (n - 1)) == 0; }
+
+size_t next_pow2(size_t n) {
+    if (n == 0) throw std::invalid_argument("next_pow2: n must be >= 1");
+    size_t p = 1;
+    while (p < n) {
+        if (p > (size_t{1} << 62)) throw std::invalid_argument("next_pow2: overflow");
+        p <<= 1;
+    }
+    return p;
+}
+
+int ilog2(size_t n) {
+    int l = 0;
+    while ((size_t{1} << l) < n) ++l;
+    return l;
+}
+
+// exp(i 2 pi q t) with q*t reduced by an fma split (numerics.cpp:122-128)
+cd cis_cycles(double q, double t) {
+    const double hi = q * t;
+    const double lo = std::fma(q, t, -hi);
+    const double frac = (hi - std::nearbyint(hi)) + lo;
+    const double ang = 2.0 * std::numbers::pi * frac;
+    return {std::cos(ang), std::sin(ang)};
+}
+
+PolarPow::PolarPow(cd z) {
+    const double mag = std::abs(z);
+    if (!(mag > 0.0)) throw std::invalid_argument("czt: parameter magnitude is zero");
+    log_mag = std::log(mag);
+    if (std::abs(log_mag) < 1e-14) log_mag = 0.0;
+    q = std::arg(z) / (2.0 * std::numbers::pi);
+}
+
+cd PolarPow::pow(double t) const {
+    cd u = cis_cycles(q, t);
+    if (log_mag != 0.0) u *= std::exp(log_mag * t);
+    return u;
+}
+
+std::vector<double> design_lowpass(double cutoff_hz, double fs, size_t num_taps) {
+    if (!(fs > 0.0)) throw std::invalid_argument("design_lowpass: sample rate must be positive");
+    if (!(cutoff_hz > 0.0) || cutoff_hz > fs / 2.0)
+        throw std::invalid_argument("design_lowpass: cutoff must lie in (0, fs/2]");
+    if (num_taps == 0 || num_taps % 2 == 0)
+        throw std::invalid_argument("design_lowpass: tap count must be odd");
+    if (num_taps == 1) return {1.0};
+    const double fc = cutoff_hz / fs;
+    const size_t mid = (num_taps - 1) / 2;
+    std::vector<double> taps(num_taps);
+    double sum = 0.0;
+    for (size_t t = 0; t < num_taps; ++t) {
+        const double k = static_cast<double>(t) - static_cast<double>(mid);
+        const double arg = 2.0 * fc * k;
+        const double sinc = k != 0.0 ? std::sin(std::numbers::pi * arg) / (std::numbers::pi * arg) : 1.0;
+        const double win = 0.54 - 0.46 * std::cos(2.0 * std::numbers::pi * static_cast<double>(t) /
+                                                   static_cast<double>(num_taps - 1));
+        taps[t] = 2.0 * fc * sinc * win;
+        sum += taps[t];
+    }
+    for (double& v : taps) v /= sum;
+    return taps;
+}
+
+// ---- device memory ----------------------------------------------------------------------------
+DevMem::DevMem(size_t n) : bytes(n) {
+    if (n) check(cudaMalloc(&p, n), "cudaMalloc");
+}
+DevMem& DevMem::operator=(DevMem&& o) noexcept {
+    if (this != &o) {
+        if (p) cudaFree(p);
+        p = o.p;
+        bytes = o.bytes;
+        o.p = nullptr;
+        o.bytes = 0;
+    }
+    return *this;
+}
+DevMem::~DevMem() {
+    if (p) cudaFree(p);
+}
+void DevMem::upload(const void* host, size_t n, cudaStream_t st) {
+    check(cudaMemcpyAsync(p, host, n, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync H2D");
+    check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+}
+
+DevMem to_device(const std::vector<cd>& h, bool f32) {
+    if (!f32) {
+        DevMem d(h.size() * sizeof(cd));
+        d.upload(h.data(), d.bytes);
+        return d;
+    }
+    std::vector<float> f(2 * h.size());
+    for (size_t i = 0; i < h.size(); ++i) {
+        f[2 * i] = static_cast<float>(h[i].real());
+        f[2 * i + 1] = static_cast<float>(h[i].imag());
+    }
+    DevMem d(f.size() * sizeof(float));
+    d.upload(f.data(), d.bytes);
+    return d;
+}
+
+namespace {
+std::mutex g_tab_mu;
+std::map<std::tuple<int, int, int, int>, DevMem>& tab_cache() {
+    static std::map<std::tuple<int, int, int, int>, DevMem> m;
+    return m;
+}
+
+template <int LG> void stockham_host(std::vector<cd>& out) {
+    using G = FftGeom<LG>;
+    out.assign(G::TW_SIZE > 0 ? G::TW_SIZE : 1, cd(1.0, 0.0));
+    if constexpr (G::L >= 16) {
+        for (int s = 1; s < G::P; ++s) {
+            const int R = G::radix(s), p = G::pval(s);
+            const double q = -1.0 / (static_cast<double>(p) * R);   // exact power of two
+            for (int j = 1; j < R; ++j)
+                for (int k = 0; k < p; ++k)
+                    out[G::tw_off(s) + (j - 1) * p + k] = cis_cycles(q, static_cast<double>(j * k));
+        }
+    }
+}
+
+template <int LO, int HI> void stockham_dispatch(int lg, std::vector<cd>& out) {
+    if constexpr (LO <= HI) {
+        if (lg == LO) return stockham_host<LO>(out);
+        stockham_dispatch<LO + 1, HI>(lg, out);
+    }
+}
+
+const void* cached(int kind, int a, int b, bool f32, const std::function<std::vector<cd>()>& build) {
+    std::lock_guard<std::mutex> lk(g_tab_mu);
+    const auto key = std::make_tuple(current_device(), kind * 4096 + a * 64 + b, f32 ? 1 : 0, 0);
+    auto it = tab_cache().find(key);
+    if (it != tab_cache().end()) return it->second.p;
+    DevMem d = to_device(build(), f32);
+    const void* p = d.p;
+    tab_cache().emplace(key, std::move(d));
+    return p;
+}
+}  // namespace
+
+int single_cta_max_log2(bool f32) { return f32 ? kMaxLog2F32 : kMaxLog2F64; }
+
+const void* stockham_twiddles(int log2L, bool f32) {
+    require_device();
+    return cached(1, log2L, 0, f32, [&] {
+        std::vector<cd> v;
+        stockham_dispatch<0, kMaxLog2F32>(log2L, v);
+        return v;
+    });
+}
+
+const void* r2c_post_twiddles(int log2M, bool f32) {
+    require_device();
+    return cached(2, log2M, 0, f32, [&] {
+        const size_t M = size_t{1} << log2M;
+        std::vector<cd> v(M);
+        const double q = -1.0 / (2.0 * static_cast<double>(M));
+        for (size_t k = 0; k < M; ++k) v[k] = cis_cycles(q, static_cast<double>(k));
+        return v;
+    });
+}
+
+const void* fourstep_twiddles(int log2R, int log2C, bool f32) {
+    require_device();
+    return cached(3, log2R, log2C, f32, [&] {
+        const size_t R = size_t{1} << log2R, C = size_t{1} << log2C;
+        std::vector<cd> v(R * C);
+        const double q = -1.0 / static_cast<double>(R * C);
+        for (size_t r = 0; r < R; ++r)
+            for (size_t c = 0; c < C; ++c) v[r * C + c] = cis_cycles(q, static_cast<double>(r * c));
+        return v;
+    });
+}
+
+// ---- transforms -------------------------------------------------------------------------------
+void fft_c2c(size_t n, bool inverse, bool f32, const void* in, long long in_stride, void* out,
+             long long out_stride, long long batch, cudaStream_t st) {
+    if (batch <= 0) return;
+    const int lg = ilog2(n);
+    if (lg > single_cta_max_log2(f32))
+        throw std::invalid_argument("fft: length " + std::to_string(n) + " exceeds the supported maximum");
+    const void* tw = stockham_twiddles(lg, f32);
+    cudaError_t e;
+    if (f32)
+        e = launch_fft_c2c<float>(lg, inverse, in, in_stride, out, out_stride, batch, tw,
+                                  inverse ? 1.0f / static_cast<float>(n) : 1.0f, st);
+    else
+        e = launch_fft_c2c<double>(lg, inverse, in, in_stride, out, out_stride, batch, tw,
+                                   inverse ? 1.0 / static_cast<double>(n) : 1.0, st);
+    check(e, "fft_c2c launch");
+    count_launch();
+}
+
+// ---- CZT ---------------------------------------------------------------------------------------
+CztPlanG::CztPlanG(size_t n, cd a, cd w, size_t m) : n_(n), m_(m) {
+    // czt.cpp:36-40, 78-82
+    if (m == 0) throw std::invalid_argument("czt: m must be >= 1");
+    if (!(std::abs(a) > 0.0) || !(std::abs(w) > 0.0))
+        throw std::invalid_argument("czt: a and w must be nonzero");
+    if (n == 0) throw std::invalid_argument("CztPlan: empty input length");
+    L_ = next_pow2(n + m - 1);
+    log2L_ = ilog2(L_);
+    const PolarPow A(a), W(w);
+    // czt.cpp:90-112 — same table formulas, fp64
+    cin_.resize(n);
+    for (size_t i = 0; i < n; ++i) {
+        const double t = static_cast<double>(i);
+        cin_[i] = A.pow(-t) * W.pow(0.5 * t * t);
+    }
+    cout_.resize(m);
+    for (size_t k = 0; k < m; ++k) {
+        const double t = static_cast<double>(k);
+        cout_[k] = W.pow(0.5 * t * t);
+    }
+    kern_.assign(L_, cd(0.0, 0.0));
+    for (size_t k = 0; k < m; ++k) {
+        const double t = static_cast<double>(k);
+        kern_[k] = W.pow(-0.5 * t * t);
+    }
+    for (size_t i = 1; i < n; ++i) {
+        const double t = static_cast<double>(i);
+        kern_[L_ - i] = W.pow(-0.5 * t * t);
+    }
+    if (log2L_ > single_cta_max_log2(false) + 7)
+        throw std::invalid_argument("czt: convolution length " + std::to_string(L_) + " exceeds the supported maximum");
+}
+
+const CztPlanG::Dev& CztPlanG::dev(bool f32) const {
+    std::call_once(once_[f32 ? 1 : 0], [&] {
+        require_device();
+        Dev& d = dev_[f32 ? 1 : 0];
+        d.cin = to_device(cin_, f32);
+        d.cout = to_device(cout_, f32);
+        // kernel spectrum: forward FFT of the circular chirp on the GPU in fp64, scaled by 1/L so the
+        // inverse transform of the fused kernel needs no extra pass (czt.cpp:113, numerics.cpp:93-96)
+        DevMem k64 = to_device(kern_, false);
+        fft_c2c(L_, false, false, k64.p, 0, k64.p, 0, 1, nullptr);
+        check(launch_scale_c64(k64.p, (long long)L_, 1.0 / static_cast<double>(L_), nullptr), "scale");
+        count_launch();
+        if (f32) {
+            DevMem k32(L_ * 2 * sizeof(float));
+            check(launch_c64_to_c32(k64.p, k32.p, (long long)L_, nullptr), "convert");
+            count_launch();
+            d.khat = std::move(k32);
+        } else {
+            d.khat = std::move(k64);
+        }
+        check(cudaStreamSynchronize(nullptr), "czt plan upload");
+    });
+    return dev_[f32 ? 1 : 0];
+}
+
+void CztPlanG::execute(const void* x, bool complex_in, long long x_stride, long long batch, void* out,
+                       long long out_stride, bool f32, cudaStream_t st, size_t load_n) const {
+    if (batch <= 0) return;
+    const Dev& d = dev(f32);
+    const long long N = static_cast<long long>(load_n ? std::min(load_n, n_) : n_);
+    if (log2L_ > single_cta_max_log2(f32))
+        throw std::invalid_argument("czt: convolution length " + std::to_string(L_) +
+                                    " needs the multi-pass path (not available in this build)");
+    const void* tw = stockham_twiddles(log2L_, f32);
+    cudaError_t e;
+    if (f32)
+        e = launch_czt<float>(log2L_, N, (long long)m_, complex_in, x, x_stride, batch, out, out_stride, tw,
+                              d.cin.p, d.khat.p, d.cout.p, st);
+    else
+        e = launch_czt<double>(log2L_, N, (long long)m_, complex_in, x, x_stride, batch, out, out_stride, tw,
+                               d.cin.p, d.khat.p, d.cout.p, st);
+    check(e, "czt launch");
+    count_launch();
+}
+
+// ---- FFT spectrum -------------------------------------------------------------------------------
+namespace {
+std::mutex g_bluestein_mu;
+std::map<size_t, std::unique_ptr<CztPlanG>>& bluestein_cache() {
+    static std::map<size_t, std::unique_ptr<CztPlanG>> m;
+    return m;
+}
+}  // namespace
+
+// dft_any's chirp route for a non-power-of-two length (czt.cpp:144-153)
+static const CztPlanG& bluestein_plan(size_t len) {
+    std::lock_guard<std::mutex> lk(g_bluestein_mu);
+    auto& m = bluestein_cache();
+    auto it = m.find(len);
+    if (it == m.end())
+        it = m.emplace(len, std::make_unique<CztPlanG>(len, cd(1.0, 0.0),
+                                                       cis_cycles(-1.0 / static_cast<double>(len), 1.0), len))
+                 .first;
+    return *it->second;
+}
+
+void fft_spectrum_batch(size_t n, size_t len, bool f32, int layout, const void* x, long long x_stride,
+                        long long batch, void* out, long long out_stride, cudaStream_t st) {
+    if (len == 0) len = next_pow2(n);
+    if (len < n) throw std::invalid_argument("fft_spectrum: transform length shorter than the trace");
+    if (batch <= 0) return;
+    if (!is_pow2(len)) {
+        if (layout != 0) throw std::invalid_argument("fft_spectrum: half layout needs a power-of-two length");
+        bluestein_plan(len).execute(x, false, x_stride, batch, out, out_stride, f32, st, n);
+        return;
+    }
+    if (len == 1) {
+        // one bin: X[0] = x[0]
+        const size_t es = f32 ? sizeof(float) : sizeof(double);
+        check(cudaMemset2DAsync(out, out_stride * 2 * es, 0, 2 * es, batch, st), "memset");
+        check(cudaMemcpy2DAsync(out, out_stride * 2 * es, x, x_stride * es, es, batch, cudaMemcpyDeviceToDevice, st),
+              "copy");
+        return;
+    }
+    const int lgM = ilog2(len) - 1;
+    if (lgM > single_cta_max_log2(f32))
+        throw std::invalid_argument("fft_spectrum: length " + std::to_string(len) +
+                                    " needs the multi-pass path (not available in this build)");
+    const void* tw = stockham_twiddles(lgM, f32);
+    const void* post = r2c_post_twiddles(lgM, f32);
+    cudaError_t e;
+    if (f32)
+        e = launch_fft_r2c<float>(lgM, (long long)n, (const float*)x, x_stride, batch, tw, post, layout, out,
+                                  out_stride, nullptr, nullptr, nullptr, 0, st);
+    else
+        e = launch_fft_r2c<double>(lgM, (long long)n, (const double*)x, x_stride, batch, tw, post, layout, out,
+                                   out_stride, nullptr, nullptr, nullptr, 0, st);
+    check(e, "fft_spectrum launch");
+    count_launch();
+}
+
+// ---- transfer function ---------------------------------------------------------------------------
+TransferPlanG::TransferPlanG(const double* ref, size_t n, size_t len, bool f32) : n_(n), f32_(f32) {
+    if (n == 0) throw std::invalid_argument("transfer: empty reference trace");
+    for (size_t i = 0; i < n; ++i)
+        if (!std::isfinite(ref[i])) throw std::invalid_argument("trace: non-finite sample");
+    len_ = len == 0 ? next_pow2(n) : len;
+    if (len_ < n) throw std::invalid_argument("fft_spectrum: transform length shorter than the trace");
+    if (!is_pow2(len_) || len_ < 2)
+        throw std::invalid_argument("transfer: transform length must be a power of two >= 2");
+    require_device();
+    // X_ref on the GPU in fp64 (the fused epilogue multiplies by 1/X_ref)
+    DevMem dref(n * sizeof(double));
+    dref.upload(ref, n * sizeof(double));
+    DevMem dx(bins() * sizeof(cd));
+    fft_spectrum_batch(n, len_, false, 1, dref.p, 0, 1, dx.p, 0, nullptr);
+    xref_.resize(bins());
+    check(cudaMemcpy(xref_.data(), dx.p, bins() * sizeof(cd), cudaMemcpyDeviceToHost), "D2H");
+    std::vector<cd> r(bins());
+    for (size_t k = 0; k < bins(); ++k) {
+        const cd v = xref_[k];
+        const double den = v.real() * v.real() + v.imag() * v.imag();
+        r[k] = den > 0.0 ? cd(v.real() / den, -v.imag() / den) : cd(0.0, 0.0);
+    }
+    rtab_ = to_device(r, f32);
+}
+
+void TransferPlanG::execute(const void* x, long long x_stride, long long batch, void* mag, void* phase,
+                            long long mp_stride, void* h, long long h_stride, cudaStream_t st) const {
+    if (batch <= 0) return;
+    const int lgM = ilog2(len_) - 1;
+    if (lgM > single_cta_max_log2(f32_))
+        throw std::invalid_argument("transfer: length needs the multi-pass path (not available in this build)");
+    const void* tw = stockham_twiddles(lgM, f32_);
+    const void* post = r2c_post_twiddles(lgM, f32_);
+    cudaError_t e;
+    if (f32_)
+        e = launch_fft_r2c<float>(lgM, (long long)n_, (const float*)x, x_stride, batch, tw, post, 2, h, h_stride,
+                                  rtab_.p, (float*)mag, (float*)phase, mp_stride, st);
+    else
+        e = launch_fft_r2c<double>(lgM, (long long)n_, (const double*)x, x_stride, batch, tw, post, 2, h, h_stride,
+                                   rtab_.p, (double*)mag, (double*)phase, mp_stride, st);
+    check(e, "transfer launch");
+    count_launch();
+}
+
+}  // namespace skg

@@ -1,0 +1,71 @@
+// kernels.hpp — host-callable launchers for the B200 spectral kernels (no torch types).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace skg {
+
+// One row of the launch table: which single-CTA sizes exist.
+constexpr int kMaxLog2F64 = 13;   // 8192 complex fp64 = 136 KB padded SMEM
+constexpr int kMaxLog2F32 = 14;   // 16384 complex fp32
+
+template <typename T> constexpr int max_log2() { return sizeof(T) == 8 ? kMaxLog2F64 : kMaxLog2F32; }
+
+// complex -> complex, natural order in and out; scale applied on store (1/L for inverse).
+// in == out allowed.
+template <typename T>
+cudaError_t launch_fft_c2c(int log2L, bool inverse, const void* in, long long in_stride, void* out,
+                           long long out_stride, long long batch, const void* tw, T scale,
+                           cudaStream_t st);
+
+// real trace (N samples, zero padded to L = 2^(log2M+1)) -> spectrum via an M-point complex FFT
+// of packed sample pairs. mode 0: full L-bin spectrum (reference layout, spectra.cpp:21-38);
+// mode 1: half spectrum, M+1 bins; mode 2: H = X * rtab (rtab = 1/X_ref), |H| and arg H on M+1
+// bins (h optional, M+1 complex).
+template <typename T>
+cudaError_t launch_fft_r2c(int log2M, long long N, const T* x, long long x_stride, long long batch,
+                           const void* tw, const void* post, int mode, void* out, long long out_stride,
+                           const void* rtab, T* mag, T* phase, long long mp_stride, cudaStream_t st);
+
+// fused Bluestein CZT (czt.cpp:116-130): x * chirp_in -> FFT_L -> * khat (pre-scaled by 1/L)
+// -> IFFT_L -> * chirp_out, first M bins stored. x real (T) or complex (cx<T>).
+template <typename T>
+cudaError_t launch_czt(int log2L, long long N, long long M, bool complex_in, const void* x,
+                       long long x_stride, long long batch, void* out, long long out_stride,
+                       const void* tw, const void* cin, const void* khat, const void* cout,
+                       cudaStream_t st);
+
+// ---- fused Zoom FFT (kernels_zoom.cu) --------------------------------------------------
+constexpr int kZoomK = 8;   // FIR outputs per thread
+struct ZoomArgs {
+    long long n;       // samples per trace
+    long long U;       // usable length (circular) or n (linear)
+    int D;             // decimation
+    int T;             // taps
+    int nout;          // FIR outputs fed to the FFT (decimated_len)
+    int trim;          // first FIR output kept (linear trim mode)
+    int rowlen;        // polyphase row length (elements, unpadded, incl. margin)
+    int pre;           // zero prefix per row (lh + kZoomK)
+    int rs;            // padded row stride (odd)
+    int lh;            // taps per phase row, rounded up to kZoomK
+    int k_lo;          // first signed band bin
+    int nbins;         // band bins
+    int mwrap;         // outputs needing the circular wrap correction
+    int circular;
+    double wre, wim;   // wrap factor e^{-i2pi fc U/fs}
+};
+cudaError_t launch_zoom_f64(const ZoomArgs& a, int log2n, const double* x, long long xs, long long batch,
+                            const void* g, const void* S, const void* tw, const void* band, void* out,
+                            long long os, cudaStream_t st);
+cudaError_t launch_zoom_f32(const ZoomArgs& a, int log2n, const float* x, long long xs, long long batch,
+                            const void* g, const void* S, const void* tw, const void* band, void* out,
+                            long long os, cudaStream_t st);
+// shared bytes the fused zoom kernel needs for this geometry
+size_t zoom_smem_bytes(const ZoomArgs& a, int log2n, bool f32);
+
+// elementwise helpers
+cudaError_t launch_c64_to_c32(const void* in, void* out, long long n, cudaStream_t st);
+cudaError_t launch_scale_c64(void* data, long long n, double s, cudaStream_t st);
+
+}  // namespace skg

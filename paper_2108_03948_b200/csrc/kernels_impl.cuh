@@ -1,0 +1,302 @@
+// kernels_impl.cuh — batched single-CTA FFT / real-input FFT / fused Bluestein CZT kernels.
+// Instantiated per scalar type in kernels_f64.cu / kernels_f32.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "fft_device.cuh"
+#include "kernels.hpp"
+
+namespace skg {
+
+template <typename T, int LOG2L> struct KCfg {
+    using G = FftGeom<LOG2L>;
+    static constexpr int GROUPS = G::NT >= 128 ? 1 : 128 / G::NT;   // transforms per CTA
+    static constexpr int BLOCK = G::NT * GROUPS;
+    static constexpr size_t SMEM_BYTES = (size_t)GROUPS * G::SMEM * sizeof(cx_t<T>);
+    // cap registers at 128/thread (>= 2 CTAs of 256 threads per SM) unless the block is 1024 wide
+    static constexpr int MINB = BLOCK >= 1024 ? 1 : (BLOCK >= 512 ? 1 : 512 / BLOCK);
+};
+
+template <typename K> inline cudaError_t prep_smem(K kernel, size_t bytes) {
+    if (bytes > 48 * 1024) return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    return cudaSuccess;
+}
+
+inline unsigned grid_for(long long batch, int groups) { return (unsigned)((batch + groups - 1) / groups); }
+
+// ---------------------------------------------------------------------------------------
+// complex -> complex (FftPlan::forward/inverse, numerics.cpp:73-100; fft/ifft 102-120)
+template <typename T, int LOG2L, bool INV>
+__global__ void __launch_bounds__(KCfg<T, LOG2L>::BLOCK, KCfg<T, LOG2L>::MINB)
+k_fft_c2c(const cx_t<T>* in, long long in_stride, cx_t<T>* out, long long out_stride, long long batch,
+          const cx_t<T>* __restrict__ tw, T scale) {
+    using C = cx_t<T>;
+    using G = FftGeom<LOG2L>;
+    using K = KCfg<T, LOG2L>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C* sm = reinterpret_cast<C*>(smraw) + (threadIdx.x / G::NT) * G::SMEM;
+    const int tid = threadIdx.x % G::NT;
+    const long long b = (long long)blockIdx.x * K::GROUPS + threadIdx.x / G::NT;
+    const bool active = b < batch;
+    C v[G::EPT];
+    const C* src = in + b * in_stride;
+#pragma unroll
+    for (int q = 0; q < G::EPT; ++q) v[q] = active ? src[tid + G::NT * q] : czero<C>();
+    block_fft<INV, LOG2L>(v, sm, tw, tid);
+    if (active) {
+        C* dst = out + b * out_stride;
+#pragma unroll
+        for (int q = 0; q < G::EPT; ++q) dst[tid + G::NT * q] = cscale(v[q], scale);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// real input, zero padded to L = 2M: M-point complex FFT of z[n] = x[2n] + i x[2n+1], then
+// X[k] = E[k] + W_L^k O[k] with E/O split from Z[k], conj Z[M-k]. Replaces fft_spectrum's
+// zero_pad + dft_any (spectra.cpp:21-38) without ever materialising the zeros.
+template <typename T, int LOG2M, int NZ>
+__global__ void __launch_bounds__(KCfg<T, LOG2M>::BLOCK, KCfg<T, LOG2M>::MINB)
+k_fft_r2c(const T* __restrict__ x, long long x_stride, long long N, int vec, long long batch,
+          const cx_t<T>* __restrict__ tw, const cx_t<T>* __restrict__ post, int mode, cx_t<T>* __restrict__ out,
+          long long out_stride, const cx_t<T>* __restrict__ rtab, T* __restrict__ mag, T* __restrict__ phase,
+          long long mp_stride) {
+    using C = cx_t<T>;
+    using G = FftGeom<LOG2M>;
+    using K = KCfg<T, LOG2M>;
+    constexpr int M = G::L;
+    constexpr long long L = 2LL * M;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C* sm = reinterpret_cast<C*>(smraw) + (threadIdx.x / G::NT) * G::SMEM;
+    const int tid = threadIdx.x % G::NT;
+    const long long b = (long long)blockIdx.x * K::GROUPS + threadIdx.x / G::NT;
+    const bool active = b < batch;
+    C v[G::EPT];
+    const T* xs = x + b * x_stride;
+    const long long half = N >> 1;
+#pragma unroll
+    for (int q = 0; q < G::EPT; ++q) {
+        v[q] = czero<C>();
+        if (q < NZ && active) {
+            const long long pos = tid + (long long)G::NT * q;
+            if (vec) {
+                if (pos < half) v[q] = __ldg(reinterpret_cast<const C*>(xs) + pos);
+                else if (2 * pos < N) v[q] = mk<C>(xs[2 * pos], (T)0);
+            } else {
+                if (2 * pos < N) v[q].x = xs[2 * pos];
+                if (2 * pos + 1 < N) v[q].y = xs[2 * pos + 1];
+            }
+        }
+    }
+    block_fft<false, LOG2M, NZ>(v, sm, tw, tid);
+
+    // pair Z[k] with Z[M-k]
+    if constexpr (G::NT > 1) {
+#pragma unroll
+        for (int q = 0; q < G::EPT; ++q) sm[pad16(tid + G::NT * q)] = v[q];
+        __syncthreads();
+    }
+    if (!active) return;
+#pragma unroll
+    for (int q = 0; q < G::EPT; ++q) {
+        const int k = tid + G::NT * q;
+        C c;
+        if constexpr (G::NT == 1) c = v[(M - q) & (M - 1)];
+        else c = sm[pad16((M - k) & (M - 1))];
+        const C z = v[q];
+        const C E = mk<C>((T)0.5 * (z.x + c.x), (T)0.5 * (z.y - c.y));
+        const C O = mk<C>((T)0.5 * (z.y + c.y), (T)0.5 * (c.x - z.x));
+        const C X = cadd(E, cmul(O, __ldg(post + k)));
+        C XM = czero<C>();
+        if (k == 0) XM = mk<C>(z.x - z.y, (T)0);   // Nyquist bin M (E - O at k = 0)
+        if (mode == 0) {
+            C* o = out + b * out_stride;
+            o[k] = X;
+            if (k) o[L - k] = cconj(X);
+            else o[M] = XM;
+        } else if (mode == 1) {
+            C* o = out + b * out_stride;
+            o[k] = X;
+            if (k == 0) o[M] = XM;
+        } else {
+            T* mg = mag + b * mp_stride;
+            T* ph = phase + b * mp_stride;
+            const C H = cmul(X, __ldg(rtab + k));
+            mg[k] = sqrt(H.x * H.x + H.y * H.y);
+            ph[k] = atan2(H.y, H.x);
+            if (out) (out + b * out_stride)[k] = H;
+            if (k == 0) {
+                const C HM = cmul(XM, __ldg(rtab + M));
+                mg[M] = sqrt(HM.x * HM.x + HM.y * HM.y);
+                ph[M] = atan2(HM.y, HM.x);
+                if (out) (out + b * out_stride)[M] = HM;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// fused Bluestein CZT (CztPlan::execute, czt.cpp:116-130)
+template <typename T, int LOG2L, int NZ, int NO>
+__global__ void __launch_bounds__(KCfg<T, LOG2L>::BLOCK, KCfg<T, LOG2L>::MINB)
+k_czt(const void* __restrict__ xin, int complex_in, long long x_stride, long long N, long long M, long long batch,
+      cx_t<T>* __restrict__ out, long long out_stride, const cx_t<T>* __restrict__ tw,
+      const cx_t<T>* __restrict__ cin, const cx_t<T>* __restrict__ khat, const cx_t<T>* __restrict__ cout) {
+    using C = cx_t<T>;
+    using G = FftGeom<LOG2L>;
+    using K = KCfg<T, LOG2L>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    C* sm = reinterpret_cast<C*>(smraw) + (threadIdx.x / G::NT) * G::SMEM;
+    const int tid = threadIdx.x % G::NT;
+    const long long b = (long long)blockIdx.x * K::GROUPS + threadIdx.x / G::NT;
+    const bool active = b < batch;
+    C v[G::EPT];
+#pragma unroll
+    for (int q = 0; q < G::EPT; ++q) {
+        v[q] = czero<C>();
+        const long long pos = tid + (long long)G::NT * q;
+        if (q < NZ && active && pos < N) {
+            const C ch = __ldg(cin + pos);
+            if (complex_in) v[q] = cmul(__ldg(reinterpret_cast<const C*>(xin) + b * x_stride + pos), ch);
+            else v[q] = rmul(__ldg(reinterpret_cast<const T*>(xin) + b * x_stride + pos), ch);
+        }
+    }
+    block_fft<false, LOG2L, NZ>(v, sm, tw, tid);
+#pragma unroll
+    for (int q = 0; q < G::EPT; ++q) v[q] = cmul(v[q], __ldg(khat + tid + G::NT * q));
+    block_fft<true, LOG2L, 16, NO>(v, sm, tw, tid);
+    if (!active) return;
+    C* o = out + b * out_stride;
+#pragma unroll
+    for (int q = 0; q < G::EPT; ++q) {
+        const long long pos = tid + (long long)G::NT * q;
+        if (q < NO && pos < M) o[pos] = cmul(v[q], __ldg(cout + pos));
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// launch plumbing
+
+template <typename T, int LOG2L, bool INV>
+cudaError_t run_c2c(const void* in, long long in_stride, void* out, long long out_stride, long long batch,
+                    const void* tw, T scale, cudaStream_t st) {
+    using K = KCfg<T, LOG2L>;
+    using C = cx_t<T>;
+    auto kern = k_fft_c2c<T, LOG2L, INV>;
+    cudaError_t e = prep_smem(kern, K::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    kern<<<grid_for(batch, K::GROUPS), K::BLOCK, K::SMEM_BYTES, st>>>(
+        (const C*)in, in_stride, (C*)out, out_stride, batch, (const C*)tw, scale);
+    return cudaGetLastError();
+}
+
+template <typename T, int LOG2M, int NZ>
+cudaError_t run_r2c(long long N, const T* x, long long x_stride, long long batch, const void* tw,
+                    const void* post, int mode, void* out, long long out_stride, const void* rtab, T* mag,
+                    T* phase, long long mp_stride, cudaStream_t st) {
+    using K = KCfg<T, LOG2M>;
+    using C = cx_t<T>;
+    auto kern = k_fft_r2c<T, LOG2M, NZ>;
+    cudaError_t e = prep_smem(kern, K::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    const int vec = ((N & 1) == 0 && (x_stride & 1) == 0 && ((uintptr_t)x % (2 * sizeof(T))) == 0) ? 1 : 0;
+    kern<<<grid_for(batch, K::GROUPS), K::BLOCK, K::SMEM_BYTES, st>>>(
+        x, x_stride, N, vec, batch, (const C*)tw, (const C*)post, mode, (C*)out, out_stride, (const C*)rtab,
+        mag, phase, mp_stride);
+    return cudaGetLastError();
+}
+
+template <typename T, int LOG2L, int NZ, int NO>
+cudaError_t run_czt(long long N, long long M, bool complex_in, const void* x, long long x_stride, long long batch,
+                    void* out, long long out_stride, const void* tw, const void* cin, const void* khat,
+                    const void* cout, cudaStream_t st) {
+    using K = KCfg<T, LOG2L>;
+    using C = cx_t<T>;
+    auto kern = k_czt<T, LOG2L, NZ, NO>;
+    cudaError_t e = prep_smem(kern, K::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    kern<<<grid_for(batch, K::GROUPS), K::BLOCK, K::SMEM_BYTES, st>>>(
+        x, complex_in ? 1 : 0, x_stride, N, M, batch, (C*)out, out_stride, (const C*)tw, (const C*)cin,
+        (const C*)khat, (const C*)cout);
+    return cudaGetLastError();
+}
+
+// leading nonzero count of the first radix-16 pass, rounded up to {4,8,16} (pruned variants
+// are only instantiated for L >= 256; smaller transforms always run the full pass)
+inline int nz_class(long long nonzero, int nt) {
+    const long long per = (nonzero + nt - 1) / nt;
+    if (per <= 4) return 4;
+    if (per <= 8) return 8;
+    return 16;
+}
+inline int no_class(long long needed, int nt) {
+    const long long per = (needed + nt - 1) / nt;
+    return per <= 8 ? 8 : 16;
+}
+
+template <int V> struct IC { static constexpr int value = V; };
+
+template <int LO, int HI, typename F> cudaError_t dispatch_log2(int lg, F&& f) {
+    if constexpr (LO > HI) {
+        return cudaErrorInvalidValue;
+    } else {
+        if (lg == LO) return f(IC<LO>{});
+        return dispatch_log2<LO + 1, HI>(lg, f);
+    }
+}
+
+template <int LG, typename F> cudaError_t dispatch_nz(int nz, F&& f) {
+    if constexpr (LG < 8) {
+        return f(IC<16>{});
+    } else {
+        if (nz == 4) return f(IC<4>{});
+        if (nz == 8) return f(IC<8>{});
+        return f(IC<16>{});
+    }
+}
+
+template <typename T>
+cudaError_t launch_fft_c2c_impl(int log2L, bool inverse, const void* in, long long in_stride, void* out,
+                                long long out_stride, long long batch, const void* tw, T scale, cudaStream_t st) {
+    return dispatch_log2<0, max_log2<T>()>(log2L, [&](auto lg) {
+        constexpr int LG = decltype(lg)::value;
+        return inverse ? run_c2c<T, LG, true>(in, in_stride, out, out_stride, batch, tw, scale, st)
+                       : run_c2c<T, LG, false>(in, in_stride, out, out_stride, batch, tw, scale, st);
+    });
+}
+
+template <typename T>
+cudaError_t launch_fft_r2c_impl(int log2M, long long N, const T* x, long long x_stride, long long batch,
+                                const void* tw, const void* post, int mode, void* out, long long out_stride,
+                                const void* rtab, T* mag, T* phase, long long mp_stride, cudaStream_t st) {
+    return dispatch_log2<0, max_log2<T>()>(log2M, [&](auto lg) {
+        constexpr int LG = decltype(lg)::value;
+        const int nz = nz_class((N + 1) / 2, FftGeom<LG>::NT);
+        return dispatch_nz<LG>(nz, [&](auto z) {
+            constexpr int NZ = decltype(z)::value;
+            return run_r2c<T, LG, NZ>(N, x, x_stride, batch, tw, post, mode, out, out_stride, rtab, mag, phase,
+                                      mp_stride, st);
+        });
+    });
+}
+
+template <typename T>
+cudaError_t launch_czt_impl(int log2L, long long N, long long M, bool complex_in, const void* x, long long x_stride,
+                            long long batch, void* out, long long out_stride, const void* tw, const void* cin,
+                            const void* khat, const void* cout, cudaStream_t st) {
+    return dispatch_log2<0, max_log2<T>()>(log2L, [&](auto lg) {
+        constexpr int LG = decltype(lg)::value;
+        const int nz = nz_class(N, FftGeom<LG>::NT);
+        const int no = no_class(M, FftGeom<LG>::NT);
+        return dispatch_nz<LG>(nz, [&](auto z) {
+            constexpr int NZ = decltype(z)::value;
+            if (LG >= 8 && no == 8)
+                return run_czt<T, LG, NZ, (LG >= 8 ? 8 : 16)>(N, M, complex_in, x, x_stride, batch, out, out_stride,
+                                                              tw, cin, khat, cout, st);
+            return run_czt<T, LG, NZ, 16>(N, M, complex_in, x, x_stride, batch, out, out_stride, tw, cin, khat,
+                                          cout, st);
+        });
+    });
+}
+
+}  // namespace skg

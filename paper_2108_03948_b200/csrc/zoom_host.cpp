@@ -1,0 +1,177 @@
+// zoom_host.cpp — ZoomFftPlan restated (make_zoom_plan, zoomfft.cpp:106-181) plus the device
+// tables of the fused zoom kernel.
+#include <algorithm>
+#include <cmath>
+
+#include "host.hpp"
+
+namespace skg {
+
+ZoomPlanG::ZoomPlanG(size_t in_len, double f1, double f2, double fs, const ZoomOptionsG& opts,
+                     size_t n_fft_override, const double* taps, size_t num_taps) {
+    // validation order and messages follow zoomfft.cpp:108-115
+    if (in_len < 2) throw std::invalid_argument("make_zoom_plan: need at least 2 input samples");
+    if (!(fs > 0.0)) throw std::invalid_argument("make_zoom_plan: sample rate must be positive");
+    if (!(f1 >= 0.0) || !(f2 > f1)) throw std::invalid_argument("make_zoom_plan: band must satisfy 0 <= f1 < f2");
+    if (f2 > fs / 2.0 * (1.0 + 1e-12))
+        throw std::invalid_argument("make_zoom_plan: band exceeds the Nyquist frequency");
+    f1_hz = f1;
+    f2_hz = f2;
+    sample_rate_hz = fs;
+    circular = opts.circular;
+    trim_transient = opts.trim_transient;
+    pad_pow2 = opts.pad_pow2;
+    input_len = in_len;
+    const double band = f2 - f1;
+    center_hz = opts.center_set ? opts.center_hz : 0.5 * (f1 + f2);
+    if (!std::isfinite(center_hz)) throw std::invalid_argument("make_zoom_plan: non-finite center frequency");
+    decimation = opts.decimation == 0
+                     ? std::max<size_t>(1, static_cast<size_t>(std::floor(fs / (2.0 * band))))
+                     : opts.decimation;
+    const double dnyq = fs / (2.0 * static_cast<double>(decimation));
+    const double reach = std::max(f2 - center_hz, center_hz - f1);
+    if (reach > dnyq * (1.0 + 1e-12))
+        throw std::invalid_argument("make_zoom_plan: decimation too large for the requested band");
+    const bool auto_filter = opts.num_taps == 0 && !(opts.cutoff_hz > 0.0);
+    if (decimation == 1 && auto_filter) {
+        filter_taps = {1.0};
+        cutoff_hz = fs / 2.0;
+    } else {
+        cutoff_hz = opts.cutoff_hz > 0.0 ? opts.cutoff_hz : 0.5 * (0.5 * band + dnyq);
+        filter_taps = design_lowpass(cutoff_hz, fs, opts.num_taps == 0 ? 101 : opts.num_taps);
+    }
+    if (taps) {   // extension: explicit filter (e.g. the even 64-tap design of the cfg3 text)
+        if (num_taps == 0) throw std::invalid_argument("zoom: empty filter");
+        filter_taps.assign(taps, taps + num_taps);
+    }
+    group_delay_samples = 0.5 * static_cast<double>(filter_taps.size() - 1);
+    usable_len = circular ? (in_len / decimation) * decimation : in_len;
+    if (usable_len / decimation < 2)
+        throw std::invalid_argument("make_zoom_plan: record too short for this decimation factor");
+    if (circular && filter_taps.size() > usable_len)
+        throw std::invalid_argument("make_zoom_plan: filter longer than the usable record");
+    size_t block = usable_len / decimation;
+    if (!circular && trim_transient) {
+        trim_samples = (filter_taps.size() - 1 + decimation - 1) / decimation;
+        if (trim_samples >= block)
+            throw std::invalid_argument("make_zoom_plan: transient trim would consume the whole record");
+        block -= trim_samples;
+    }
+    decimated_len = block;
+    n_fft = pad_pow2 ? next_pow2(block) : block;
+    if (n_fft_override) {
+        if (n_fft_override < block) throw std::invalid_argument("zoom: n_fft shorter than the decimated block");
+        n_fft = n_fft_override;
+    }
+    compute_band();
+    if (!is_pow2(n_fft))   // dft_any's chirp route for the short transform (zoomfft.cpp:204-207)
+        bluestein_ = std::make_unique<CztPlanG>(n_fft, cd(1.0, 0.0),
+                                                cis_cycles(-1.0 / static_cast<double>(n_fft), 1.0), n_fft);
+}
+
+double ZoomPlanG::f_step_hz() const {   // zoomfft.cpp:11-13
+    return sample_rate_hz / (static_cast<double>(decimation) * static_cast<double>(n_fft));
+}
+
+double ZoomPlanG::f_start_hz() const { return center_hz + static_cast<double>(k_lo) * f_step_hz(); }
+
+void ZoomPlanG::compute_band() {   // zoomfft.cpp:209-219
+    const double step = f_step_hz();
+    const long n = static_cast<long>(n_fft);
+    const double lo_idx = (f1_hz - center_hz) / step;
+    const double hi_idx = (f2_hz - center_hz) / step;
+    const double eps = 1e-9 * (1.0 + std::max(std::abs(lo_idx), std::abs(hi_idx)));
+    k_lo = static_cast<long>(std::ceil(lo_idx - eps));
+    k_hi = static_cast<long>(std::floor(hi_idx + eps));
+    k_lo = std::max(k_lo, -(n / 2));
+    k_hi = std::min(k_hi, n - 1 - n / 2);
+    // an empty window is reported by execute, like zoom_fft (zoomfft.cpp:218-219)
+}
+
+namespace {
+ZoomArgs make_args(const ZoomPlanG& p) {
+    ZoomArgs a{};
+    const int D = static_cast<int>(p.decimation);
+    const int T = static_cast<int>(p.filter_taps.size());
+    a.n = static_cast<long long>(p.input_len);
+    a.U = static_cast<long long>(p.usable_len);
+    a.D = D;
+    a.T = T;
+    a.nout = static_cast<int>(p.decimated_len);
+    a.trim = static_cast<int>(p.trim_samples);
+    const int per_row = (T + D - 1) / D;
+    a.lh = (per_row + kZoomK - 1) / kZoomK * kZoomK;
+    a.pre = a.lh + kZoomK;
+    a.rowlen = static_cast<int>((p.usable_len + p.decimation - 1) / p.decimation) + 2 * kZoomK;
+    int rs = (a.pre + a.rowlen) + (a.pre + a.rowlen) / kZoomK + 1;
+    if ((rs & 1) == 0) ++rs;
+    a.rs = rs;
+    a.k_lo = static_cast<int>(p.k_lo);
+    a.nbins = static_cast<int>(p.k_hi - p.k_lo + 1);
+    a.mwrap = (p.circular && T >= 2) ? (T - 2) / D + 1 : 0;
+    a.circular = p.circular ? 1 : 0;
+    const cd w = cis_cycles(-p.center_hz / p.sample_rate_hz, static_cast<double>(p.usable_len));
+    a.wre = w.real();
+    a.wim = w.imag();
+    return a;
+}
+}  // namespace
+
+const ZoomPlanG::Dev& ZoomPlanG::dev(bool f32) const {
+    std::call_once(once_[f32 ? 1 : 0], [&] {
+        require_device();
+        Dev& d = dev_[f32 ? 1 : 0];
+        const ZoomArgs a = make_args(*this);
+        const double qc = -center_hz / sample_rate_hz;   // zoomfft.cpp:174
+        const int D = a.D, T = a.T;
+        // taps by phase row: g[t] = h[t] e^{-i 2pi qc t}, row ph holds t = l D + (D - ph) % D
+        std::vector<cd> g(static_cast<size_t>(D) * a.lh, cd(0.0, 0.0));
+        for (int ph = 0; ph < D; ++ph) {
+            const int t0 = (D - ph) % D;
+            for (int l = 0; l < a.lh; ++l) {
+                const int t = l * D + t0;
+                if (t < T) g[static_cast<size_t>(ph) * a.lh + l] = filter_taps[t] * cis_cycles(-qc, static_cast<double>(t));
+            }
+        }
+        d.g = to_device(g, f32);
+        // S[m] = e^{i 2pi qc (m + trim) D} (the shift table sampled at the decimation points)
+        std::vector<cd> S(decimated_len);
+        for (size_t m = 0; m < decimated_len; ++m)
+            S[m] = cis_cycles(qc, static_cast<double>((m + trim_samples) * decimation));
+        d.sdec = to_device(S, f32);
+        // band: D e^{i 2pi k delay / (D n_fft)} (zoomfft.cpp:223-234)
+        const double delay = group_delay_samples + static_cast<double>(trim_samples * decimation);
+        const double q = delay / (static_cast<double>(decimation) * static_cast<double>(n_fft));
+        std::vector<cd> band(static_cast<size_t>(std::max<long>(0, k_hi - k_lo + 1)));
+        for (long k = k_lo; k <= k_hi; ++k)
+            band[static_cast<size_t>(k - k_lo)] = static_cast<double>(decimation) * cis_cycles(q, static_cast<double>(k));
+        d.band = to_device(band.empty() ? std::vector<cd>{cd(0, 0)} : band, f32);
+    });
+    return dev_[f32 ? 1 : 0];
+}
+
+void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void* out, long long out_stride,
+                        bool f32, cudaStream_t st) const {
+    if (k_lo > k_hi) throw std::invalid_argument("zoom_fft: no transform bins fall inside the band");
+    if (batch <= 0) return;
+    const Dev& d = dev(f32);
+    const ZoomArgs a = make_args(*this);
+    const int lg = ilog2(n_fft);
+    int dev_id = current_device();
+    int smem_max = 0;
+    check(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev_id), "attr");
+    const bool fused = is_pow2(n_fft) && lg <= single_cta_max_log2(f32) &&
+                       zoom_smem_bytes(a, lg, f32) <= static_cast<size_t>(smem_max);
+    if (!fused)
+        throw std::invalid_argument("zoom_fft: geometry (n=" + std::to_string(input_len) + ", n_fft=" +
+                                    std::to_string(n_fft) + ") needs the unfused path (not available in this build)");
+    const void* tw = stockham_twiddles(lg, f32);
+    cudaError_t e = f32 ? launch_zoom_f32(a, lg, (const float*)x, x_stride, batch, d.g.p, d.sdec.p, tw, d.band.p,
+                                          out, out_stride, st)
+                        : launch_zoom_f64(a, lg, (const double*)x, x_stride, batch, d.g.p, d.sdec.p, tw, d.band.p,
+                                          out, out_stride, st);
+    check(e, "zoom launch");
+    count_launch();
+}
+
+}  // namespace skg

@@ -1,0 +1,167 @@
+"""Generate the golden fixtures in tests/golden/ from the REFERENCE ITSELF.
+
+Run in the build container (needs /root/reference and `make -C oracle ref`):
+    python tests/golden/make_golden.py
+Every output array here is produced by the unmodified reference C++ (oracle/_ref/libskref.so:
+its own sk_* C ABI plus the plan-reuse shim), never by our code. Inputs are seeded. The
+fixtures pin (a) the oracle restatement (tests/test_oracle.py) and (b) the GPU path
+(tests/test_gpu_*.py) at sizes that stay small in git.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+from paper_2108_03948_b200 import workloads as W  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+R = oracle.ref()
+if R is None:
+    raise SystemExit("oracle/_ref/libskref.so missing: run `make -C oracle ref` first")
+P = oracle._p
+
+
+def ref_fft(x, inverse=False):
+    re, im = np.ascontiguousarray(x.real), np.ascontiguousarray(x.imag)
+    rc = (R.sk_ifft if inverse else R.sk_fft)(P(re), P(im), re.size)
+    assert rc == 0, R.sk_last_error()
+    return re + 1j * im
+
+
+def ref_czt(x, a, w, m):
+    x = np.asarray(x, np.complex128)
+    re, im = np.ascontiguousarray(x.real), np.ascontiguousarray(x.imag)
+    orr, oi = np.zeros(m), np.zeros(m)
+    rc = R.sk_czt(P(re), P(im), x.size, a.real, a.imag, w.real, w.imag, m, P(orr), P(oi))
+    assert rc == 0, R.sk_last_error()
+    return orr + 1j * oi
+
+
+def ref_dft_naive(x):
+    re, im = np.ascontiguousarray(x.real), np.ascontiguousarray(x.imag)
+    orr, oi = np.zeros(x.size), np.zeros(x.size)
+    assert R.sk_dft_naive(P(re), P(im), x.size, P(orr), P(oi)) == 0
+    return orr + 1j * oi
+
+
+def ref_fft_spectrum(samples, fs, length):
+    s = np.ascontiguousarray(samples, np.float64)
+    t = C.c_void_p()
+    assert R.sk_trace_create(P(s), s.size, fs, 0.0, C.byref(t)) == 0
+    sp = C.c_void_p()
+    assert R.sk_fft_spectrum(t, length, C.byref(sp)) == 0, R.sk_last_error()
+    n = R.sk_spectrum_size(sp)
+    re, im = np.zeros(n), np.zeros(n)
+    R.sk_spectrum_copy_data(sp, P(re), P(im))
+    f0, df = R.sk_spectrum_f_start(sp), R.sk_spectrum_f_step(sp)
+    R.sk_spectrum_free(sp)
+    R.sk_trace_free(t)
+    return re + 1j * im, f0, df
+
+
+def ref_zoom(samples, fs, f1, f2, taps=None, n_fft=None, **kw):
+    o = dict(center_hz=0.0, center_set=0, decimation=0, cutoff_hz=0.0, num_taps=0, circular=1,
+             trim_transient=0, pad_pow2=1)
+    o.update(kw)
+    x = np.ascontiguousarray(np.atleast_2d(samples), np.float64)
+    n = x.shape[1]
+    p = R.skr_zoom_plan_create(n, f1, f2, fs, o["center_hz"], o["center_set"], o["decimation"],
+                               o["cutoff_hz"], o["num_taps"], o["circular"], o["trim_transient"],
+                               o["pad_pow2"])
+    assert p
+    if taps is not None:
+        t = np.ascontiguousarray(taps, np.float64)
+        R.skr_zoom_plan_set_taps(p, P(t), t.size)
+    if n_fft is not None:
+        assert R.skr_zoom_plan_set_n_fft(p, n_fft) == 0
+    nb, f0, df = C.c_size_t(), C.c_double(), C.c_double()
+    R.skr_zoom_batch(p, P(x), n, fs, 0, 1, None, C.byref(nb), C.byref(f0), C.byref(df))
+    out = np.zeros((x.shape[0], nb.value), np.complex128)
+    R.skr_zoom_batch(p, P(x), n, fs, x.shape[0], 1, P(out.view(np.float64)), C.byref(nb), C.byref(f0),
+                     C.byref(df))
+    R.skr_zoom_plan_free(p)
+    return out, f0.value, df.value
+
+
+def main():
+    rng = np.random.default_rng(101)
+    # --- FFT: random complex inputs, every power of two 1..4096 plus the reference KAT ------
+    fft = {}
+    for lg in range(0, 13):
+        n = 1 << lg
+        x = rng.uniform(-1, 1, (2, n)) + 1j * rng.uniform(-1, 1, (2, n))
+        fft[f"x{n}"] = x
+        fft[f"X{n}"] = np.stack([ref_fft(r) for r in x])
+        fft[f"i{n}"] = np.stack([ref_fft(r, inverse=True) for r in x])
+    fft["kat_x"] = np.array([1, 2, 3, 4], np.complex128)
+    fft["kat_X"] = ref_fft(fft["kat_x"])
+    x = rng.uniform(-1, 1, 12) + 1j * rng.uniform(-1, 1, 12)
+    fft["naive_x"], fft["naive_X"] = x, ref_dft_naive(x)
+    np.savez_compressed(os.path.join(OUT, "fft.npz"), **fft)
+
+    # --- CZT: cfg2-shape trace, random band configs, off-circle spiral, full circle ----------
+    czt = {}
+    a, w = W.cfg2_czt_params(2048)
+    x = W.cfg2_batch(2, 1024)[[0, 2]]   # one reference and one sample trace
+    czt["cfg2_x"], czt["cfg2_a"], czt["cfg2_w"] = x, a, w
+    czt["cfg2_X"] = np.stack([ref_czt(r, a, w, 2048) for r in x])
+    cases = []
+    crng = np.random.default_rng(303)
+    for i in range(24):
+        n = int(crng.integers(2, 700))
+        m = int(crng.integers(2, 700))
+        f1 = crng.uniform(0, 3500)
+        f2 = crng.uniform(f1 + 10, 4000)
+        ab, wb = oracle.czt_params_for_band(f1, f2, 8000.0, m)
+        xx = crng.uniform(-1, 1, n) + 1j * crng.uniform(-1, 1, n)
+        czt[f"r{i}_x"], czt[f"r{i}_X"] = xx, ref_czt(xx, ab, wb, m)
+        cases.append((n, m, ab.real, ab.imag, wb.real, wb.imag))
+    czt["rand_params"] = np.array(cases)
+    sa, sw = 1.05 * np.exp(0.3j), 0.995 * np.exp(-0.11j)
+    xx = np.random.default_rng(5).uniform(-1, 1, 20) + 1j * np.random.default_rng(6).uniform(-1, 1, 20)
+    czt["spiral_x"], czt["spiral_a"], czt["spiral_w"] = xx, sa, sw
+    czt["spiral_X"] = ref_czt(xx, sa, sw, 24)
+    np.savez_compressed(os.path.join(OUT, "czt.npz"), **czt)
+
+    # --- spectra: cfg1 pair at 4096, the 500-sample pulse (pow2 pad and exact 500) ----------
+    sp = {}
+    ref, sample = W.cfg1_pair()
+    sp["cfg1_ref"], sp["cfg1_sample"] = ref, sample
+    sp["cfg1_Xr"], f0, df = ref_fft_spectrum(ref, W.FS, 4096)
+    sp["cfg1_Xs"], _, _ = ref_fft_spectrum(sample, W.FS, 4096)
+    sp["cfg1_df"] = df
+    pulse = W.thz_pulse(500, fs=10e12)
+    sp["pulse500"] = pulse
+    sp["pulse500_X512"], _, _ = ref_fft_spectrum(pulse, 10e12, 0)
+    sp["pulse500_X500"], _, _ = ref_fft_spectrum(pulse, 10e12, 500)
+    np.savez_compressed(os.path.join(OUT, "spectra.npz"), **sp)
+
+    # --- zoom: cfg3 reference sizing (65 taps, n_fft 512), the 2048 variant, 500-sample plans ----
+    zm = {}
+    x3 = W.cfg3_batch(3, 4096)
+    zm["cfg3_x"] = x3
+    zm["cfg3_Z512"], zm["cfg3_f0_512"], zm["cfg3_df_512"] = ref_zoom(x3, W.FS, 0.4e12, 1.2e12, decimation=8,
+                                                                      num_taps=65)
+    zm["cfg3_Z2048"], zm["cfg3_f0_2048"], zm["cfg3_df_2048"] = ref_zoom(x3, W.FS, 0.4e12, 1.2e12, decimation=8,
+                                                                        num_taps=65, n_fft=2048)
+    p500 = W.thz_pulse(500, fs=10e12)
+    zm["p500"] = p500
+    zm["p500_default"], zm["p500_default_f0"], _ = ref_zoom(p500, 10e12, 0.5e12, 2.0e12)
+    zm["p500_lin_trim"], zm["p500_lin_trim_f0"], _ = ref_zoom(p500, 10e12, 0.5e12, 2.0e12, decimation=4,
+                                                              circular=0, trim_transient=1)
+    zm["p500_d2"], _, _ = ref_zoom(p500, 10e12, 0.5e12, 2.0e12, decimation=2)
+    np.savez_compressed(os.path.join(OUT, "zoom.npz"), **zm)
+    for f in sorted(os.listdir(OUT)):
+        if f.endswith(".npz"):
+            print(f, os.path.getsize(os.path.join(OUT, f)))
+
+
+if __name__ == "__main__":
+    main()
