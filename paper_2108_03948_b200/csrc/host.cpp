@@ -219,13 +219,80 @@ const void* fourstep_twiddles(int log2R, int log2C, bool f32) {
     });
 }
 
+// ---- four-step plumbing -------------------------------------------------------------------------
+namespace {
+struct FourStep {
+    int lR, lC;
+    long long L;
+    const void *twR, *twC, *twL;
+    FourStep(int log2L, bool f32) {
+        lR = log2L / 2;
+        lC = log2L - lR;
+        if (lC > 10 || lR < 4)
+            throw std::invalid_argument("fft: length 2^" + std::to_string(log2L) + " exceeds the supported maximum 2^20");
+        L = 1LL << log2L;
+        twR = stockham_twiddles(lR, f32);
+        twC = stockham_twiddles(lC, f32);
+        twL = fourstep_twiddles(lR, lC, f32);
+    }
+    // traces per chunk so the work buffer stays L2 resident (~48 MB)
+    long long chunk(bool f32) const {
+        const long long bytes = L * (f32 ? 8 : 16);
+        return std::max<long long>(1, (48LL << 20) / bytes);
+    }
+};
+
+struct Scratch {   // stream-ordered work buffer
+    void* p = nullptr;
+    cudaStream_t st;
+    Scratch(size_t bytes, cudaStream_t s) : st(s) { check(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync"); }
+    ~Scratch() {
+        if (p) cudaFreeAsync(p, st);
+    }
+};
+
+template <typename T>
+void c2c_4step(const FourStep& f, bool inverse, int in_kind, const void* in, long long in_stride, long long N, void* out,
+               long long out_stride, long long batch, cudaStream_t st) {
+    const long long ch = f.chunk(sizeof(T) == 4);
+    Scratch Y((size_t)std::min(ch, batch) * f.L * 2 * sizeof(T), st);
+    const T scale = inverse ? (T)(1.0 / (double)f.L) : (T)1;
+    for (long long b0 = 0; b0 < batch; b0 += ch) {
+        const long long nb = std::min(ch, batch - b0);
+        const size_t es = in_kind == 1 ? sizeof(T) : 2 * sizeof(T);
+        const void* src = static_cast<const char*>(in) + (size_t)b0 * in_stride * es;
+        void* dst = static_cast<char*>(out) + (size_t)b0 * out_stride * 2 * sizeof(T);
+        check(launch_4step_col<T>(f.lR, false, in_kind, inverse ? 1 : 0, src, in_stride, N, nullptr, Y.p, f.lC, nb,
+                                  f.twR, f.twL, 0, nullptr, 0, 0, nullptr, (T)1, 0, st),
+              "4step col");
+        check(launch_4step_row<T>(f.lC, 0, Y.p, f.lR, nb, f.twC, f.twL, nullptr, dst, out_stride, scale,
+                                  inverse ? 1 : 0, st),
+              "4step row");
+        count_launch(2);
+    }
+}
+}  // namespace
+
 // ---- transforms -------------------------------------------------------------------------------
 void fft_c2c(size_t n, bool inverse, bool f32, const void* in, long long in_stride, void* out,
              long long out_stride, long long batch, cudaStream_t st) {
     if (batch <= 0) return;
     const int lg = ilog2(n);
-    if (lg > single_cta_max_log2(f32))
-        throw std::invalid_argument("fft: length " + std::to_string(n) + " exceeds the supported maximum");
+    if (lg > single_cta_max_log2(f32)) {
+        FourStep f(lg, f32);
+        if (in == out) {   // the row pass scatters: stage through a copy for in-place calls
+            Scratch tmp((size_t)batch * n * (f32 ? 8 : 16), st);
+            check(cudaMemcpy2DAsync(tmp.p, n * (f32 ? 8 : 16), in, in_stride * (f32 ? 8 : 16), n * (f32 ? 8 : 16),
+                                    batch, cudaMemcpyDeviceToDevice, st),
+                  "copy");
+            if (f32) c2c_4step<float>(f, inverse, 0, tmp.p, (long long)n, (long long)n, out, out_stride, batch, st);
+            else c2c_4step<double>(f, inverse, 0, tmp.p, (long long)n, (long long)n, out, out_stride, batch, st);
+            return;
+        }
+        if (f32) c2c_4step<float>(f, inverse, 0, in, in_stride, (long long)n, out, out_stride, batch, st);
+        else c2c_4step<double>(f, inverse, 0, in, in_stride, (long long)n, out, out_stride, batch, st);
+        return;
+    }
     const void* tw = stockham_twiddles(lg, f32);
     cudaError_t e;
     if (f32)
@@ -268,8 +335,8 @@ CztPlanG::CztPlanG(size_t n, cd a, cd w, size_t m) : n_(n), m_(m) {
         const double t = static_cast<double>(i);
         kern_[L_ - i] = W.pow(-0.5 * t * t);
     }
-    if (log2L_ > single_cta_max_log2(false) + 7)
-        throw std::invalid_argument("czt: convolution length " + std::to_string(L_) + " exceeds the supported maximum");
+    if (log2L_ > 20)
+        throw std::invalid_argument("czt: convolution length " + std::to_string(L_) + " exceeds the supported maximum 2^20");
 }
 
 const CztPlanG::Dev& CztPlanG::dev(bool f32) const {
@@ -284,6 +351,16 @@ const CztPlanG::Dev& CztPlanG::dev(bool f32) const {
         fft_c2c(L_, false, false, k64.p, 0, k64.p, 0, 1, nullptr);
         check(launch_scale_c64(k64.p, (long long)L_, 1.0 / static_cast<double>(L_), nullptr), "scale");
         count_launch();
+        if (log2L_ > single_cta_max_log2(f32)) {
+            // four-step layout: khat_p[k1][k2] = khat[k1 + R k2]
+            const int lR = log2L_ / 2, lC = log2L_ - lR;
+            const size_t R = size_t{1} << lR, Cn = size_t{1} << lC;
+            std::vector<cd> h(L_), p(L_);
+            check(cudaMemcpy(h.data(), k64.p, L_ * sizeof(cd), cudaMemcpyDeviceToHost), "D2H khat");
+            for (size_t k1 = 0; k1 < R; ++k1)
+                for (size_t k2 = 0; k2 < Cn; ++k2) p[k1 * Cn + k2] = h[k1 + R * k2];
+            k64.upload(p.data(), L_ * sizeof(cd));
+        }
         if (f32) {
             DevMem k32(L_ * 2 * sizeof(float));
             check(launch_c64_to_c32(k64.p, k32.p, (long long)L_, nullptr), "convert");
@@ -302,9 +379,37 @@ void CztPlanG::execute(const void* x, bool complex_in, long long x_stride, long 
     if (batch <= 0) return;
     const Dev& d = dev(f32);
     const long long N = static_cast<long long>(load_n ? std::min(load_n, n_) : n_);
-    if (log2L_ > single_cta_max_log2(f32))
-        throw std::invalid_argument("czt: convolution length " + std::to_string(L_) +
-                                    " needs the multi-pass path (not available in this build)");
+    if (log2L_ > single_cta_max_log2(f32)) {
+        FourStep f(log2L_, f32);
+        const long long ch = f.chunk(f32);
+        const size_t cs = f32 ? 8 : 16, es = complex_in ? cs : cs / 2;
+        Scratch Y((size_t)std::min(ch, batch) * f.L * cs, st);
+        const int kind = complex_in ? 3 : 2;
+        for (long long b0 = 0; b0 < batch; b0 += ch) {
+            const long long nb = std::min(ch, batch - b0);
+            const void* src = static_cast<const char*>(x) + (size_t)b0 * x_stride * es;
+            void* dst = static_cast<char*>(out) + (size_t)b0 * out_stride * cs;
+            cudaError_t e1, e2, e3;
+            if (f32) {
+                e1 = launch_4step_col<float>(f.lR, false, kind, 0, src, x_stride, N, d.cin.p, Y.p, f.lC, nb, f.twR, f.twL,
+                                             0, nullptr, 0, 0, nullptr, 1.0f, 0, st);
+                e2 = launch_4step_row<float>(f.lC, 1, Y.p, f.lR, nb, f.twC, f.twL, d.khat.p, nullptr, 0, 1.0f, 0, st);
+                e3 = launch_4step_col<float>(f.lR, true, 4, 0, nullptr, 0, 0, nullptr, Y.p, f.lC, nb, f.twR, f.twL, 1,
+                                             dst, out_stride, (long long)m_, d.cout.p, 1.0f, 0, st);
+            } else {
+                e1 = launch_4step_col<double>(f.lR, false, kind, 0, src, x_stride, N, d.cin.p, Y.p, f.lC, nb, f.twR,
+                                              f.twL, 0, nullptr, 0, 0, nullptr, 1.0, 0, st);
+                e2 = launch_4step_row<double>(f.lC, 1, Y.p, f.lR, nb, f.twC, f.twL, d.khat.p, nullptr, 0, 1.0, 0, st);
+                e3 = launch_4step_col<double>(f.lR, true, 4, 0, nullptr, 0, 0, nullptr, Y.p, f.lC, nb, f.twR, f.twL, 1,
+                                              dst, out_stride, (long long)m_, d.cout.p, 1.0, 0, st);
+            }
+            check(e1, "czt 4step col");
+            check(e2, "czt 4step row");
+            check(e3, "czt 4step col inv");
+            count_launch(3);
+        }
+        return;
+    }
     const void* tw = stockham_twiddles(log2L_, f32);
     cudaError_t e;
     if (f32)
@@ -357,9 +462,23 @@ void fft_spectrum_batch(size_t n, size_t len, bool f32, int layout, const void* 
         return;
     }
     const int lgM = ilog2(len) - 1;
-    if (lgM > single_cta_max_log2(f32))
-        throw std::invalid_argument("fft_spectrum: length " + std::to_string(len) +
-                                    " needs the multi-pass path (not available in this build)");
+    if (lgM > single_cta_max_log2(f32)) {
+        // multi-pass: complex FFT of the zero-padded real rows (imaginary part synthesised as 0)
+        FourStep f(lgM + 1, f32);
+        const size_t cs = f32 ? 8 : 16;
+        if (layout == 0) {
+            if (f32) c2c_4step<float>(f, false, 1, x, x_stride, (long long)n, out, out_stride, batch, st);
+            else c2c_4step<double>(f, false, 1, x, x_stride, (long long)n, out, out_stride, batch, st);
+        } else {
+            Scratch full((size_t)batch * len * cs, st);
+            if (f32) c2c_4step<float>(f, false, 1, x, x_stride, (long long)n, full.p, (long long)len, batch, st);
+            else c2c_4step<double>(f, false, 1, x, x_stride, (long long)n, full.p, (long long)len, batch, st);
+            check(cudaMemcpy2DAsync(out, out_stride * cs, full.p, len * cs, (len / 2 + 1) * cs, batch,
+                                    cudaMemcpyDeviceToDevice, st),
+                  "half copy");
+        }
+        return;
+    }
     const void* tw = stockham_twiddles(lgM, f32);
     const void* post = r2c_post_twiddles(lgM, f32);
     cudaError_t e;

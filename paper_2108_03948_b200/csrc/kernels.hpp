@@ -36,6 +36,20 @@ cudaError_t launch_czt(int log2L, long long N, long long M, bool complex_in, con
                        const void* tw, const void* cin, const void* khat, const void* cout,
                        cudaStream_t st);
 
+// ---- four-step passes for L = R * C beyond one CTA (kernels_4step.cuh) ----------------------
+// in_kind: 0 complex x, 1 real x, 2 real x * chirp, 3 complex x * chirp, 4 work buffer Y
+// out_kind: 0 Y with the W_L twiddle, 1 out * chirp_out (n < M), 2 out * scale (conj optional)
+template <typename T>
+cudaError_t launch_4step_col(int log2R, bool inverse, int in_kind, int conj_in, const void* x, long long x_stride,
+                             long long N, const void* cin, void* Y, int log2C, long long batch, const void* tw,
+                             const void* twL, int out_kind, void* out, long long out_stride, long long M,
+                             const void* cout, T scale, int conj_out, cudaStream_t st);
+// mode 0: FFT_C per row, natural-order store to out (scale/conj); mode 1: Bluestein middle in place
+template <typename T>
+cudaError_t launch_4step_row(int log2C, int mode, void* Y, int log2R, long long batch, const void* tw,
+                             const void* twL, const void* khat_p, void* out, long long out_stride, T scale,
+                             int conj_out, cudaStream_t st);
+
 // ---- fused Zoom FFT (kernels_zoom.cu) --------------------------------------------------
 constexpr int kZoomK = 8;   // FIR outputs per thread
 struct ZoomArgs {

@@ -1,0 +1,200 @@
+// kernels_4step.cuh — transforms longer than one CTA's shared memory (L = R * C, up to 2^20).
+//
+// Four-step factorisation with n = C n1 + n2, k = k1 + R k2:
+//   X[k1 + R k2] = sum_n2 W_C^{n2 k2} [ W_L^{n2 k1} sum_n1 x[C n1 + n2] W_R^{n1 k1} ]
+// Column pass (k4_col): for a tile of TC adjacent columns n2 (lane-interleaved so every load and
+// store moves 128-byte segments) an R-point Stockham FFT per column, the W_L twiddle applied on
+// the store into the work buffer Y[k1][n2]. Row pass (k4_row): a C-point FFT per row k1 of Y, then
+//   mode 0: natural-order store X[k1 + R k2] (rows lane-interleaved so the stride-R scatter is
+//           written as 128-byte segments) — complex FFT / zero-padded spectrum;
+//   mode 1: the whole Bluestein middle in shared memory: FFT_C, x khat (stored permuted as
+//           khat_p[k1][k2]), IFFT_C, x conj twiddle, back into Y — one read and one write of Y;
+// then an inverse column pass (input Y) finishes the CZT with the output chirp on the store.
+// The batch is processed in chunks small enough that Y stays resident in the 126 MB L2.
+#pragma once
+
+#include "kernels_impl.cuh"
+
+namespace skg {
+
+template <typename T> struct Tile {
+    static constexpr int W = 128 / (int)sizeof(cx_t<T>);   // columns per CTA: 8 (fp64) / 16 (fp32)
+};
+
+// column pass kinds
+enum : int { IN_CPLX = 0, IN_REAL = 1, IN_REAL_CHIRP = 2, IN_CPLX_CHIRP = 3, IN_WORK = 4 };
+enum : int { OUT_WORK_TW = 0, OUT_CHIRP = 1, OUT_SCALE = 2 };
+
+template <typename T, int LOG2R, bool INV>
+__global__ void __launch_bounds__(FftGeom<LOG2R>::NT * Tile<T>::W)
+k4_col(const void* __restrict__ xin, int in_kind, int conj_in, long long x_stride, long long N,
+       const cx_t<T>* __restrict__ cin, cx_t<T>* __restrict__ Y, int log2C, long long batch,
+       const cx_t<T>* __restrict__ tw, const cx_t<T>* __restrict__ twL, int out_kind, void* __restrict__ out,
+       long long out_stride, long long M, const cx_t<T>* __restrict__ cout, T scale, int conj_out) {
+    using C = cx_t<T>;
+    using G = FftGeom<LOG2R>;
+    constexpr int TC = Tile<T>::W;
+    constexpr int REG = G::SMEM + 1;   // odd-ish region stride keeps the 8/16 groups on distinct banks
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int g = threadIdx.x % TC;
+    const int tid = threadIdx.x / TC;
+    C* sm = reinterpret_cast<C*>(smraw) + g * REG;
+    const long long Cn = 1LL << log2C;
+    const long long tiles = Cn / TC;
+    const long long b = blockIdx.x / tiles;
+    const long long n2 = (blockIdx.x % tiles) * TC + g;
+    const long long L = Cn << LOG2R;
+    C v[G::EPT];
+#pragma unroll
+    for (int q = 0; q < G::EPT; ++q) {
+        const long long n1 = tid + (long long)G::NT * q;
+        const long long n = n1 * Cn + n2;
+        C val = czero<C>();
+        if (in_kind == IN_WORK) {
+            val = Y[b * L + n];   // Y[k1][n2] with k1 = n1
+        } else if (n < N) {
+            if (in_kind == IN_REAL || in_kind == IN_REAL_CHIRP)
+                val = mk<C>(__ldg(reinterpret_cast<const T*>(xin) + b * x_stride + n), (T)0);
+            else
+                val = __ldg(reinterpret_cast<const C*>(xin) + b * x_stride + n);
+            if (conj_in) val = cconj(val);
+            if (in_kind == IN_REAL_CHIRP || in_kind == IN_CPLX_CHIRP) val = cmul(val, __ldg(cin + n));
+        }
+        v[q] = val;
+    }
+    block_fft<INV, LOG2R>(v, sm, tw, tid);
+#pragma unroll
+    for (int q = 0; q < G::EPT; ++q) {
+        const long long k1 = tid + (long long)G::NT * q;
+        if (out_kind == OUT_WORK_TW) {
+            // Y[k1][n2] = v * W_L^{n2 k1} (forward twiddle of the four-step split)
+            Y[b * L + k1 * Cn + n2] = cmul(v[q], __ldg(twL + k1 * Cn + n2));
+        } else {
+            const long long n = k1 * Cn + n2;   // output sample index C n1 + n2
+            if (out_kind == OUT_CHIRP) {
+                if (n < M) reinterpret_cast<C*>(out)[b * out_stride + n] = cmul(v[q], __ldg(cout + n));
+            } else {
+                C r = cscale(v[q], scale);
+                if (conj_out) r = cconj(r);
+                reinterpret_cast<C*>(out)[b * out_stride + n] = r;
+            }
+        }
+    }
+}
+
+// mode 0: rows lane-interleaved (TR = Tile::W rows per CTA), natural-order scatter store.
+// mode 1: rows contiguous per group, Bluestein middle in place.
+template <typename T, int LOG2C, int MODE>
+__global__ void __launch_bounds__(MODE == 0 ? FftGeom<LOG2C>::NT * Tile<T>::W : KCfg<T, LOG2C>::BLOCK)
+k4_row(cx_t<T>* __restrict__ Y, int log2R, long long batch, const cx_t<T>* __restrict__ tw,
+       const cx_t<T>* __restrict__ twL, const cx_t<T>* __restrict__ khat_p, cx_t<T>* __restrict__ out,
+       long long out_stride, T scale, int conj_out) {
+    using C = cx_t<T>;
+    using G = FftGeom<LOG2C>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const long long R = 1LL << log2R;
+    const long long Cn = G::L;
+    const long long L = R * Cn;
+    int g, tid, rows_per_cta;
+    if constexpr (MODE == 0) {
+        rows_per_cta = Tile<T>::W;
+        g = threadIdx.x % rows_per_cta;
+        tid = threadIdx.x / rows_per_cta;
+    } else {
+        rows_per_cta = KCfg<T, LOG2C>::GROUPS;
+        g = threadIdx.x / G::NT;
+        tid = threadIdx.x % G::NT;
+    }
+    C* sm = reinterpret_cast<C*>(smraw) + g * (G::SMEM + 1);
+    const long long tiles = R / rows_per_cta;
+    const long long b = blockIdx.x / tiles;
+    const long long k1 = (blockIdx.x % tiles) * rows_per_cta + g;
+    C* row = Y + b * L + k1 * Cn;
+    C v[G::EPT];
+#pragma unroll
+    for (int q = 0; q < G::EPT; ++q) v[q] = row[tid + G::NT * q];
+    block_fft<false, LOG2C>(v, sm, tw, tid);
+    if constexpr (MODE == 0) {
+        C* o = out + b * out_stride;
+#pragma unroll
+        for (int q = 0; q < G::EPT; ++q) {
+            const long long k2 = tid + (long long)G::NT * q;
+            C r = cscale(v[q], scale);
+            if (conj_out) r = cconj(r);
+            o[k1 + R * k2] = r;
+        }
+    } else {
+        const C* kp = khat_p + k1 * Cn;
+#pragma unroll
+        for (int q = 0; q < G::EPT; ++q) v[q] = cmul(v[q], __ldg(kp + tid + G::NT * q));
+        block_fft<true, LOG2C>(v, sm, tw, tid);
+        const C* t = twL + k1 * Cn;
+#pragma unroll
+        for (int q = 0; q < G::EPT; ++q) {
+            const int n2 = tid + G::NT * q;
+            row[n2] = cmulc(v[q], __ldg(t + n2));   // x conj(W_L^{n2 k1})
+        }
+    }
+}
+
+}  // namespace skg
+
+namespace skg {
+
+template <typename T>
+cudaError_t launch_4step_col_impl(int log2R, bool inverse, int in_kind, int conj_in, const void* x, long long x_stride,
+                                  long long N, const void* cin, void* Y, int log2C, long long batch, const void* tw,
+                                  const void* twL, int out_kind, void* out, long long out_stride, long long M,
+                                  const void* cout, T scale, int conj_out, cudaStream_t st) {
+    using C = cx_t<T>;
+    return dispatch_log2<4, 10>(log2R, [&](auto lg) {
+        constexpr int LG = decltype(lg)::value;
+        using G = FftGeom<LG>;
+        constexpr int TC = Tile<T>::W;
+        const size_t smem = (size_t)TC * (G::SMEM + 1) * sizeof(C);
+        const long long tiles = (1LL << log2C) / TC;
+        auto launch = [&](auto kern) {
+            cudaError_t e = prep_smem(kern, smem);
+            if (e != cudaSuccess) return e;
+            kern<<<(unsigned)(tiles * batch), G::NT * TC, smem, st>>>(
+                x, in_kind, conj_in, x_stride, N, (const C*)cin, (C*)Y, log2C, batch, (const C*)tw, (const C*)twL,
+                out_kind, out, out_stride, M, (const C*)cout, scale, conj_out);
+            return cudaGetLastError();
+        };
+        return inverse ? launch(k4_col<T, LG, true>) : launch(k4_col<T, LG, false>);
+    });
+}
+
+template <typename T>
+cudaError_t launch_4step_row_impl(int log2C, int mode, void* Y, int log2R, long long batch, const void* tw,
+                                  const void* twL, const void* khat_p, void* out, long long out_stride, T scale,
+                                  int conj_out, cudaStream_t st) {
+    using C = cx_t<T>;
+    return dispatch_log2<4, 10>(log2C, [&](auto lg) {
+        constexpr int LG = decltype(lg)::value;
+        using G = FftGeom<LG>;
+        const long long R = 1LL << log2R;
+        if (mode == 0) {
+            constexpr int TR = Tile<T>::W;
+            const size_t smem = (size_t)TR * (G::SMEM + 1) * sizeof(C);
+            auto kern = k4_row<T, LG, 0>;
+            cudaError_t e = prep_smem(kern, smem);
+            if (e != cudaSuccess) return e;
+            kern<<<(unsigned)(R / TR * batch), G::NT * TR, smem, st>>>((C*)Y, log2R, batch, (const C*)tw,
+                                                                       (const C*)twL, (const C*)khat_p, (C*)out,
+                                                                       out_stride, scale, conj_out);
+        } else {
+            using K = KCfg<T, LG>;
+            const size_t smem = (size_t)K::GROUPS * (G::SMEM + 1) * sizeof(C);
+            auto kern = k4_row<T, LG, 1>;
+            cudaError_t e = prep_smem(kern, smem);
+            if (e != cudaSuccess) return e;
+            kern<<<(unsigned)(R / K::GROUPS * batch), K::BLOCK, smem, st>>>((C*)Y, log2R, batch, (const C*)tw,
+                                                                           (const C*)twL, (const C*)khat_p, (C*)out,
+                                                                           out_stride, scale, conj_out);
+        }
+        return cudaGetLastError();
+    });
+}
+
+}  // namespace skg

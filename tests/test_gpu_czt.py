@@ -98,7 +98,7 @@ def test_sweep_vs_oracle(prec, n, m):
 def test_complex_input_and_ragged_batches():
     rng = np.random.default_rng(8)
     n, m = 300, 77
-    a, w = 1.05 * np.exp(0.3j), 0.995 * np.exp(-0.011j)
+    a, w = 1.001 * np.exp(0.3j), 0.9999 * np.exp(-0.011j)   # mild spiral: |a^-n|, |w^(k^2/2)| stay O(1)
     plan = sk.CztPlanGPU(n, a, w, m)
     ref = O.CztPlan(n, a, w, m)
     for b in (1, 3, 17, 129):
