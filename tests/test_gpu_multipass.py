@@ -1,0 +1,94 @@
+"""GPU parity for lengths beyond one CTA's shared memory: the four-step multi-pass path
+(complex FFT up to 2^20, cfg5's long zero-padded spectra and CZTs up to L = 2^19)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2108_03948_b200 as sk
+from helpers import TOL_F32, TOL_F64, rel_l2_rows, rel_max_rows
+from paper_2108_03948_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+DEV = "cuda"
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("lg", [14, 15, 16, 17, 18, 20])
+def test_c2c_large(prec, lg):
+    if prec == "f32" and lg == 14:
+        pytest.skip("single-CTA size for fp32")
+    n = 1 << lg
+    b = 3 if lg < 18 else 1
+    rng = np.random.default_rng(lg)
+    x = rng.uniform(-1, 1, (b, n)) + 1j * rng.uniform(-1, 1, (b, n))
+    dt = torch.complex128 if prec == "f64" else torch.complex64
+    xd = torch.from_numpy(x).to(dt).to(DEV)
+    xin = xd.cpu().numpy().astype(np.complex128)
+    want = np.stack([O.fft(r) for r in xin])
+    got = sk.fft_batch(xd).cpu().numpy()
+    back = sk.fft_batch(torch.from_numpy(got).to(DEV), inverse=True).cpu().numpy()
+    if prec == "f64":
+        assert rel_max_rows(got, want) <= TOL_F64
+        assert rel_max_rows(back, xin) <= TOL_F64
+    else:
+        assert rel_l2_rows(got, want) <= TOL_F32
+        assert rel_l2_rows(back, xin) <= TOL_F32
+    if lg == 16:   # the C ABI one-shot path uses the same engine (sk_fft in place)
+        g = sk.fft(xin[0]) if prec == "f64" else None
+        if g is not None:
+            assert rel_max_rows([g], want[:1]) <= TOL_F64
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("n", [16384, 65536])
+def test_cfg5_long_spectra(prec, n):
+    L = 4 * n
+    x = W.sample_traces(2, n)
+    dt = torch.float64 if prec == "f64" else torch.float32
+    xd = torch.from_numpy(x).to(dt).to(DEV)
+    xin = xd.cpu().double().numpy()
+    want = O.fft_spectrum_batch(xin, L)
+    got = sk.fft_spectrum_batch(xd, L).cpu().numpy()
+    half = sk.fft_spectrum_batch(xd, L, layout=sk.SKG_HALF).cpu().numpy()
+    if prec == "f64":
+        assert rel_max_rows(got, want) <= TOL_F64
+    else:
+        assert rel_l2_rows(got, want) <= TOL_F32
+    np.testing.assert_array_equal(half, got[:, : L // 2 + 1])
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("n,m", [(4096, 16384), (16384, 4096), (16384, 16384), (3000, 12000), (65536, 16384)])
+def test_cfg5_long_czt(prec, n, m):
+    x = W.sample_traces(2, n)
+    a, w = W.cfg2_czt_params(m)
+    dt = torch.float64 if prec == "f64" else torch.float32
+    xd = torch.from_numpy(x).to(dt).to(DEV)
+    xin = xd.cpu().double().numpy()
+    plan = sk.CztPlanGPU(n, a, w, m, sk.SKG_F64 if prec == "f64" else sk.SKG_F32)
+    got = plan.execute(xd).cpu().numpy()
+    want = O.CztPlan(n, a, w, m).batch_real(xin)
+    if prec == "f64":
+        assert rel_max_rows(got, want) <= TOL_F64
+    else:
+        assert rel_l2_rows(got, want) <= TOL_F32
+
+
+def test_largest_czt_row_fp64():
+    """cfg5's largest row: N=65536, M=4N, L=2^19 (one trace; the oracle takes ~0.5 s)."""
+    n, m = 65536, 262144
+    x = W.sample_traces(1, n)
+    a, w = W.cfg2_czt_params(m)
+    got = sk.CztPlanGPU(n, a, w, m).execute(torch.from_numpy(x).to(DEV)).cpu().numpy()
+    assert rel_max_rows(got, O.CztPlan(n, a, w, m).batch_real(x)) <= TOL_F64
+
+
+def test_chunking_many_traces():
+    """More traces than one L2-resident chunk: results must not depend on the chunk boundaries."""
+    n, L = 16384, 65536
+    x = W.sample_traces(200, n)
+    xd = torch.from_numpy(x).to(DEV)
+    got = sk.fft_spectrum_batch(xd, L).cpu().numpy()
+    for i in (0, 95, 96, 97, 199):
+        assert rel_max_rows(got[i:i + 1], O.fft_spectrum_batch(x[i:i + 1], L)) <= TOL_F64
