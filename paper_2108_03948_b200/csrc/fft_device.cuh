@@ -176,6 +176,10 @@ template <int R, bool INV, int NZ, int NO, typename C> __device__ __forceinline_
 }
 
 // ---- geometry of an L = 2^LOG2L transform ------------------------------------------------
+// Twiddles of pass s (p = 16^s) are W_{pR}^{jk}, k < p. They are stored factorised by the base-16
+// digits of k: W_{pR}^{jk} = prod_d W_{pR/16^d}^{j k_d}, one (R-1) x 16 table per digit, so a
+// whole transform needs only sum_s s*(R_s-1)*16 entries (720 for L = 4096) and the tables live in
+// shared memory next to the data (no global loads inside the passes).
 template <int LOG2L> struct FftGeom {
     static constexpr int L = 1 << LOG2L;
     static constexpr int EPT = L < 16 ? L : 16;        // elements per thread
@@ -185,15 +189,23 @@ template <int LOG2L> struct FftGeom {
     static constexpr int SMEM = L < 16 ? 0 : L + (L >> 4);   // padded elements per transform
     __host__ __device__ static constexpr int radix(int s) { return L < 16 ? L : (s < P - 1 ? 16 : RLAST); }
     __host__ __device__ static constexpr int pval(int s) { return 1 << (4 * s); }
-    __host__ __device__ static constexpr int tw_off(int s) {
+    // offset of the digit-d table of pass s
+    __host__ __device__ static constexpr int tw_off(int s, int d) {
         int o = 0;
-        for (int t = 1; t < s; ++t) o += (radix(t) - 1) * pval(t);
-        return o;
+        for (int t = 1; t < s; ++t) o += t * (radix(t) - 1) * 16;
+        return o + d * (radix(s) - 1) * 16;
     }
-    static constexpr int TW_SIZE = tw_off(P);   // twiddle entries (pass 0 needs none)
+    static constexpr int TW_SIZE = tw_off(P, 0);   // entries (pass 0 needs none)
+    static constexpr int TW_ALLOC = TW_SIZE > 0 ? TW_SIZE : 1;
 };
 
 __device__ __forceinline__ int pad16(int a) { return a + (a >> 4); }
+
+// copy the factorised twiddle tables of an L-point transform into shared memory (whole CTA)
+template <int LOG2L, typename C>
+__device__ __forceinline__ void load_twiddles(C* dst, const C* __restrict__ src) {
+    for (int i = threadIdx.x; i < FftGeom<LOG2L>::TW_SIZE; i += blockDim.x) dst[i] = __ldg(src + i);
+}
 
 template <typename C> __device__ __forceinline__ C ldg_c(const C* p) {
 #ifdef SKG_PLAIN_LD
@@ -220,9 +232,13 @@ __device__ __forceinline__ void stockham_pass(C (&v)[FftGeom<LOG2L>::EPT], C* sm
         const int i = tid + G::NT * b;
         const int k = i & (p - 1);
         if constexpr (p > 1) {
-            const C* t = tw + G::tw_off(S) + k;
 #pragma unroll
-            for (int j = 1; j < R; ++j) u[j] = twmul<INV>(u[j], ldg_c(t + (j - 1) * p));
+            for (int j = 1; j < R; ++j) {
+                C w = tw[G::tw_off(S, 0) + (j - 1) * 16 + (k & 15)];
+#pragma unroll
+                for (int d = 1; d < S; ++d) w = cmul(w, tw[G::tw_off(S, d) + (j - 1) * 16 + ((k >> (4 * d)) & 15)]);
+                u[j] = twmul<INV>(u[j], w);
+            }
         }
         dft_r<R, INV, (S == 0 ? NZ : 16), (last ? NO : 16)>(u);
         if constexpr (last) {

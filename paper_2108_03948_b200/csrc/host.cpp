@@ -154,14 +154,18 @@ std::map<std::tuple<int, int, int, int>, DevMem>& tab_cache() {
 
 template <int LG> void stockham_host(std::vector<cd>& out) {
     using G = FftGeom<LG>;
-    out.assign(G::TW_SIZE > 0 ? G::TW_SIZE : 1, cd(1.0, 0.0));
+    out.assign(G::TW_ALLOC, cd(1.0, 0.0));
     if constexpr (G::L >= 16) {
         for (int s = 1; s < G::P; ++s) {
-            const int R = G::radix(s), p = G::pval(s);
-            const double q = -1.0 / (static_cast<double>(p) * R);   // exact power of two
-            for (int j = 1; j < R; ++j)
-                for (int k = 0; k < p; ++k)
-                    out[G::tw_off(s) + (j - 1) * p + k] = cis_cycles(q, static_cast<double>(j * k));
+            const int R = G::radix(s);
+            for (int d = 0; d < s; ++d) {
+                // digit d of k carries weight 16^d: W_{pR}^{j kd 16^d} = W_{M}^{j kd}, M = R 16^{s-d}
+                const double M = static_cast<double>(R) * static_cast<double>(1 << (4 * (s - d)));
+                const double q = -1.0 / M;   // exact power of two
+                for (int j = 1; j < R; ++j)
+                    for (int kd = 0; kd < 16; ++kd)
+                        out[G::tw_off(s, d) + (j - 1) * 16 + kd] = cis_cycles(q, static_cast<double>(j * kd));
+            }
         }
     }
 }

@@ -51,7 +51,7 @@ cudaError_t launch_4step_row(int log2C, int mode, void* Y, int log2R, long long 
                              int conj_out, cudaStream_t st);
 
 // ---- fused Zoom FFT (kernels_zoom.cu) --------------------------------------------------
-constexpr int kZoomK = 8;   // FIR outputs per thread
+constexpr int kZoomK = 4;   // FIR outputs per thread
 struct ZoomArgs {
     long long n;       // samples per trace
     long long U;       // usable length (circular) or n (linear)

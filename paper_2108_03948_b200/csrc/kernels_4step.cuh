@@ -39,6 +39,9 @@ k4_col(const void* __restrict__ xin, int in_kind, int conj_in, long long x_strid
     const int g = threadIdx.x % TC;
     const int tid = threadIdx.x / TC;
     C* sm = reinterpret_cast<C*>(smraw) + g * REG;
+    C* tws = reinterpret_cast<C*>(smraw) + TC * REG;
+    load_twiddles<LOG2R>(tws, tw);
+    __syncthreads();
     const long long Cn = 1LL << log2C;
     const long long tiles = Cn / TC;
     const long long b = blockIdx.x / tiles;
@@ -62,7 +65,7 @@ k4_col(const void* __restrict__ xin, int in_kind, int conj_in, long long x_strid
         }
         v[q] = val;
     }
-    block_fft<INV, LOG2R>(v, sm, tw, tid);
+    block_fft<INV, LOG2R>(v, sm, tws, tid);
 #pragma unroll
     for (int q = 0; q < G::EPT; ++q) {
         const long long k1 = tid + (long long)G::NT * q;
@@ -106,6 +109,9 @@ k4_row(cx_t<T>* __restrict__ Y, int log2R, long long batch, const cx_t<T>* __res
         tid = threadIdx.x % G::NT;
     }
     C* sm = reinterpret_cast<C*>(smraw) + g * (G::SMEM + 1);
+    C* tws = reinterpret_cast<C*>(smraw) + rows_per_cta * (G::SMEM + 1);
+    load_twiddles<LOG2C>(tws, tw);
+    __syncthreads();
     const long long tiles = R / rows_per_cta;
     const long long b = blockIdx.x / tiles;
     const long long k1 = (blockIdx.x % tiles) * rows_per_cta + g;
@@ -113,7 +119,7 @@ k4_row(cx_t<T>* __restrict__ Y, int log2R, long long batch, const cx_t<T>* __res
     C v[G::EPT];
 #pragma unroll
     for (int q = 0; q < G::EPT; ++q) v[q] = row[tid + G::NT * q];
-    block_fft<false, LOG2C>(v, sm, tw, tid);
+    block_fft<false, LOG2C>(v, sm, tws, tid);
     if constexpr (MODE == 0) {
         C* o = out + b * out_stride;
 #pragma unroll
@@ -127,7 +133,7 @@ k4_row(cx_t<T>* __restrict__ Y, int log2R, long long batch, const cx_t<T>* __res
         const C* kp = khat_p + k1 * Cn;
 #pragma unroll
         for (int q = 0; q < G::EPT; ++q) v[q] = cmul(v[q], __ldg(kp + tid + G::NT * q));
-        block_fft<true, LOG2C>(v, sm, tw, tid);
+        block_fft<true, LOG2C>(v, sm, tws, tid);
         const C* t = twL + k1 * Cn;
 #pragma unroll
         for (int q = 0; q < G::EPT; ++q) {
@@ -151,7 +157,7 @@ cudaError_t launch_4step_col_impl(int log2R, bool inverse, int in_kind, int conj
         constexpr int LG = decltype(lg)::value;
         using G = FftGeom<LG>;
         constexpr int TC = Tile<T>::W;
-        const size_t smem = (size_t)TC * (G::SMEM + 1) * sizeof(C);
+        const size_t smem = ((size_t)TC * (G::SMEM + 1) + G::TW_ALLOC) * sizeof(C);
         const long long tiles = (1LL << log2C) / TC;
         auto launch = [&](auto kern) {
             cudaError_t e = prep_smem(kern, smem);
@@ -176,7 +182,7 @@ cudaError_t launch_4step_row_impl(int log2C, int mode, void* Y, int log2R, long 
         const long long R = 1LL << log2R;
         if (mode == 0) {
             constexpr int TR = Tile<T>::W;
-            const size_t smem = (size_t)TR * (G::SMEM + 1) * sizeof(C);
+            const size_t smem = ((size_t)TR * (G::SMEM + 1) + G::TW_ALLOC) * sizeof(C);
             auto kern = k4_row<T, LG, 0>;
             cudaError_t e = prep_smem(kern, smem);
             if (e != cudaSuccess) return e;
@@ -185,7 +191,7 @@ cudaError_t launch_4step_row_impl(int log2C, int mode, void* Y, int log2R, long 
                                                                        out_stride, scale, conj_out);
         } else {
             using K = KCfg<T, LG>;
-            const size_t smem = (size_t)K::GROUPS * (G::SMEM + 1) * sizeof(C);
+            const size_t smem = ((size_t)K::GROUPS * (G::SMEM + 1) + G::TW_ALLOC) * sizeof(C);
             auto kern = k4_row<T, LG, 1>;
             cudaError_t e = prep_smem(kern, smem);
             if (e != cudaSuccess) return e;

@@ -13,9 +13,10 @@ template <typename T, int LOG2L> struct KCfg {
     using G = FftGeom<LOG2L>;
     static constexpr int GROUPS = G::NT >= 128 ? 1 : 128 / G::NT;   // transforms per CTA
     static constexpr int BLOCK = G::NT * GROUPS;
-    static constexpr size_t SMEM_BYTES = (size_t)GROUPS * G::SMEM * sizeof(cx_t<T>);
-    // cap registers at 128/thread (>= 2 CTAs of 256 threads per SM) unless the block is 1024 wide
-    static constexpr int MINB = BLOCK >= 1024 ? 1 : (BLOCK >= 512 ? 1 : 512 / BLOCK);
+    // [GROUPS padded data regions][factorised twiddle tables]
+    static constexpr size_t SMEM_BYTES = ((size_t)GROUPS * G::SMEM + (G::L >= 16 ? G::TW_ALLOC : 0)) * sizeof(cx_t<T>);
+    // cap registers at 128/thread (>= 2 CTAs of 256 threads per SM) unless the block is wider
+    static constexpr int MINB = BLOCK >= 512 ? 1 : 512 / BLOCK;
 };
 
 template <typename K> inline cudaError_t prep_smem(K kernel, size_t bytes) {
@@ -25,29 +26,55 @@ template <typename K> inline cudaError_t prep_smem(K kernel, size_t bytes) {
 
 inline unsigned grid_for(long long batch, int groups) { return (unsigned)((batch + groups - 1) / groups); }
 
+// persistent grid: as many CTAs as fit on the device at once (capped by the work)
+template <typename K> inline unsigned persistent_grid(K kernel, int block, size_t smem, long long units) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    const long long cap = (long long)per_sm * sms;
+    return (unsigned)(units < cap ? (units > 0 ? units : 1) : cap);
+}
+
+// common prologue: shared-memory carve-up and the twiddle tables
+#define SKG_PROLOGUE(T, LG)                                                                        \
+    using C = cx_t<T>;                                                                             \
+    using G = FftGeom<LG>;                                                                         \
+    using K = KCfg<T, LG>;                                                                         \
+    extern __shared__ __align__(16) unsigned char smraw[];                                         \
+    C* sm = reinterpret_cast<C*>(smraw) + (threadIdx.x / G::NT) * G::SMEM;                         \
+    C* tws = reinterpret_cast<C*>(smraw) + K::GROUPS * G::SMEM;                                    \
+    if constexpr (G::L >= 16) load_twiddles<LG>(tws, tw);                                          \
+    __syncthreads();                                                                               \
+    const int tid = threadIdx.x % G::NT;                                                           \
+    const int gid = threadIdx.x / G::NT;
+
 // ---------------------------------------------------------------------------------------
 // complex -> complex (FftPlan::forward/inverse, numerics.cpp:73-100; fft/ifft 102-120)
 template <typename T, int LOG2L, bool INV>
 __global__ void __launch_bounds__(KCfg<T, LOG2L>::BLOCK, KCfg<T, LOG2L>::MINB)
 k_fft_c2c(const cx_t<T>* in, long long in_stride, cx_t<T>* out, long long out_stride, long long batch,
           const cx_t<T>* __restrict__ tw, T scale) {
-    using C = cx_t<T>;
-    using G = FftGeom<LOG2L>;
-    using K = KCfg<T, LOG2L>;
-    extern __shared__ __align__(16) unsigned char smraw[];
-    C* sm = reinterpret_cast<C*>(smraw) + (threadIdx.x / G::NT) * G::SMEM;
-    const int tid = threadIdx.x % G::NT;
-    const long long b = (long long)blockIdx.x * K::GROUPS + threadIdx.x / G::NT;
-    const bool active = b < batch;
-    C v[G::EPT];
-    const C* src = in + b * in_stride;
+    SKG_PROLOGUE(T, LOG2L)
+    for (long long base = (long long)blockIdx.x * K::GROUPS; base < batch; base += (long long)gridDim.x * K::GROUPS) {
+        const long long b = base + gid;
+        const bool active = b < batch;
+        C v[G::EPT];
+        const C* src = in + b * in_stride;
 #pragma unroll
-    for (int q = 0; q < G::EPT; ++q) v[q] = active ? src[tid + G::NT * q] : czero<C>();
-    block_fft<INV, LOG2L>(v, sm, tw, tid);
-    if (active) {
-        C* dst = out + b * out_stride;
+        for (int q = 0; q < G::EPT; ++q) v[q] = active ? src[tid + G::NT * q] : czero<C>();
+        block_fft<INV, LOG2L>(v, sm, tws, tid);
+        if (active) {
+            C* dst = out + b * out_stride;
 #pragma unroll
-        for (int q = 0; q < G::EPT; ++q) dst[tid + G::NT * q] = cscale(v[q], scale);
+            for (int q = 0; q < G::EPT; ++q) dst[tid + G::NT * q] = cscale(v[q], scale);
+        }
+        __syncthreads();
     }
 }
 
@@ -61,77 +88,75 @@ k_fft_r2c(const T* __restrict__ x, long long x_stride, long long N, int vec, lon
           const cx_t<T>* __restrict__ tw, const cx_t<T>* __restrict__ post, int mode, cx_t<T>* __restrict__ out,
           long long out_stride, const cx_t<T>* __restrict__ rtab, T* __restrict__ mag, T* __restrict__ phase,
           long long mp_stride) {
-    using C = cx_t<T>;
-    using G = FftGeom<LOG2M>;
-    using K = KCfg<T, LOG2M>;
+    SKG_PROLOGUE(T, LOG2M)
     constexpr int M = G::L;
     constexpr long long L = 2LL * M;
-    extern __shared__ __align__(16) unsigned char smraw[];
-    C* sm = reinterpret_cast<C*>(smraw) + (threadIdx.x / G::NT) * G::SMEM;
-    const int tid = threadIdx.x % G::NT;
-    const long long b = (long long)blockIdx.x * K::GROUPS + threadIdx.x / G::NT;
-    const bool active = b < batch;
-    C v[G::EPT];
-    const T* xs = x + b * x_stride;
     const long long half = N >> 1;
+    for (long long base = (long long)blockIdx.x * K::GROUPS; base < batch; base += (long long)gridDim.x * K::GROUPS) {
+        const long long b = base + gid;
+        const bool active = b < batch;
+        C v[G::EPT];
+        const T* xs = x + b * x_stride;
 #pragma unroll
-    for (int q = 0; q < G::EPT; ++q) {
-        v[q] = czero<C>();
-        if (q < NZ && active) {
-            const long long pos = tid + (long long)G::NT * q;
-            if (vec) {
-                if (pos < half) v[q] = __ldg(reinterpret_cast<const C*>(xs) + pos);
-                else if (2 * pos < N) v[q] = mk<C>(xs[2 * pos], (T)0);
-            } else {
-                if (2 * pos < N) v[q].x = xs[2 * pos];
-                if (2 * pos + 1 < N) v[q].y = xs[2 * pos + 1];
+        for (int q = 0; q < G::EPT; ++q) {
+            v[q] = czero<C>();
+            if (q < NZ && active) {
+                const long long pos = tid + (long long)G::NT * q;
+                if (vec) {
+                    if (pos < half) v[q] = __ldg(reinterpret_cast<const C*>(xs) + pos);
+                    else if (2 * pos < N) v[q] = mk<C>(xs[2 * pos], (T)0);
+                } else {
+                    if (2 * pos < N) v[q].x = xs[2 * pos];
+                    if (2 * pos + 1 < N) v[q].y = xs[2 * pos + 1];
+                }
             }
         }
-    }
-    block_fft<false, LOG2M, NZ>(v, sm, tw, tid);
-
-    // pair Z[k] with Z[M-k]
-    if constexpr (G::NT > 1) {
+        block_fft<false, LOG2M, NZ>(v, sm, tws, tid);
+        // pair Z[k] with Z[M-k]
+        if constexpr (G::NT > 1) {
 #pragma unroll
-        for (int q = 0; q < G::EPT; ++q) sm[pad16(tid + G::NT * q)] = v[q];
+            for (int q = 0; q < G::EPT; ++q) sm[pad16(tid + G::NT * q)] = v[q];
+            __syncthreads();
+        }
+        if (active) {
+#pragma unroll
+            for (int q = 0; q < G::EPT; ++q) {
+                const int k = tid + G::NT * q;
+                C c;
+                if constexpr (G::NT == 1) c = v[(M - q) & (M - 1)];
+                else c = sm[pad16((M - k) & (M - 1))];
+                const C z = v[q];
+                const C E = mk<C>((T)0.5 * (z.x + c.x), (T)0.5 * (z.y - c.y));
+                const C O = mk<C>((T)0.5 * (z.y + c.y), (T)0.5 * (c.x - z.x));
+                const C X = cadd(E, cmul(O, __ldg(post + k)));
+                C XM = czero<C>();
+                if (k == 0) XM = mk<C>(z.x - z.y, (T)0);   // Nyquist bin M (E - O at k = 0)
+                if (mode == 0) {
+                    C* o = out + b * out_stride;
+                    o[k] = X;
+                    if (k) o[L - k] = cconj(X);
+                    else o[M] = XM;
+                } else if (mode == 1) {
+                    C* o = out + b * out_stride;
+                    o[k] = X;
+                    if (k == 0) o[M] = XM;
+                } else {
+                    T* mg = mag + b * mp_stride;
+                    T* ph = phase + b * mp_stride;
+                    const C H = cmul(X, __ldg(rtab + k));
+                    mg[k] = sqrt(H.x * H.x + H.y * H.y);
+                    ph[k] = atan2(H.y, H.x);
+                    if (out) (out + b * out_stride)[k] = H;
+                    if (k == 0) {
+                        const C HM = cmul(XM, __ldg(rtab + M));
+                        mg[M] = sqrt(HM.x * HM.x + HM.y * HM.y);
+                        ph[M] = atan2(HM.y, HM.x);
+                        if (out) (out + b * out_stride)[M] = HM;
+                    }
+                }
+            }
+        }
         __syncthreads();
-    }
-    if (!active) return;
-#pragma unroll
-    for (int q = 0; q < G::EPT; ++q) {
-        const int k = tid + G::NT * q;
-        C c;
-        if constexpr (G::NT == 1) c = v[(M - q) & (M - 1)];
-        else c = sm[pad16((M - k) & (M - 1))];
-        const C z = v[q];
-        const C E = mk<C>((T)0.5 * (z.x + c.x), (T)0.5 * (z.y - c.y));
-        const C O = mk<C>((T)0.5 * (z.y + c.y), (T)0.5 * (c.x - z.x));
-        const C X = cadd(E, cmul(O, __ldg(post + k)));
-        C XM = czero<C>();
-        if (k == 0) XM = mk<C>(z.x - z.y, (T)0);   // Nyquist bin M (E - O at k = 0)
-        if (mode == 0) {
-            C* o = out + b * out_stride;
-            o[k] = X;
-            if (k) o[L - k] = cconj(X);
-            else o[M] = XM;
-        } else if (mode == 1) {
-            C* o = out + b * out_stride;
-            o[k] = X;
-            if (k == 0) o[M] = XM;
-        } else {
-            T* mg = mag + b * mp_stride;
-            T* ph = phase + b * mp_stride;
-            const C H = cmul(X, __ldg(rtab + k));
-            mg[k] = sqrt(H.x * H.x + H.y * H.y);
-            ph[k] = atan2(H.y, H.x);
-            if (out) (out + b * out_stride)[k] = H;
-            if (k == 0) {
-                const C HM = cmul(XM, __ldg(rtab + M));
-                mg[M] = sqrt(HM.x * HM.x + HM.y * HM.y);
-                ph[M] = atan2(HM.y, HM.x);
-                if (out) (out + b * out_stride)[M] = HM;
-            }
-        }
     }
 }
 
@@ -142,35 +167,34 @@ __global__ void __launch_bounds__(KCfg<T, LOG2L>::BLOCK, KCfg<T, LOG2L>::MINB)
 k_czt(const void* __restrict__ xin, int complex_in, long long x_stride, long long N, long long M, long long batch,
       cx_t<T>* __restrict__ out, long long out_stride, const cx_t<T>* __restrict__ tw,
       const cx_t<T>* __restrict__ cin, const cx_t<T>* __restrict__ khat, const cx_t<T>* __restrict__ cout) {
-    using C = cx_t<T>;
-    using G = FftGeom<LOG2L>;
-    using K = KCfg<T, LOG2L>;
-    extern __shared__ __align__(16) unsigned char smraw[];
-    C* sm = reinterpret_cast<C*>(smraw) + (threadIdx.x / G::NT) * G::SMEM;
-    const int tid = threadIdx.x % G::NT;
-    const long long b = (long long)blockIdx.x * K::GROUPS + threadIdx.x / G::NT;
-    const bool active = b < batch;
-    C v[G::EPT];
+    SKG_PROLOGUE(T, LOG2L)
+    for (long long base = (long long)blockIdx.x * K::GROUPS; base < batch; base += (long long)gridDim.x * K::GROUPS) {
+        const long long b = base + gid;
+        const bool active = b < batch;
+        C v[G::EPT];
 #pragma unroll
-    for (int q = 0; q < G::EPT; ++q) {
-        v[q] = czero<C>();
-        const long long pos = tid + (long long)G::NT * q;
-        if (q < NZ && active && pos < N) {
-            const C ch = __ldg(cin + pos);
-            if (complex_in) v[q] = cmul(__ldg(reinterpret_cast<const C*>(xin) + b * x_stride + pos), ch);
-            else v[q] = rmul(__ldg(reinterpret_cast<const T*>(xin) + b * x_stride + pos), ch);
+        for (int q = 0; q < G::EPT; ++q) {
+            v[q] = czero<C>();
+            const long long pos = tid + (long long)G::NT * q;
+            if (q < NZ && active && pos < N) {
+                const C ch = __ldg(cin + pos);
+                if (complex_in) v[q] = cmul(__ldg(reinterpret_cast<const C*>(xin) + b * x_stride + pos), ch);
+                else v[q] = rmul(__ldg(reinterpret_cast<const T*>(xin) + b * x_stride + pos), ch);
+            }
         }
-    }
-    block_fft<false, LOG2L, NZ>(v, sm, tw, tid);
+        block_fft<false, LOG2L, NZ>(v, sm, tws, tid);
 #pragma unroll
-    for (int q = 0; q < G::EPT; ++q) v[q] = cmul(v[q], __ldg(khat + tid + G::NT * q));
-    block_fft<true, LOG2L, 16, NO>(v, sm, tw, tid);
-    if (!active) return;
-    C* o = out + b * out_stride;
+        for (int q = 0; q < G::EPT; ++q) v[q] = cmul(v[q], __ldg(khat + tid + G::NT * q));
+        block_fft<true, LOG2L, 16, NO>(v, sm, tws, tid);
+        if (active) {
+            C* o = out + b * out_stride;
 #pragma unroll
-    for (int q = 0; q < G::EPT; ++q) {
-        const long long pos = tid + (long long)G::NT * q;
-        if (q < NO && pos < M) o[pos] = cmul(v[q], __ldg(cout + pos));
+            for (int q = 0; q < G::EPT; ++q) {
+                const long long pos = tid + (long long)G::NT * q;
+                if (q < NO && pos < M) o[pos] = cmul(v[q], __ldg(cout + pos));
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -185,7 +209,7 @@ cudaError_t run_c2c(const void* in, long long in_stride, void* out, long long ou
     auto kern = k_fft_c2c<T, LOG2L, INV>;
     cudaError_t e = prep_smem(kern, K::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    kern<<<grid_for(batch, K::GROUPS), K::BLOCK, K::SMEM_BYTES, st>>>(
+    kern<<<persistent_grid(kern, K::BLOCK, K::SMEM_BYTES, grid_for(batch, K::GROUPS)), K::BLOCK, K::SMEM_BYTES, st>>>(
         (const C*)in, in_stride, (C*)out, out_stride, batch, (const C*)tw, scale);
     return cudaGetLastError();
 }
@@ -200,7 +224,7 @@ cudaError_t run_r2c(long long N, const T* x, long long x_stride, long long batch
     cudaError_t e = prep_smem(kern, K::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     const int vec = ((N & 1) == 0 && (x_stride & 1) == 0 && ((uintptr_t)x % (2 * sizeof(T))) == 0) ? 1 : 0;
-    kern<<<grid_for(batch, K::GROUPS), K::BLOCK, K::SMEM_BYTES, st>>>(
+    kern<<<persistent_grid(kern, K::BLOCK, K::SMEM_BYTES, grid_for(batch, K::GROUPS)), K::BLOCK, K::SMEM_BYTES, st>>>(
         x, x_stride, N, vec, batch, (const C*)tw, (const C*)post, mode, (C*)out, out_stride, (const C*)rtab,
         mag, phase, mp_stride);
     return cudaGetLastError();
@@ -215,7 +239,7 @@ cudaError_t run_czt(long long N, long long M, bool complex_in, const void* x, lo
     auto kern = k_czt<T, LOG2L, NZ, NO>;
     cudaError_t e = prep_smem(kern, K::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    kern<<<grid_for(batch, K::GROUPS), K::BLOCK, K::SMEM_BYTES, st>>>(
+    kern<<<persistent_grid(kern, K::BLOCK, K::SMEM_BYTES, grid_for(batch, K::GROUPS)), K::BLOCK, K::SMEM_BYTES, st>>>(
         x, complex_in ? 1 : 0, x_stride, N, M, batch, (C*)out, out_stride, (const C*)tw, (const C*)cin,
         (const C*)khat, (const C*)cout);
     return cudaGetLastError();

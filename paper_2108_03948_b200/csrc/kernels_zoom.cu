@@ -25,8 +25,13 @@ constexpr int ZK = kZoomK;   // outputs per thread (register window)
 
 __host__ __device__ inline int zpad(int r) { return r + r / ZK; }
 
+template <int LOG2N> struct ZoomCfg {
+    static constexpr int NT = FftGeom<LOG2N>::NT;
+    static constexpr int NTH = NT > 128 ? NT : 128;   // CTA width
+};
+
 template <typename T, int LOG2N>
-__global__ void __launch_bounds__(FftGeom<LOG2N>::NT > 64 ? FftGeom<LOG2N>::NT : 64)
+__global__ void __launch_bounds__(ZoomCfg<LOG2N>::NTH)
 k_zoom(const T* __restrict__ x, long long x_stride, long long batch, ZoomArgs a,
        const cx_t<T>* __restrict__ gph,     // taps by phase row: gph[ph * lh + l] = g[l D + (D - ph) % D]
        const cx_t<T>* __restrict__ S,       // S[m], m < nout (already offset by trim)
@@ -34,41 +39,55 @@ k_zoom(const T* __restrict__ x, long long x_stride, long long batch, ZoomArgs a,
        long long out_stride) {
     using C = cx_t<T>;
     using G = FftGeom<LOG2N>;
-    constexpr int NTH = G::NT > 64 ? G::NT : 64;
+    constexpr int NTH = ZoomCfg<LOG2N>::NTH;
     extern __shared__ __align__(16) unsigned char smraw[];
-    // shared layout: [FFT buffer: G::SMEM complex][wrap terms: mwrap complex][polyphase rows]
+    // shared layout: [FFT buffer][twiddles][wrap terms: mwrap complex][polyphase rows]
     C* fb = reinterpret_cast<C*>(smraw);
-    C* cw = fb + (G::L + (G::L >> 4) + 1);
+    C* tws = fb + (G::L + (G::L >> 4) + 1);
+    C* cw = tws + G::TW_ALLOC;
     T* xs = reinterpret_cast<T*>(cw + (a.mwrap + 1));
     const long long b = blockIdx.x;
     const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
     const T* xr = x + b * x_stride;
     const int D = a.D;
+    const int U = (int)a.U;
+    const bool dpow2 = (D & (D - 1)) == 0;
+    const int ld = 31 - __clz(D);
 
-    // 1. load the trace into the polyphase rows; zero prefix and tail; clear the FFT buffer
+    // 1. trace -> polyphase rows (zero prefix and tail); clear the FFT buffer; twiddles
+    if constexpr (G::L >= 16) load_twiddles<LOG2N>(tws, tw);
     const int total = D * a.rs;
     for (int i = tid; i < total; i += NTH) xs[i] = (T)0;
     for (int i = tid; i < G::L; i += NTH) fb[pad16(i)] = czero<C>();
     __syncthreads();
-    for (long long n = tid; n < a.U; n += NTH) {
-        const int ph = (int)(n % D);
-        const int r = (int)(n / D);
+    for (int n = tid; n < U; n += NTH) {
+        const int ph = dpow2 ? (n & (D - 1)) : n % D;
+        const int r = dpow2 ? (n >> ld) : n / D;
         xs[ph * a.rs + zpad(r + a.pre)] = __ldg(xr + n);
     }
     __syncthreads();
 
-    // wrap correction (circular): cw[m] = w * sum_{t > mD} g[t] x[U + mD - t], m < mwrap
+    // wrap correction (circular): cw[m] = w * sum_{t > mD} g[t] x[U + mD - t], m < mwrap;
+    // one warp per output, lanes stride the taps, shuffle reduction
     if (a.circular) {
-        for (int m = tid; m < a.mwrap; m += NTH) {
+        for (int m = warp; m < a.mwrap; m += NTH / 32) {
             C acc = czero<C>();
-            for (int t = m * D + 1; t < a.T; ++t) {
-                const long long j = a.U + (long long)m * D - t;
-                const int ph = (int)(j % D), r = (int)(j / D);
-                const int trow = (D - (t % D)) % D;   // phase row holding tap t
-                const C g = __ldg(gph + trow * a.lh + t / D);
+            for (int t = m * D + 1 + lane; t < a.T; t += 32) {
+                const int j = U + m * D - t;
+                const int ph = dpow2 ? (j & (D - 1)) : j % D;
+                const int r = dpow2 ? (j >> ld) : j / D;
+                const int tm = dpow2 ? (t & (D - 1)) : t % D;
+                const int trow = tm ? D - tm : 0;   // phase row holding tap t
+                const C g = __ldg(gph + trow * a.lh + (dpow2 ? (t >> ld) : t / D));
                 acc = cadd(acc, rmul(xs[ph * a.rs + zpad(r + a.pre)], g));
             }
-            cw[m] = cmul(acc, mk<C>((T)a.wre, (T)a.wim));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+            }
+            if (lane == 0) cw[m] = cmul(acc, mk<C>((T)a.wre, (T)a.wim));
         }
         __syncthreads();
     }
@@ -126,7 +145,7 @@ k_zoom(const T* __restrict__ x, long long x_stride, long long batch, ZoomArgs a,
 #pragma unroll
     for (int q = 0; q < G::EPT; ++q) v[q] = act ? fb[pad16(tid + G::NT * q)] : czero<C>();
     __syncthreads();
-    block_fft<false, LOG2N>(v, fb, tw, act ? tid : 0, act);
+    block_fft<false, LOG2N>(v, fb, tws, act ? tid : 0, act);
     if (act) {
 #pragma unroll
         for (int q = 0; q < G::EPT; ++q) fb[pad16(tid + G::NT * q)] = v[q];
@@ -148,8 +167,8 @@ static cudaError_t run_zoom(const ZoomArgs& a, const T* x, long long x_stride, l
                             cudaStream_t st) {
     using C = cx_t<T>;
     using G = FftGeom<LOG2N>;
-    constexpr int NTH = G::NT > 64 ? G::NT : 64;
-    constexpr int kFb = G::L + (G::L >> 4) + 1;
+    constexpr int NTH = ZoomCfg<LOG2N>::NTH;
+    constexpr int kFb = G::L + (G::L >> 4) + 1 + G::TW_ALLOC;
     const size_t smem = (size_t)(kFb + a.mwrap + 1) * sizeof(C) + (size_t)a.D * a.rs * sizeof(T);
     auto kern = k_zoom<T, LOG2N>;
     cudaError_t e = prep_smem(kern, smem);
@@ -205,6 +224,11 @@ namespace skg {
 size_t zoom_smem_bytes(const ZoomArgs& a, int log2n, bool f32) {
     const size_t L = size_t{1} << log2n;
     const size_t cs = f32 ? 8 : 16, rs = f32 ? 4 : 8;
-    return (L + (L >> 4) + 1 + a.mwrap + 1) * cs + (size_t)a.D * a.rs * rs;
+    int tw = 1;
+    dispatch_log2<1, 14>(log2n, [&](auto lg) {
+        tw = FftGeom<decltype(lg)::value>::TW_ALLOC;
+        return cudaSuccess;
+    });
+    return (L + (L >> 4) + 1 + tw + a.mwrap + 1) * cs + (size_t)a.D * a.rs * rs;
 }
 }  // namespace skg
