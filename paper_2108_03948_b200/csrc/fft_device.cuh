@@ -75,6 +75,35 @@ template <bool INV, typename C> __device__ __forceinline__ C mul_cs(C a, sc_t<C>
     return INV ? mk<C>(a.x * c - a.y * s, a.y * c + a.x * s) : mk<C>(a.x * c + a.y * s, a.y * c - a.x * s);
 }
 
+// ---- epilogue math ----------------------------------------------------------------------------
+// fp32 atan2: odd minimax polynomial for atan on [0, 1] (degree 15, max error 1.4e-7 rad in fp32
+// arithmetic, i.e. at the level of atan2f's own ~2 ulp) plus octant fixups; ~20 instructions.
+__device__ __forceinline__ float fast_atan2f(float y, float x) {
+    const float ax = fabsf(x), ay = fabsf(y);
+    const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+    const float a = mx > 0.0f ? __fdividef(mn, mx) : 0.0f;
+    const float s = a * a;
+    float r = -0.004054566379636526f;
+    r = fmaf(r, s, 0.02186295948922634f);
+    r = fmaf(r, s, -0.055912334471940994f);
+    r = fmaf(r, s, 0.0964219868183136f);
+    r = fmaf(r, s, -0.1390863060951233f);
+    r = fmaf(r, s, 0.19946566224098206f);
+    r = fmaf(r, s, -0.33329859375953674f);
+    r = fmaf(r, s, 0.9999993443489075f);
+    r *= a;
+    if (ay > ax) r = 1.57079632679489662f - r;
+    if (x < 0.0f) r = 3.14159265358979324f - r;
+    return copysignf(r, y);
+}
+__device__ __forceinline__ double atan2_t(double y, double x) { return atan2(y, x); }
+__device__ __forceinline__ float atan2_t(float y, float x) { return fast_atan2f(y, x); }
+__device__ __forceinline__ double abs_t(double x, double y) { return hypot(x, y); }
+__device__ __forceinline__ float abs_t(float x, float y) {
+    const float h = fmaf(x, x, y * y);
+    return h > 0.0f ? h * rsqrtf(h) : 0.0f;
+}
+
 // ---- small DFTs, natural order in and out.
 // NZ = number of leading inputs that may be nonzero, NO = number of leading outputs needed.
 template <bool INV, int NZ = 4, int NO = 4, typename C>

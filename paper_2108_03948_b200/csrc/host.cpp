@@ -317,30 +317,52 @@ CztPlanG::CztPlanG(size_t n, cd a, cd w, size_t m) : n_(n), m_(m) {
         throw std::invalid_argument("czt: a and w must be nonzero");
     if (n == 0) throw std::invalid_argument("CztPlan: empty input length");
     L_ = next_pow2(n + m - 1);
-    log2L_ = ilog2(L_);
-    const PolarPow A(a), W(w);
-    // czt.cpp:90-112 — same table formulas, fp64
-    cin_.resize(n);
-    for (size_t i = 0; i < n; ++i) {
-        const double t = static_cast<double>(i);
-        cin_[i] = A.pow(-t) * W.pow(0.5 * t * t);
+    // Output segmentation: X[s M' + k'] for k' < M' is the chirp-z transform with start
+    // A_s = A W^{-s M'} and the same W, so the m bins can run as S independent transforms of
+    // length Ls = next_pow2(n + M' - 1) that share the kernel spectrum and the output chirp. Pick S
+    // minimising S Ls log2 Ls (transforms that fit one CTA preferred): for configs[1]
+    // (n=1024, m=2048) this is S=2, Ls=2048 — slightly less arithmetic than one 4096-point pair
+    // and half the shared memory per CTA, i.e. twice the resident CTAs per SM.
+    double best = 0.0;
+    for (size_t S = 1; S <= m; S *= 2) {
+        const size_t seg = (m + S - 1) / S;
+        const size_t Ls = next_pow2(n + seg - 1);
+        double cost = static_cast<double>((m + seg - 1) / seg) * static_cast<double>(Ls) * ilog2(Ls);
+        if (ilog2(Ls) > single_cta_max_log2(false)) cost *= 1.5;   // multi-pass: work buffer round trips
+        if (S == 1 || cost < best * 0.999) {
+            best = cost;
+            nseg_ = (m + seg - 1) / seg;
+            seg_ = seg;
+            Ls_ = Ls;
+        }
+        if (seg == 1) break;
     }
-    cout_.resize(m);
-    for (size_t k = 0; k < m; ++k) {
+    log2L_ = ilog2(Ls_);
+    if (log2L_ > 20)
+        throw std::invalid_argument("czt: convolution length " + std::to_string(Ls_) +
+                                    " exceeds the supported maximum 2^20");
+    const PolarPow A(a), W(w);
+    // czt.cpp:90-112, per segment: input chirp A^{-i} W^{i^2/2 + s M' i} (one fma-split phase)
+    cin_.resize(nseg_ * n);
+    for (size_t sg = 0; sg < nseg_; ++sg)
+        for (size_t i = 0; i < n; ++i) {
+            const double t = static_cast<double>(i);
+            cin_[sg * n + i] = A.pow(-t) * W.pow(0.5 * t * t + static_cast<double>(sg * seg_) * t);
+        }
+    cout_.resize(seg_);
+    for (size_t k = 0; k < seg_; ++k) {
         const double t = static_cast<double>(k);
         cout_[k] = W.pow(0.5 * t * t);
     }
-    kern_.assign(L_, cd(0.0, 0.0));
-    for (size_t k = 0; k < m; ++k) {
+    kern_.assign(Ls_, cd(0.0, 0.0));
+    for (size_t k = 0; k < seg_; ++k) {
         const double t = static_cast<double>(k);
         kern_[k] = W.pow(-0.5 * t * t);
     }
     for (size_t i = 1; i < n; ++i) {
         const double t = static_cast<double>(i);
-        kern_[L_ - i] = W.pow(-0.5 * t * t);
+        kern_[Ls_ - i] = W.pow(-0.5 * t * t);
     }
-    if (log2L_ > 20)
-        throw std::invalid_argument("czt: convolution length " + std::to_string(L_) + " exceeds the supported maximum 2^20");
 }
 
 const CztPlanG::Dev& CztPlanG::dev(bool f32) const {
@@ -352,22 +374,22 @@ const CztPlanG::Dev& CztPlanG::dev(bool f32) const {
         // kernel spectrum: forward FFT of the circular chirp on the GPU in fp64, scaled by 1/L so the
         // inverse transform of the fused kernel needs no extra pass (czt.cpp:113, numerics.cpp:93-96)
         DevMem k64 = to_device(kern_, false);
-        fft_c2c(L_, false, false, k64.p, 0, k64.p, 0, 1, nullptr);
-        check(launch_scale_c64(k64.p, (long long)L_, 1.0 / static_cast<double>(L_), nullptr), "scale");
+        fft_c2c(Ls_, false, false, k64.p, 0, k64.p, 0, 1, nullptr);
+        check(launch_scale_c64(k64.p, (long long)Ls_, 1.0 / static_cast<double>(Ls_), nullptr), "scale");
         count_launch();
         if (log2L_ > single_cta_max_log2(f32)) {
             // four-step layout: khat_p[k1][k2] = khat[k1 + R k2]
             const int lR = log2L_ / 2, lC = log2L_ - lR;
             const size_t R = size_t{1} << lR, Cn = size_t{1} << lC;
-            std::vector<cd> h(L_), p(L_);
-            check(cudaMemcpy(h.data(), k64.p, L_ * sizeof(cd), cudaMemcpyDeviceToHost), "D2H khat");
+            std::vector<cd> h(Ls_), p(Ls_);
+            check(cudaMemcpy(h.data(), k64.p, Ls_ * sizeof(cd), cudaMemcpyDeviceToHost), "D2H khat");
             for (size_t k1 = 0; k1 < R; ++k1)
                 for (size_t k2 = 0; k2 < Cn; ++k2) p[k1 * Cn + k2] = h[k1 + R * k2];
-            k64.upload(p.data(), L_ * sizeof(cd));
+            k64.upload(p.data(), Ls_ * sizeof(cd));
         }
         if (f32) {
-            DevMem k32(L_ * 2 * sizeof(float));
-            check(launch_c64_to_c32(k64.p, k32.p, (long long)L_, nullptr), "convert");
+            DevMem k32(Ls_ * 2 * sizeof(float));
+            check(launch_c64_to_c32(k64.p, k32.p, (long long)Ls_, nullptr), "convert");
             count_launch();
             d.khat = std::move(k32);
         } else {
@@ -392,35 +414,43 @@ void CztPlanG::execute(const void* x, bool complex_in, long long x_stride, long 
         for (long long b0 = 0; b0 < batch; b0 += ch) {
             const long long nb = std::min(ch, batch - b0);
             const void* src = static_cast<const char*>(x) + (size_t)b0 * x_stride * es;
-            void* dst = static_cast<char*>(out) + (size_t)b0 * out_stride * cs;
-            cudaError_t e1, e2, e3;
-            if (f32) {
-                e1 = launch_4step_col<float>(f.lR, false, kind, 0, src, x_stride, N, d.cin.p, Y.p, f.lC, nb, f.twR, f.twL,
-                                             0, nullptr, 0, 0, nullptr, 1.0f, 0, st);
-                e2 = launch_4step_row<float>(f.lC, 1, Y.p, f.lR, nb, f.twC, f.twL, d.khat.p, nullptr, 0, 1.0f, 0, st);
-                e3 = launch_4step_col<float>(f.lR, true, 4, 0, nullptr, 0, 0, nullptr, Y.p, f.lC, nb, f.twR, f.twL, 1,
-                                             dst, out_stride, (long long)m_, d.cout.p, 1.0f, 0, st);
-            } else {
-                e1 = launch_4step_col<double>(f.lR, false, kind, 0, src, x_stride, N, d.cin.p, Y.p, f.lC, nb, f.twR,
-                                              f.twL, 0, nullptr, 0, 0, nullptr, 1.0, 0, st);
-                e2 = launch_4step_row<double>(f.lC, 1, Y.p, f.lR, nb, f.twC, f.twL, d.khat.p, nullptr, 0, 1.0, 0, st);
-                e3 = launch_4step_col<double>(f.lR, true, 4, 0, nullptr, 0, 0, nullptr, Y.p, f.lC, nb, f.twR, f.twL, 1,
-                                              dst, out_stride, (long long)m_, d.cout.p, 1.0, 0, st);
+            for (size_t sg = 0; sg < nseg_; ++sg) {
+                void* dst = static_cast<char*>(out) + ((size_t)b0 * out_stride + sg * seg_) * cs;
+                const void* cs_ = static_cast<const char*>(d.cin.p) + sg * n_ * cs;
+                const long long mh = (long long)std::min(seg_, m_ - sg * seg_);
+                cudaError_t e1, e2, e3;
+                if (f32) {
+                    e1 = launch_4step_col<float>(f.lR, false, kind, 0, src, x_stride, N, cs_, Y.p, f.lC, nb, f.twR,
+                                                 f.twL, 0, nullptr, 0, 0, nullptr, 1.0f, 0, st);
+                    e2 = launch_4step_row<float>(f.lC, 1, Y.p, f.lR, nb, f.twC, f.twL, d.khat.p, nullptr, 0, 1.0f, 0,
+                                                 st);
+                    e3 = launch_4step_col<float>(f.lR, true, 4, 0, nullptr, 0, 0, nullptr, Y.p, f.lC, nb, f.twR, f.twL,
+                                                 1, dst, out_stride, mh, d.cout.p, 1.0f, 0, st);
+                } else {
+                    e1 = launch_4step_col<double>(f.lR, false, kind, 0, src, x_stride, N, cs_, Y.p, f.lC, nb, f.twR,
+                                                  f.twL, 0, nullptr, 0, 0, nullptr, 1.0, 0, st);
+                    e2 = launch_4step_row<double>(f.lC, 1, Y.p, f.lR, nb, f.twC, f.twL, d.khat.p, nullptr, 0, 1.0, 0,
+                                                  st);
+                    e3 = launch_4step_col<double>(f.lR, true, 4, 0, nullptr, 0, 0, nullptr, Y.p, f.lC, nb, f.twR, f.twL,
+                                                  1, dst, out_stride, mh, d.cout.p, 1.0, 0, st);
+                }
+                check(e1, "czt 4step col");
+                check(e2, "czt 4step row");
+                check(e3, "czt 4step col inv");
+                count_launch(3);
             }
-            check(e1, "czt 4step col");
-            check(e2, "czt 4step row");
-            check(e3, "czt 4step col inv");
-            count_launch(3);
         }
         return;
     }
     const void* tw = stockham_twiddles(log2L_, f32);
     cudaError_t e;
     if (f32)
-        e = launch_czt<float>(log2L_, N, (long long)m_, complex_in, x, x_stride, batch, out, out_stride, tw,
+        e = launch_czt<float>(log2L_, N, (long long)m_, complex_in, x, x_stride, batch, (int)nseg_, (long long)seg_,
+                              out, out_stride, tw,
                               d.cin.p, d.khat.p, d.cout.p, st);
     else
-        e = launch_czt<double>(log2L_, N, (long long)m_, complex_in, x, x_stride, batch, out, out_stride, tw,
+        e = launch_czt<double>(log2L_, N, (long long)m_, complex_in, x, x_stride, batch, (int)nseg_,
+                               (long long)seg_, out, out_stride, tw,
                                d.cin.p, d.khat.p, d.cout.p, st);
     check(e, "czt launch");
     count_launch();

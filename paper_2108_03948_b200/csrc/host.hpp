@@ -79,7 +79,10 @@ class CztPlanG {
     CztPlanG(size_t n, cd a, cd w, size_t m);
     size_t input_size() const { return n_; }
     size_t output_size() const { return m_; }
-    size_t conv_size() const { return L_; }
+    size_t conv_size() const { return L_; }          // the reference's next_pow2(n + m - 1), czt.hpp:46
+    size_t segments() const { return nseg_; }        // output segments executed independently
+    size_t segment_len() const { return seg_; }
+    size_t segment_conv_size() const { return Ls_; } // transform length actually run per segment
     // x rows of n real (complex_in = false) or complex values; `load_n` <= n leading samples are
     // read (the rest are zeros — used by dft_any on zero-padded traces)
     void execute(const void* x, bool complex_in, long long x_stride, long long batch, void* out,
@@ -91,7 +94,8 @@ class CztPlanG {
     };
     const Dev& dev(bool f32) const;
     size_t n_, m_, L_;
-    int log2L_;
+    size_t nseg_ = 1, seg_ = 0, Ls_ = 0;
+    int log2L_;   // of Ls_
     std::vector<cd> cin_, cout_, kern_;
     mutable std::once_flag once_[2];
     mutable Dev dev_[2];

@@ -29,12 +29,14 @@ cudaError_t launch_fft_r2c(int log2M, long long N, const T* x, long long x_strid
                            const void* rtab, T* mag, T* phase, long long mp_stride, cudaStream_t st);
 
 // fused Bluestein CZT (czt.cpp:116-130): x * chirp_in -> FFT_L -> * khat (pre-scaled by 1/L)
-// -> IFFT_L -> * chirp_out, first M bins stored. x real (T) or complex (cx<T>).
+// -> IFFT_L -> * chirp_out, first M bins stored. x real (T) or complex (cx<T>). The M outputs are
+// split into nseg segments of seg_len bins (segment s uses input chirp cin + s*N, shared khat and
+// output chirp); L is the convolution length of ONE segment.
 template <typename T>
 cudaError_t launch_czt(int log2L, long long N, long long M, bool complex_in, const void* x,
-                       long long x_stride, long long batch, void* out, long long out_stride,
-                       const void* tw, const void* cin, const void* khat, const void* cout,
-                       cudaStream_t st);
+                       long long x_stride, long long batch, int nseg, long long seg_len, void* out,
+                       long long out_stride, const void* tw, const void* cin, const void* khat,
+                       const void* cout, cudaStream_t st);
 
 // ---- four-step passes for L = R * C beyond one CTA (kernels_4step.cuh) ----------------------
 // in_kind: 0 complex x, 1 real x, 2 real x * chirp, 3 complex x * chirp, 4 work buffer Y
@@ -75,6 +77,12 @@ cudaError_t launch_zoom_f64(const ZoomArgs& a, int log2n, const double* x, long 
 cudaError_t launch_zoom_f32(const ZoomArgs& a, int log2n, const float* x, long long xs, long long batch,
                             const void* g, const void* S, const void* tw, const void* band, void* out,
                             long long os, cudaStream_t st);
+// unfused path: FIR/decimate into zb (rows of z_stride complex, first nout written), band gather
+cudaError_t launch_zoom_fir(const ZoomArgs& a, bool f32, const void* x, long long xs, long long batch, const void* g,
+                            const void* S, void* zb, long long z_stride, cudaStream_t st);
+cudaError_t launch_zoom_band(bool f32, const void* Z, long long z_stride, long long n_fft, int k_lo, int nbins,
+                             const void* band, void* out, long long out_stride, long long batch, cudaStream_t st);
+int zoom_chunk_rowlen(const ZoomArgs& a);
 // shared bytes the fused zoom kernel needs for this geometry
 size_t zoom_smem_bytes(const ZoomArgs& a, int log2n, bool f32);
 

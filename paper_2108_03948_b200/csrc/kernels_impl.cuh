@@ -82,10 +82,10 @@ k_fft_c2c(const cx_t<T>* in, long long in_stride, cx_t<T>* out, long long out_st
 // real input, zero padded to L = 2M: M-point complex FFT of z[n] = x[2n] + i x[2n+1], then
 // X[k] = E[k] + W_L^k O[k] with E/O split from Z[k], conj Z[M-k]. Replaces fft_spectrum's
 // zero_pad + dft_any (spectra.cpp:21-38) without ever materialising the zeros.
-template <typename T, int LOG2M, int NZ>
+template <typename T, int LOG2M, int NZ, int MODE>
 __global__ void __launch_bounds__(KCfg<T, LOG2M>::BLOCK, KCfg<T, LOG2M>::MINB)
 k_fft_r2c(const T* __restrict__ x, long long x_stride, long long N, int vec, long long batch,
-          const cx_t<T>* __restrict__ tw, const cx_t<T>* __restrict__ post, int mode, cx_t<T>* __restrict__ out,
+          const cx_t<T>* __restrict__ tw, const cx_t<T>* __restrict__ post, cx_t<T>* __restrict__ out,
           long long out_stride, const cx_t<T>* __restrict__ rtab, T* __restrict__ mag, T* __restrict__ phase,
           long long mp_stride) {
     SKG_PROLOGUE(T, LOG2M)
@@ -119,6 +119,9 @@ k_fft_r2c(const T* __restrict__ x, long long x_stride, long long N, int vec, lon
             __syncthreads();
         }
         if (active) {
+            C* o = out ? out + b * out_stride : nullptr;
+            T* mg = MODE == 2 ? mag + b * mp_stride : nullptr;
+            T* ph = MODE == 2 ? phase + b * mp_stride : nullptr;
 #pragma unroll
             for (int q = 0; q < G::EPT; ++q) {
                 const int k = tid + G::NT * q;
@@ -129,30 +132,27 @@ k_fft_r2c(const T* __restrict__ x, long long x_stride, long long N, int vec, lon
                 const C E = mk<C>((T)0.5 * (z.x + c.x), (T)0.5 * (z.y - c.y));
                 const C O = mk<C>((T)0.5 * (z.y + c.y), (T)0.5 * (c.x - z.x));
                 const C X = cadd(E, cmul(O, __ldg(post + k)));
-                C XM = czero<C>();
-                if (k == 0) XM = mk<C>(z.x - z.y, (T)0);   // Nyquist bin M (E - O at k = 0)
-                if (mode == 0) {
-                    C* o = out + b * out_stride;
+                if constexpr (MODE == 0) {
                     o[k] = X;
                     if (k) o[L - k] = cconj(X);
-                    else o[M] = XM;
-                } else if (mode == 1) {
-                    C* o = out + b * out_stride;
+                } else if constexpr (MODE == 1) {
                     o[k] = X;
-                    if (k == 0) o[M] = XM;
                 } else {
-                    T* mg = mag + b * mp_stride;
-                    T* ph = phase + b * mp_stride;
                     const C H = cmul(X, __ldg(rtab + k));
-                    mg[k] = sqrt(H.x * H.x + H.y * H.y);
-                    ph[k] = atan2(H.y, H.x);
-                    if (out) (out + b * out_stride)[k] = H;
-                    if (k == 0) {
-                        const C HM = cmul(XM, __ldg(rtab + M));
-                        mg[M] = sqrt(HM.x * HM.x + HM.y * HM.y);
-                        ph[M] = atan2(HM.y, HM.x);
-                        if (out) (out + b * out_stride)[M] = HM;
-                    }
+                    mg[k] = abs_t(H.x, H.y);
+                    ph[k] = atan2_t(H.y, H.x);
+                    if (o) o[k] = H;
+                }
+            }
+            if (tid == 0) {   // Nyquist bin M = E - O at k = 0
+                const C XM = mk<C>(v[0].x - v[0].y, (T)0);
+                if constexpr (MODE == 0 || MODE == 1) {
+                    o[M] = XM;
+                } else {
+                    const C HM = cmul(XM, __ldg(rtab + M));
+                    mg[M] = abs_t(HM.x, HM.y);
+                    ph[M] = atan2_t(HM.y, HM.x);
+                    if (o) o[M] = HM;
                 }
             }
         }
@@ -165,19 +165,25 @@ k_fft_r2c(const T* __restrict__ x, long long x_stride, long long N, int vec, lon
 template <typename T, int LOG2L, int NZ, int NO>
 __global__ void __launch_bounds__(KCfg<T, LOG2L>::BLOCK, KCfg<T, LOG2L>::MINB)
 k_czt(const void* __restrict__ xin, int complex_in, long long x_stride, long long N, long long M, long long batch,
-      cx_t<T>* __restrict__ out, long long out_stride, const cx_t<T>* __restrict__ tw,
+      int nseg, long long seg_len, cx_t<T>* __restrict__ out, long long out_stride, const cx_t<T>* __restrict__ tw,
       const cx_t<T>* __restrict__ cin, const cx_t<T>* __restrict__ khat, const cx_t<T>* __restrict__ cout) {
     SKG_PROLOGUE(T, LOG2L)
-    for (long long base = (long long)blockIdx.x * K::GROUPS; base < batch; base += (long long)gridDim.x * K::GROUPS) {
-        const long long b = base + gid;
-        const bool active = b < batch;
+    // work unit u = trace * nseg + segment; segment s covers outputs [s seg_len, (s+1) seg_len)
+    const long long units = batch * nseg;
+    for (long long base = (long long)blockIdx.x * K::GROUPS; base < units; base += (long long)gridDim.x * K::GROUPS) {
+        const long long u = base + gid;
+        const bool active = u < units;
+        const long long b = active ? u / nseg : 0;
+        const long long sg = active ? u - b * nseg : 0;
+        const C* cs = cin + sg * N;
+        const long long m_here = min(seg_len, M - sg * seg_len);
         C v[G::EPT];
 #pragma unroll
         for (int q = 0; q < G::EPT; ++q) {
             v[q] = czero<C>();
             const long long pos = tid + (long long)G::NT * q;
             if (q < NZ && active && pos < N) {
-                const C ch = __ldg(cin + pos);
+                const C ch = __ldg(cs + pos);
                 if (complex_in) v[q] = cmul(__ldg(reinterpret_cast<const C*>(xin) + b * x_stride + pos), ch);
                 else v[q] = rmul(__ldg(reinterpret_cast<const T*>(xin) + b * x_stride + pos), ch);
             }
@@ -187,11 +193,11 @@ k_czt(const void* __restrict__ xin, int complex_in, long long x_stride, long lon
         for (int q = 0; q < G::EPT; ++q) v[q] = cmul(v[q], __ldg(khat + tid + G::NT * q));
         block_fft<true, LOG2L, 16, NO>(v, sm, tws, tid);
         if (active) {
-            C* o = out + b * out_stride;
+            C* o = out + b * out_stride + sg * seg_len;
 #pragma unroll
             for (int q = 0; q < G::EPT; ++q) {
                 const long long pos = tid + (long long)G::NT * q;
-                if (q < NO && pos < M) o[pos] = cmul(v[q], __ldg(cout + pos));
+                if (q < NO && pos < m_here) o[pos] = cmul(v[q], __ldg(cout + pos));
             }
         }
         __syncthreads();
@@ -214,34 +220,34 @@ cudaError_t run_c2c(const void* in, long long in_stride, void* out, long long ou
     return cudaGetLastError();
 }
 
-template <typename T, int LOG2M, int NZ>
+template <typename T, int LOG2M, int NZ, int MODE>
 cudaError_t run_r2c(long long N, const T* x, long long x_stride, long long batch, const void* tw,
-                    const void* post, int mode, void* out, long long out_stride, const void* rtab, T* mag,
+                    const void* post, void* out, long long out_stride, const void* rtab, T* mag,
                     T* phase, long long mp_stride, cudaStream_t st) {
     using K = KCfg<T, LOG2M>;
     using C = cx_t<T>;
-    auto kern = k_fft_r2c<T, LOG2M, NZ>;
+    auto kern = k_fft_r2c<T, LOG2M, NZ, MODE>;
     cudaError_t e = prep_smem(kern, K::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     const int vec = ((N & 1) == 0 && (x_stride & 1) == 0 && ((uintptr_t)x % (2 * sizeof(T))) == 0) ? 1 : 0;
     kern<<<persistent_grid(kern, K::BLOCK, K::SMEM_BYTES, grid_for(batch, K::GROUPS)), K::BLOCK, K::SMEM_BYTES, st>>>(
-        x, x_stride, N, vec, batch, (const C*)tw, (const C*)post, mode, (C*)out, out_stride, (const C*)rtab,
+        x, x_stride, N, vec, batch, (const C*)tw, (const C*)post, (C*)out, out_stride, (const C*)rtab,
         mag, phase, mp_stride);
     return cudaGetLastError();
 }
 
 template <typename T, int LOG2L, int NZ, int NO>
 cudaError_t run_czt(long long N, long long M, bool complex_in, const void* x, long long x_stride, long long batch,
-                    void* out, long long out_stride, const void* tw, const void* cin, const void* khat,
-                    const void* cout, cudaStream_t st) {
+                    int nseg, long long seg_len, void* out, long long out_stride, const void* tw, const void* cin,
+                    const void* khat, const void* cout, cudaStream_t st) {
     using K = KCfg<T, LOG2L>;
     using C = cx_t<T>;
     auto kern = k_czt<T, LOG2L, NZ, NO>;
     cudaError_t e = prep_smem(kern, K::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    kern<<<persistent_grid(kern, K::BLOCK, K::SMEM_BYTES, grid_for(batch, K::GROUPS)), K::BLOCK, K::SMEM_BYTES, st>>>(
-        x, complex_in ? 1 : 0, x_stride, N, M, batch, (C*)out, out_stride, (const C*)tw, (const C*)cin,
-        (const C*)khat, (const C*)cout);
+    kern<<<persistent_grid(kern, K::BLOCK, K::SMEM_BYTES, grid_for(batch * nseg, K::GROUPS)), K::BLOCK, K::SMEM_BYTES,
+           st>>>(x, complex_in ? 1 : 0, x_stride, N, M, batch, nseg, seg_len, (C*)out, out_stride, (const C*)tw,
+                 (const C*)cin, (const C*)khat, (const C*)cout);
     return cudaGetLastError();
 }
 
@@ -298,27 +304,33 @@ cudaError_t launch_fft_r2c_impl(int log2M, long long N, const T* x, long long x_
         const int nz = nz_class((N + 1) / 2, FftGeom<LG>::NT);
         return dispatch_nz<LG>(nz, [&](auto z) {
             constexpr int NZ = decltype(z)::value;
-            return run_r2c<T, LG, NZ>(N, x, x_stride, batch, tw, post, mode, out, out_stride, rtab, mag, phase,
-                                      mp_stride, st);
+            if (mode == 0)
+                return run_r2c<T, LG, NZ, 0>(N, x, x_stride, batch, tw, post, out, out_stride, rtab, mag, phase,
+                                             mp_stride, st);
+            if (mode == 1)
+                return run_r2c<T, LG, NZ, 1>(N, x, x_stride, batch, tw, post, out, out_stride, rtab, mag, phase,
+                                             mp_stride, st);
+            return run_r2c<T, LG, NZ, 2>(N, x, x_stride, batch, tw, post, out, out_stride, rtab, mag, phase,
+                                         mp_stride, st);
         });
     });
 }
 
 template <typename T>
 cudaError_t launch_czt_impl(int log2L, long long N, long long M, bool complex_in, const void* x, long long x_stride,
-                            long long batch, void* out, long long out_stride, const void* tw, const void* cin,
-                            const void* khat, const void* cout, cudaStream_t st) {
+                            long long batch, int nseg, long long seg_len, void* out, long long out_stride,
+                            const void* tw, const void* cin, const void* khat, const void* cout, cudaStream_t st) {
     return dispatch_log2<0, max_log2<T>()>(log2L, [&](auto lg) {
         constexpr int LG = decltype(lg)::value;
         const int nz = nz_class(N, FftGeom<LG>::NT);
-        const int no = no_class(M, FftGeom<LG>::NT);
+        const int no = no_class(seg_len, FftGeom<LG>::NT);
         return dispatch_nz<LG>(nz, [&](auto z) {
             constexpr int NZ = decltype(z)::value;
             if (LG >= 8 && no == 8)
-                return run_czt<T, LG, NZ, (LG >= 8 ? 8 : 16)>(N, M, complex_in, x, x_stride, batch, out, out_stride,
-                                                              tw, cin, khat, cout, st);
-            return run_czt<T, LG, NZ, 16>(N, M, complex_in, x, x_stride, batch, out, out_stride, tw, cin, khat,
-                                          cout, st);
+                return run_czt<T, LG, NZ, (LG >= 8 ? 8 : 16)>(N, M, complex_in, x, x_stride, batch, nseg, seg_len,
+                                                              out, out_stride, tw, cin, khat, cout, st);
+            return run_czt<T, LG, NZ, 16>(N, M, complex_in, x, x_stride, batch, nseg, seg_len, out, out_stride, tw,
+                                          cin, khat, cout, st);
         });
     });
 }

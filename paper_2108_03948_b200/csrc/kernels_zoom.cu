@@ -232,3 +232,148 @@ size_t zoom_smem_bytes(const ZoomArgs& a, int log2n, bool f32) {
     return (L + (L >> 4) + 1 + tw + a.mwrap + 1) * cs + (size_t)a.D * a.rs * rs;
 }
 }  // namespace skg
+
+// ---- unfused zoom: FIR/decimate by output chunks into a work buffer, then the FFT (any length, incl.
+// multi-pass and the chirp route for non-power-of-two n_fft) and a band-gather kernel. Used when the
+// record or the short transform does not fit one CTA's shared memory (cfg5 N = 65536) and for the
+// natural-length mode (pad_pow2 = 0, zoomfft.cpp:172).
+namespace skg {
+
+constexpr int ZCH_THREADS = 128;
+constexpr int ZCH = ZCH_THREADS * ZK;   // outputs per CTA
+
+template <typename T>
+__global__ void __launch_bounds__(ZCH_THREADS)
+k_zoom_fir(const T* __restrict__ x, long long x_stride, ZoomArgs a, int chunks, const cx_t<T>* __restrict__ gph,
+           const cx_t<T>* __restrict__ S, cx_t<T>* __restrict__ zb, long long z_stride) {
+    using C = cx_t<T>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const long long b = blockIdx.x / chunks;
+    const int ck = blockIdx.x % chunks;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int D = a.D, U = (int)a.U;
+    const T* xr = x + b * x_stride;
+    // rows hold samples n with n/D in [r0 - pre, r0 - pre + rowlen)
+    const int m_first = ck * ZCH + a.trim;                 // first FIR output of this chunk
+    const int r0 = m_first;                                 // row index of the chunk's first output
+    const int rs = a.rs;                                    // padded row stride for ZCH + pre + margin
+    C* cw = reinterpret_cast<C*>(smraw);
+    T* xs = reinterpret_cast<T*>(cw + (a.mwrap + 1));
+    const int span = a.rowlen;                              // unpadded row entries (pre + ZCH + margin)
+    for (int i = tid; i < D * rs; i += ZCH_THREADS) xs[i] = (T)0;
+    __syncthreads();
+    // samples n in [ (r0 - pre) D, (r0 - pre + span) D ) intersect [0, U)
+    const long long n_lo = (long long)(r0 - a.pre) * D;
+    const long long n_hi = (long long)(r0 - a.pre + span) * D;
+    for (long long n = (n_lo < 0 ? 0 : n_lo) + tid; n < n_hi && n < U; n += ZCH_THREADS) {
+        const int ph = (int)(n % D);
+        const int rr = (int)(n / D) - (r0 - a.pre);
+        xs[ph * rs + zpad(rr)] = __ldg(xr + n);
+    }
+    if (a.circular && ck == 0) {   // wrap terms, read straight from global memory
+        for (int m = warp; m < a.mwrap; m += ZCH_THREADS / 32) {
+            C acc = czero<C>();
+            for (int t = m * D + 1 + lane; t < a.T; t += 32) {
+                const int tm = t % D;
+                const int trow = tm ? D - tm : 0;
+                acc = cadd(acc, rmul(__ldg(xr + (U + m * D - t)), __ldg(gph + trow * a.lh + t / D)));
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+            }
+            if (lane == 0) cw[m] = cmul(acc, mk<C>((T)a.wre, (T)a.wim));
+        }
+    }
+    __syncthreads();
+    const int m_local0 = tid * ZK;                     // within the chunk
+    C acc[ZK];
+#pragma unroll
+    for (int c = 0; c < ZK; ++c) acc[c] = czero<C>();
+    for (int ph = 0; ph < D; ++ph) {
+        const T* row = xs + ph * rs;
+        const int delta = ph != 0 ? 1 : 0;
+        const C* gr = gph + ph * a.lh;
+        T w[ZK];
+        const int base = m_local0 - delta + a.pre;
+#pragma unroll
+        for (int c = 0; c < ZK; ++c) w[c] = row[zpad(base + c)];
+        for (int l0 = 0; l0 < a.lh; l0 += ZK) {
+            T nw[ZK];
+#pragma unroll
+            for (int c = 0; c < ZK; ++c) nw[c] = row[zpad(base - l0 - ZK + c)];
+#pragma unroll
+            for (int s = 0; s < ZK; ++s) {
+                const C g = __ldg(gr + l0 + s);
+#pragma unroll
+                for (int c = 0; c < ZK; ++c) {
+                    acc[c].x = fma(g.x, w[c], acc[c].x);
+                    acc[c].y = fma(g.y, w[c], acc[c].y);
+                }
+#pragma unroll
+                for (int c = ZK - 1; c > 0; --c) w[c] = w[c - 1];
+                w[0] = nw[ZK - 1 - s];
+            }
+        }
+    }
+    C* zr = zb + b * z_stride;
+#pragma unroll
+    for (int c = 0; c < ZK; ++c) {
+        const int m = ck * ZCH + m_local0 + c;   // index in the decimated block
+        const int mf = m + a.trim;
+        if (m < a.nout) {
+            C v = acc[c];
+            if (a.circular && mf < a.mwrap) v = cadd(v, cw[mf]);
+            zr[m] = cmul(v, __ldg(S + m));
+        }
+    }
+}
+
+template <typename T>
+__global__ void k_zoom_band(const cx_t<T>* __restrict__ Z, long long z_stride, long long n_fft, int k_lo, int nbins,
+                            const cx_t<T>* __restrict__ band, cx_t<T>* __restrict__ out, long long out_stride) {
+    const long long b = blockIdx.y;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nbins) return;
+    const long long k = k_lo + i;
+    const long long idx = ((k % n_fft) + n_fft) % n_fft;
+    out[b * out_stride + i] = cmul(Z[b * z_stride + idx], __ldg(band + i));
+}
+
+// rows needed per chunk: ZCH outputs + pre + margin
+int zoom_chunk_rowlen(const ZoomArgs& a) { return a.pre + ZCH + 2 * ZK; }
+
+template <typename T>
+static cudaError_t zoom_fir_impl(const ZoomArgs& a, const T* x, long long xs, long long batch, const void* g,
+                                 const void* S, void* zb, long long z_stride, cudaStream_t st) {
+    using C = cx_t<T>;
+    const int chunks = (a.nout + ZCH - 1) / ZCH;
+    const size_t smem = (size_t)(a.mwrap + 1) * sizeof(C) + (size_t)a.D * a.rs * sizeof(T);
+    auto kern = k_zoom_fir<T>;
+    cudaError_t e = prep_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)(batch * chunks), ZCH_THREADS, smem, st>>>(x, xs, a, chunks, (const C*)g, (const C*)S, (C*)zb,
+                                                                 z_stride);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_zoom_fir(const ZoomArgs& a, bool f32, const void* x, long long xs, long long batch, const void* g,
+                            const void* S, void* zb, long long z_stride, cudaStream_t st) {
+    return f32 ? zoom_fir_impl<float>(a, (const float*)x, xs, batch, g, S, zb, z_stride, st)
+               : zoom_fir_impl<double>(a, (const double*)x, xs, batch, g, S, zb, z_stride, st);
+}
+
+cudaError_t launch_zoom_band(bool f32, const void* Z, long long z_stride, long long n_fft, int k_lo, int nbins,
+                             const void* band, void* out, long long out_stride, long long batch, cudaStream_t st) {
+    const dim3 grid((unsigned)((nbins + 255) / 256), (unsigned)batch);
+    if (f32)
+        k_zoom_band<float><<<grid, 256, 0, st>>>((const float2*)Z, z_stride, n_fft, k_lo, nbins, (const float2*)band,
+                                                 (float2*)out, out_stride);
+    else
+        k_zoom_band<double><<<grid, 256, 0, st>>>((const double2*)Z, z_stride, n_fft, k_lo, nbins,
+                                                  (const double2*)band, (double2*)out, out_stride);
+    return cudaGetLastError();
+}
+
+}  // namespace skg

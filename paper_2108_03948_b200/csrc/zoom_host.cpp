@@ -162,9 +162,35 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
     check(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev_id), "attr");
     const bool fused = is_pow2(n_fft) && lg <= single_cta_max_log2(f32) &&
                        zoom_smem_bytes(a, lg, f32) <= static_cast<size_t>(smem_max);
-    if (!fused)
-        throw std::invalid_argument("zoom_fft: geometry (n=" + std::to_string(input_len) + ", n_fft=" +
-                                    std::to_string(n_fft) + ") needs the unfused path (not available in this build)");
+    if (!fused) {
+        // FIR/decimate by output chunks -> work buffer (zero padded to n_fft) -> FFT -> band gather
+        ZoomArgs c = a;
+        c.rowlen = zoom_chunk_rowlen(a);
+        int rs = c.rowlen + c.rowlen / kZoomK + 1;
+        if ((rs & 1) == 0) ++rs;
+        c.rs = rs;
+        const size_t cs = f32 ? 8 : 16;
+        void* zb = nullptr;
+        check(cudaMallocAsync(&zb, (size_t)batch * n_fft * cs, st), "cudaMallocAsync");
+        check(cudaMemsetAsync(zb, 0, (size_t)batch * n_fft * cs, st), "memset");
+        check(launch_zoom_fir(c, f32, x, x_stride, batch, d.g.p, d.sdec.p, zb, (long long)n_fft, st), "zoom fir");
+        count_launch();
+        if (is_pow2(n_fft)) {
+            fft_c2c(n_fft, false, f32, zb, (long long)n_fft, zb, (long long)n_fft, batch, st);
+        } else {   // dft_any's chirp route (zoomfft.cpp:204-207)
+            void* zf = nullptr;
+            check(cudaMallocAsync(&zf, (size_t)batch * n_fft * cs, st), "cudaMallocAsync");
+            bluestein_->execute(zb, true, (long long)n_fft, batch, zf, (long long)n_fft, f32, st);
+            check(cudaFreeAsync(zb, st), "free");
+            zb = zf;
+        }
+        check(launch_zoom_band(f32, zb, (long long)n_fft, (long long)n_fft, (int)k_lo, (int)bins(), d.band.p, out,
+                               out_stride, batch, st),
+              "zoom band");
+        count_launch();
+        check(cudaFreeAsync(zb, st), "free");
+        return;
+    }
     const void* tw = stockham_twiddles(lg, f32);
     cudaError_t e = f32 ? launch_zoom_f32(a, lg, (const float*)x, x_stride, batch, d.g.p, d.sdec.p, tw, d.band.p,
                                           out, out_stride, st)

@@ -123,3 +123,37 @@ def test_linear_mode_and_centre_override():
         got = plan.execute(_dev(x, "f64")).cpu().numpy()
         ref = O.ZoomPlan(2000, 0.4e12, 1.2e12, W.FS, **kw)
         assert rel_max_rows(got, [ref(r)[0] for r in x]) <= TOL_F64, kw
+
+
+def test_natural_length_mode_chirp_route():   # test_zoomfft.cpp:110-126 (n_fft = 125, dft_any)
+    p = sk.ZoomPlan(500, 0.5e12, 2.0e12, 10e12, decimation=4, pad_pow2=0)
+    assert p.n_fft == 125 and abs(p.f_step_hz - 20e9) < 1e-3
+    t = W.thz_pulse(500, fs=10e12)
+    s = p.spectrum(t)
+    assert s.bins.size == 75 and abs(s.f_start_hz - (1.25e12 - 37 * 20e9)) < 1.0 and s.source_n == 125
+    want, f0, _ = O.ZoomPlan(500, 0.5e12, 2.0e12, 10e12, decimation=4, pad_pow2=0)(t)
+    assert rel_max(s.bins, want) <= TOL_F64
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("n,D", [(16384, 4), (65536, 4), (65536, 16)])
+def test_cfg5_zoom_long_records_unfused(prec, n, D):
+    """Records / short transforms beyond one CTA: chunked FIR -> (multi-pass) FFT -> band gather."""
+    x = W.sample_traces(2, n)
+    plan = sk.ZoomPlanGPU(n, 0.4e12, 1.2e12, W.FS, sk.SKG_F64 if prec == "f64" else sk.SKG_F32, decimation=D)
+    xd = _dev(x, prec)
+    got = plan.execute(xd).cpu().numpy()
+    ref = O.ZoomPlan(n, 0.4e12, 1.2e12, W.FS, decimation=D)
+    want = [ref(r)[0] for r in xd.cpu().double().numpy()]
+    if prec == "f64":
+        assert rel_max_rows(got, want) <= TOL_F64
+    else:
+        assert rel_l2_rows(got, want) <= TOL_F32
+
+
+def test_unfused_linear_trim_long():
+    x = W.sample_traces(2, 40000)
+    kw = {"circular": 0, "trim_transient": 1, "decimation": 4}
+    got = sk.ZoomPlanGPU(40000, 0.4e12, 1.2e12, W.FS, **kw).execute(_dev(x, "f64")).cpu().numpy()
+    ref = O.ZoomPlan(40000, 0.4e12, 1.2e12, W.FS, **kw)
+    assert rel_max_rows(got, [ref(r)[0] for r in x]) <= TOL_F64
