@@ -230,6 +230,10 @@ template <int LOG2L> struct FftGeom {
 
 __device__ __forceinline__ int pad16(int a) { return a + (a >> 4); }
 
+// cache-line prefetches (no registers consumed; the data waits in L1 / L2 for the real load)
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 // copy the factorised twiddle tables of an L-point transform into shared memory (whole CTA)
 template <int LOG2L, typename C>
 __device__ __forceinline__ void load_twiddles(C* dst, const C* __restrict__ src) {

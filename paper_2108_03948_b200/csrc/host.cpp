@@ -2,6 +2,7 @@
 #include "host.hpp"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -324,12 +325,19 @@ CztPlanG::CztPlanG(size_t n, cd a, cd w, size_t m) : n_(n), m_(m) {
     // (n=1024, m=2048) this is S=2, Ls=2048 — slightly less arithmetic than one 4096-point pair
     // and half the shared memory per CTA, i.e. twice the resident CTAs per SM.
     double best = 0.0;
+    // SKG_CZT_SEGMENTS=<S> pins the segment count (tuning / A-B experiments)
+    const char* env = std::getenv("SKG_CZT_SEGMENTS");
+    const size_t forced = env ? static_cast<size_t>(std::strtoul(env, nullptr, 10)) : 0;
     for (size_t S = 1; S <= m; S *= 2) {
+        if (forced && S != forced) {
+            if (S > forced) break;
+            continue;
+        }
         const size_t seg = (m + S - 1) / S;
         const size_t Ls = next_pow2(n + seg - 1);
         double cost = static_cast<double>((m + seg - 1) / seg) * static_cast<double>(Ls) * ilog2(Ls);
         if (ilog2(Ls) > single_cta_max_log2(false)) cost *= 1.5;   // multi-pass: work buffer round trips
-        if (S == 1 || cost < best * 0.999) {
+        if (S == 1 || forced || cost < best * 0.999) {
             best = cost;
             nseg_ = (m + seg - 1) / seg;
             seg_ = seg;
@@ -446,11 +454,11 @@ void CztPlanG::execute(const void* x, bool complex_in, long long x_stride, long 
     cudaError_t e;
     if (f32)
         e = launch_czt<float>(log2L_, N, (long long)m_, complex_in, x, x_stride, batch, (int)nseg_, (long long)seg_,
-                              out, out_stride, tw,
+                              (long long)n_, out, out_stride, tw,
                               d.cin.p, d.khat.p, d.cout.p, st);
     else
         e = launch_czt<double>(log2L_, N, (long long)m_, complex_in, x, x_stride, batch, (int)nseg_,
-                               (long long)seg_, out, out_stride, tw,
+                               (long long)seg_, (long long)n_, out, out_stride, tw,
                                d.cin.p, d.khat.p, d.cout.p, st);
     check(e, "czt launch");
     count_launch();

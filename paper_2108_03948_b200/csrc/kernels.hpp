@@ -34,8 +34,8 @@ cudaError_t launch_fft_r2c(int log2M, long long N, const T* x, long long x_strid
 // output chirp); L is the convolution length of ONE segment.
 template <typename T>
 cudaError_t launch_czt(int log2L, long long N, long long M, bool complex_in, const void* x,
-                       long long x_stride, long long batch, int nseg, long long seg_len, void* out,
-                       long long out_stride, const void* tw, const void* cin, const void* khat,
+                       long long x_stride, long long batch, int nseg, long long seg_len, long long cin_stride,
+                       void* out, long long out_stride, const void* tw, const void* cin, const void* khat,
                        const void* cout, cudaStream_t st);
 
 // ---- four-step passes for L = R * C beyond one CTA (kernels_4step.cuh) ----------------------

@@ -97,6 +97,17 @@ k_fft_r2c(const T* __restrict__ x, long long x_stride, long long N, int vec, lon
         const bool active = b < batch;
         C v[G::EPT];
         const T* xs = x + b * x_stride;
+        {
+            const long long bn = b + (long long)gridDim.x * K::GROUPS;
+            if (bn < batch) {
+                const T* xn = x + bn * x_stride;
+#pragma unroll
+                for (int q = 0; q < G::EPT; ++q) {
+                    const long long pos = tid + (long long)G::NT * q;
+                    if (q < NZ && 2 * pos < N) prefetch_l2(xn + 2 * pos);
+                }
+            }
+        }
 #pragma unroll
         for (int q = 0; q < G::EPT; ++q) {
             v[q] = czero<C>();
@@ -165,7 +176,7 @@ k_fft_r2c(const T* __restrict__ x, long long x_stride, long long N, int vec, lon
 template <typename T, int LOG2L, int NZ, int NO>
 __global__ void __launch_bounds__(KCfg<T, LOG2L>::BLOCK, KCfg<T, LOG2L>::MINB)
 k_czt(const void* __restrict__ xin, int complex_in, long long x_stride, long long N, long long M, long long batch,
-      int nseg, long long seg_len, cx_t<T>* __restrict__ out, long long out_stride, const cx_t<T>* __restrict__ tw,
+      int nseg, long long seg_len, long long cin_stride, cx_t<T>* __restrict__ out, long long out_stride, const cx_t<T>* __restrict__ tw,
       const cx_t<T>* __restrict__ cin, const cx_t<T>* __restrict__ khat, const cx_t<T>* __restrict__ cout) {
     SKG_PROLOGUE(T, LOG2L)
     // work unit u = trace * nseg + segment; segment s covers outputs [s seg_len, (s+1) seg_len)
@@ -175,8 +186,26 @@ k_czt(const void* __restrict__ xin, int complex_in, long long x_stride, long lon
         const bool active = u < units;
         const long long b = active ? u / nseg : 0;
         const long long sg = active ? u - b * nseg : 0;
-        const C* cs = cin + sg * N;
+        const C* cs = cin + sg * cin_stride;
         const long long m_here = min(seg_len, M - sg * seg_len);
+        if (active) {
+            // the kernel spectrum is needed after the forward transform: pull this thread's lines
+            // into L1 now (every CTA on the SM reads the same table)
+#pragma unroll
+            for (int q = 0; q < G::EPT; q += (G::NT >= 8 ? 1 : G::EPT)) prefetch_l1(khat + tid + G::NT * q);
+            // next unit of this CTA: its trace row into L2 while we work on this one
+            const long long un = u + (long long)gridDim.x * K::GROUPS;
+            if (un < units) {
+                const long long bn = un / nseg;
+                const char* xn = reinterpret_cast<const char*>(xin) +
+                                 (size_t)(bn * x_stride) * (complex_in ? sizeof(C) : sizeof(T));
+#pragma unroll
+                for (int q = 0; q < G::EPT; ++q) {
+                    const long long pos = tid + (long long)G::NT * q;
+                    if (q < NZ && pos < N) prefetch_l2(xn + pos * (complex_in ? sizeof(C) : sizeof(T)));
+                }
+            }
+        }
         C v[G::EPT];
 #pragma unroll
         for (int q = 0; q < G::EPT; ++q) {
@@ -238,15 +267,15 @@ cudaError_t run_r2c(long long N, const T* x, long long x_stride, long long batch
 
 template <typename T, int LOG2L, int NZ, int NO>
 cudaError_t run_czt(long long N, long long M, bool complex_in, const void* x, long long x_stride, long long batch,
-                    int nseg, long long seg_len, void* out, long long out_stride, const void* tw, const void* cin,
-                    const void* khat, const void* cout, cudaStream_t st) {
+                    int nseg, long long seg_len, long long cin_stride, void* out, long long out_stride,
+                    const void* tw, const void* cin, const void* khat, const void* cout, cudaStream_t st) {
     using K = KCfg<T, LOG2L>;
     using C = cx_t<T>;
     auto kern = k_czt<T, LOG2L, NZ, NO>;
     cudaError_t e = prep_smem(kern, K::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     kern<<<persistent_grid(kern, K::BLOCK, K::SMEM_BYTES, grid_for(batch * nseg, K::GROUPS)), K::BLOCK, K::SMEM_BYTES,
-           st>>>(x, complex_in ? 1 : 0, x_stride, N, M, batch, nseg, seg_len, (C*)out, out_stride, (const C*)tw,
+           st>>>(x, complex_in ? 1 : 0, x_stride, N, M, batch, nseg, seg_len, cin_stride, (C*)out, out_stride, (const C*)tw,
                  (const C*)cin, (const C*)khat, (const C*)cout);
     return cudaGetLastError();
 }
@@ -318,8 +347,9 @@ cudaError_t launch_fft_r2c_impl(int log2M, long long N, const T* x, long long x_
 
 template <typename T>
 cudaError_t launch_czt_impl(int log2L, long long N, long long M, bool complex_in, const void* x, long long x_stride,
-                            long long batch, int nseg, long long seg_len, void* out, long long out_stride,
-                            const void* tw, const void* cin, const void* khat, const void* cout, cudaStream_t st) {
+                            long long batch, int nseg, long long seg_len, long long cin_stride, void* out,
+                            long long out_stride, const void* tw, const void* cin, const void* khat, const void* cout,
+                            cudaStream_t st) {
     return dispatch_log2<0, max_log2<T>()>(log2L, [&](auto lg) {
         constexpr int LG = decltype(lg)::value;
         const int nz = nz_class(N, FftGeom<LG>::NT);
@@ -328,9 +358,9 @@ cudaError_t launch_czt_impl(int log2L, long long N, long long M, bool complex_in
             constexpr int NZ = decltype(z)::value;
             if (LG >= 8 && no == 8)
                 return run_czt<T, LG, NZ, (LG >= 8 ? 8 : 16)>(N, M, complex_in, x, x_stride, batch, nseg, seg_len,
-                                                              out, out_stride, tw, cin, khat, cout, st);
-            return run_czt<T, LG, NZ, 16>(N, M, complex_in, x, x_stride, batch, nseg, seg_len, out, out_stride, tw,
-                                          cin, khat, cout, st);
+                                                              cin_stride, out, out_stride, tw, cin, khat, cout, st);
+            return run_czt<T, LG, NZ, 16>(N, M, complex_in, x, x_stride, batch, nseg, seg_len, cin_stride, out,
+                                          out_stride, tw, cin, khat, cout, st);
         });
     });
 }
