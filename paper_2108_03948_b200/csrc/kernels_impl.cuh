@@ -133,19 +133,11 @@ k_fft_r2c(const T* __restrict__ x, long long x_stride, long long N, int vec, lon
             C* o = out ? out + b * out_stride : nullptr;
             T* mg = MODE == 2 ? mag + b * mp_stride : nullptr;
             T* ph = MODE == 2 ? phase + b * mp_stride : nullptr;
-#pragma unroll
-            for (int q = 0; q < G::EPT; ++q) {
-                const int k = tid + G::NT * q;
-                C c;
-                if constexpr (G::NT == 1) c = v[(M - q) & (M - 1)];
-                else c = sm[pad16((M - k) & (M - 1))];
-                const C z = v[q];
-                const C E = mk<C>((T)0.5 * (z.x + c.x), (T)0.5 * (z.y - c.y));
-                const C O = mk<C>((T)0.5 * (z.y + c.y), (T)0.5 * (c.x - z.x));
-                const C X = cadd(E, cmul(O, __ldg(post + k)));
+            // store one output bin (full / half spectrum or H = X / X_ref as |H|, arg H)
+            auto emit = [&](long long k, C X) {
                 if constexpr (MODE == 0) {
                     o[k] = X;
-                    if (k) o[L - k] = cconj(X);
+                    if (k && k < M) o[L - k] = cconj(X);
                 } else if constexpr (MODE == 1) {
                     o[k] = X;
                 } else {
@@ -154,16 +146,34 @@ k_fft_r2c(const T* __restrict__ x, long long x_stride, long long N, int vec, lon
                     ph[k] = atan2_t(H.y, H.x);
                     if (o) o[k] = H;
                 }
+            };
+            // bins in conjugate pairs (k, M - k), k < M/2: from Z[k], Z[M-k]
+            //   E = (Z[k] + conj Z[M-k]) / 2, O = (Z[k] - conj Z[M-k]) / 2i,
+            //   X[k] = E + W^k O,  X[M-k] = conj(E - W^k O)   (W = e^{-2 pi i / 2M})
+            // k = 0 pairs with the Nyquist bin M; k = M/2 is its own partner.
+#pragma unroll
+            for (int q = 0; q < (G::EPT > 1 ? G::EPT / 2 : 1); ++q) {
+                const int k = tid + G::NT * q;
+                C c;
+                if constexpr (G::NT == 1) c = v[(M - q) & (M - 1)];
+                else c = sm[pad16((M - k) & (M - 1))];
+                const C z = v[q];
+                const C E = mk<C>((T)0.5 * (z.x + c.x), (T)0.5 * (z.y - c.y));
+                const C O = mk<C>((T)0.5 * (z.y + c.y), (T)0.5 * (c.x - z.x));
+                const C WO = cmul(O, __ldg(post + k));
+                emit(k, cadd(E, WO));
+                emit(M - k, cconj(csub(E, WO)));
             }
-            if (tid == 0) {   // Nyquist bin M = E - O at k = 0
-                const C XM = mk<C>(v[0].x - v[0].y, (T)0);
-                if constexpr (MODE == 0 || MODE == 1) {
-                    o[M] = XM;
-                } else {
-                    const C HM = cmul(XM, __ldg(rtab + M));
-                    mg[M] = abs_t(HM.x, HM.y);
-                    ph[M] = atan2_t(HM.y, HM.x);
-                    if (o) o[M] = HM;
+            if constexpr (G::EPT > 1) {
+                if (tid == 0) {   // k = M/2 (its own partner)
+                    const int k = M / 2;
+                    const C z = v[G::EPT / 2];
+                    C c;
+                    if constexpr (G::NT == 1) c = v[G::EPT / 2];
+                    else c = z;
+                    const C E = mk<C>((T)0.5 * (z.x + c.x), (T)0.5 * (z.y - c.y));
+                    const C O = mk<C>((T)0.5 * (z.y + c.y), (T)0.5 * (c.x - z.x));
+                    emit(k, cadd(E, cmul(O, __ldg(post + k))));
                 }
             }
         }

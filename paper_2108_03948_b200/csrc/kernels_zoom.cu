@@ -28,10 +28,12 @@ __host__ __device__ inline int zpad(int r) { return r + r / ZK; }
 template <int LOG2N> struct ZoomCfg {
     static constexpr int NT = FftGeom<LOG2N>::NT;
     static constexpr int NTH = NT > 128 ? NT : 128;   // CTA width
+    // register cap: 4 CTAs of 128 threads per SM for fp32, 3 for fp64 (the FFT-512 stage would spill at 128)
+    template <typename T> static constexpr int minb() { return NTH >= 512 ? 1 : (sizeof(T) == 8 ? 384 : 512) / NTH; }
 };
 
 template <typename T, int LOG2N>
-__global__ void __launch_bounds__(ZoomCfg<LOG2N>::NTH)
+__global__ void __launch_bounds__(ZoomCfg<LOG2N>::NTH, ZoomCfg<LOG2N>::template minb<T>())
 k_zoom(const T* __restrict__ x, long long x_stride, long long batch, ZoomArgs a,
        const cx_t<T>* __restrict__ gph,     // taps by phase row: gph[ph * lh + l] = g[l D + (D - ph) % D]
        const cx_t<T>* __restrict__ S,       // S[m], m < nout (already offset by trim)
@@ -61,10 +63,55 @@ k_zoom(const T* __restrict__ x, long long x_stride, long long batch, ZoomArgs a,
     for (int i = tid; i < total; i += NTH) xs[i] = (T)0;
     for (int i = tid; i < G::L; i += NTH) fb[pad16(i)] = czero<C>();
     __syncthreads();
-    for (int n = tid; n < U; n += NTH) {
-        const int ph = dpow2 ? (n & (D - 1)) : n % D;
-        const int r = dpow2 ? (n >> ld) : n / D;
-        xs[ph * a.rs + zpad(r + a.pre)] = __ldg(xr + n);
+    // the CTA that takes the next trace (blockIdx + gridDim) gets its row pulled into L2 now
+    if (b + gridDim.x < batch) {
+        const T* xn = x + (b + gridDim.x) * x_stride;
+        for (int n = tid * (128 / (int)sizeof(T)); n < U; n += NTH * (128 / (int)sizeof(T))) prefetch_l2(xn + n);
+    }
+    {
+        // 16-byte loads, several in flight per thread, scattered into the polyphase rows
+        constexpr int V = 16 / (int)sizeof(T);
+        const bool vec = ((reinterpret_cast<uintptr_t>(xr) & 15) == 0);
+        const int nv = vec ? U / V : 0;
+        constexpr int UNR = 4;
+        for (int i0 = tid; i0 < nv; i0 += NTH * UNR) {
+            T buf[UNR][V];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int i = i0 + u * NTH;
+                if (i < nv) {
+                    if constexpr (sizeof(T) == 8) {
+                        const double2 t = __ldg(reinterpret_cast<const double2*>(xr) + i);
+                        buf[u][0] = t.x;
+                        buf[u][1] = t.y;
+                    } else {
+                        const float4 t = __ldg(reinterpret_cast<const float4*>(xr) + i);
+                        buf[u][0] = t.x;
+                        buf[u][1] = t.y;
+                        buf[u][2 % V] = t.z;
+                        buf[u][3 % V] = t.w;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int i = i0 + u * NTH;
+                if (i < nv) {
+#pragma unroll
+                    for (int e = 0; e < V; ++e) {
+                        const int n = i * V + e;
+                        const int ph = dpow2 ? (n & (D - 1)) : n % D;
+                        const int r = dpow2 ? (n >> ld) : n / D;
+                        xs[ph * a.rs + zpad(r + a.pre)] = buf[u][e];
+                    }
+                }
+            }
+        }
+        for (int n = nv * V + tid; n < U; n += NTH) {   // tail (or the whole row when unaligned)
+            const int ph = dpow2 ? (n & (D - 1)) : n % D;
+            const int r = dpow2 ? (n >> ld) : n / D;
+            xs[ph * a.rs + zpad(r + a.pre)] = __ldg(xr + n);
+        }
     }
     __syncthreads();
 
