@@ -29,6 +29,22 @@ METRIC = "traces/sec & achieved HBM GB/s (% of roofline) for batched FFT / CZT /
 UNIT = "traces/s"
 
 
+def ncu_traffic(kernel_prefix):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the named kernel from the newest
+    committed ncu --set full summary in profiles/ (None when absent)."""
+    import glob
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*.json"))):
+        try:
+            with open(f) as fh:
+                for d in json.load(fh)["launches"]:
+                    if d["kernel"].startswith(kernel_prefix) and "dram_bytes" in d:
+                        best = {"bytes": d["dram_bytes"], "source": os.path.relpath(f, ROOT)}
+        except Exception:
+            pass
+    return best
+
+
 def peaks():
     p = {"hbm_gbs": 6540.2, "source": "fallback"}
     try:
@@ -257,6 +273,8 @@ def bench_ours(args):
     achieved_tf = c["flops"] * B / kern_s / 1e12
     hbm_gbs = c["bytes"] * B / kern_s / 1e9
     roof_t = max(c["bytes"] * B / (pk["hbm_gbs"] * 1e9), c["flops"] * B / (fp64_peak * 1e12))
+    kname = "k_czt<double, 11, 8, 8>"   # S=2 output segments of the L=4096 plan, run at L'=2048
+    tr = ncu_traffic(kname)
 
     # ---- e2e: host buffers through the C ABI, H2D + kernel + D2H per step ---------------------
     xh = torch.from_numpy(x_host).pin_memory()
@@ -309,9 +327,10 @@ def bench_ours(args):
                    "parallelism": f"dp{world} (independent traces, no collective)",
                    "l2": "inputs 64 MiB + outputs 256 MiB per step > 126 MB L2 (no flush needed)"},
         "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": fp64_peak, "unit": "TFLOP/s",
-                     "frac": achieved_tf / fp64_peak, "traffic": None,
+                     "frac": achieved_tf / fp64_peak, "traffic": (tr or {}).get("bytes"),
+                     "traffic_source": (tr or {}).get("source"),
                      "peak_source": "in-run cuBLAS DGEMM 4096^3 (no fp64 entry in MEASURED_PEAKS.json)",
-                     "kernel": "skg::k_czt<double,12,4,8>", "kernel_ms": kern_s * 1e3,
+                     "kernel": kname, "kernel_ms": kern_s * 1e3,
                      "flops_per_trace": c["flops"], "bytes_per_trace": c["bytes"],
                      "hbm_achieved_gbs": hbm_gbs, "hbm_peak_gbs": pk["hbm_gbs"], "hbm_frac": hbm_gbs / pk["hbm_gbs"],
                      "roof_frac": roof_t / kern_s},
