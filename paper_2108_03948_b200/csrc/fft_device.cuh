@@ -248,10 +248,22 @@ template <typename C> __device__ __forceinline__ C ldg_c(const C* p) {
 #endif
 }
 
+// Barrier used between passes: the whole CTA, or — for kernels whose thread groups work on
+// independent transforms — a named barrier shared only by the group's warps.
+struct CtaSync {
+    __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+struct GroupSync {
+    int id, nthreads;   // id >= 1 (0 is __syncthreads), nthreads a multiple of 32
+    __device__ __forceinline__ void operator()() const {
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+    }
+};
+
 // One Stockham pass. v[q] holds position tid + NT*q on entry and exit.
-template <bool INV, int S, int NZ, int NO, int LOG2L, typename C>
+template <bool INV, int S, int NZ, int NO, int LOG2L, typename C, typename SYNC = CtaSync>
 __device__ __forceinline__ void stockham_pass(C (&v)[FftGeom<LOG2L>::EPT], C* sm, const C* __restrict__ tw,
-                                              int tid, bool active = true) {
+                                              int tid, bool active = true, SYNC sync = SYNC()) {
     using G = FftGeom<LOG2L>;
     constexpr int R = G::radix(S);
     constexpr int p = G::pval(S);
@@ -286,30 +298,30 @@ __device__ __forceinline__ void stockham_pass(C (&v)[FftGeom<LOG2L>::EPT], C* sm
         }
     }
     if constexpr (!last) {
-        __syncthreads();
+        sync();
         if (active) {
 #pragma unroll
             for (int q = 0; q < G::EPT; ++q) v[q] = sm[pad16(tid + G::NT * q)];
         }
-        __syncthreads();
+        sync();
     }
 }
 
 // Full transform: NZ = leading nonzero inputs of the first radix-16 pass (1..16),
 // NO = leading outputs needed from the last radix-16 pass (4, 8 or 16).
-template <bool INV, int LOG2L, int NZ = 16, int NO = 16, typename C>
+template <bool INV, int LOG2L, int NZ = 16, int NO = 16, typename C, typename SYNC = CtaSync>
 __device__ __forceinline__ void block_fft(C (&v)[FftGeom<LOG2L>::EPT], C* sm, const C* __restrict__ tw, int tid,
-                                          bool active = true) {
+                                          bool active = true, SYNC sync = SYNC()) {
     using G = FftGeom<LOG2L>;
     if constexpr (G::L < 16) {
         dft_r<G::L, INV, 16, 16>(v);
     } else {
         constexpr int nz = G::radix(0) == 16 ? NZ : 16;
         constexpr int no = G::radix(G::P - 1) == 16 ? NO : 16;
-        stockham_pass<INV, 0, nz, (G::P == 1 ? no : 16), LOG2L>(v, sm, tw, tid, active);
-        if constexpr (G::P > 1) stockham_pass<INV, 1, 16, (G::P == 2 ? no : 16), LOG2L>(v, sm, tw, tid, active);
-        if constexpr (G::P > 2) stockham_pass<INV, 2, 16, (G::P == 3 ? no : 16), LOG2L>(v, sm, tw, tid, active);
-        if constexpr (G::P > 3) stockham_pass<INV, 3, 16, (G::P == 4 ? no : 16), LOG2L>(v, sm, tw, tid, active);
+        stockham_pass<INV, 0, nz, (G::P == 1 ? no : 16), LOG2L, C, SYNC>(v, sm, tw, tid, active, sync);
+        if constexpr (G::P > 1) stockham_pass<INV, 1, 16, (G::P == 2 ? no : 16), LOG2L, C, SYNC>(v, sm, tw, tid, active, sync);
+        if constexpr (G::P > 2) stockham_pass<INV, 2, 16, (G::P == 3 ? no : 16), LOG2L, C, SYNC>(v, sm, tw, tid, active, sync);
+        if constexpr (G::P > 3) stockham_pass<INV, 3, 16, (G::P == 4 ? no : 16), LOG2L, C, SYNC>(v, sm, tw, tid, active, sync);
         static_assert(G::P <= 4, "single-CTA engine handles L <= 65536");
     }
 }

@@ -4,6 +4,9 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "fft_device.cuh"
 #include "kernels.hpp"
 
@@ -244,6 +247,93 @@ k_czt(const void* __restrict__ xin, int complex_in, long long x_stride, long lon
 }
 
 // ---------------------------------------------------------------------------------------
+// Resident-table Bluestein CZT: one CTA per SM, RG independent trace groups of NT threads (each
+// group syncs on its own named barrier), and every table the segment needs — factorised twiddles,
+// the segment's input chirp, the kernel spectrum K̂ and the output chirp — resident in shared
+// memory for the whole launch. The only global traffic left is the trace in and the bins out.
+template <typename T, int LOG2L> struct RtCfg {
+    using G = FftGeom<LOG2L>;
+    static constexpr int RG = G::NT >= 128 ? 4 : 512 / G::NT;   // trace groups per CTA (512 threads)
+    static constexpr int BLOCK = G::NT * RG;
+};
+
+template <typename T, int LOG2L, int NZ, int NO>
+__global__ void __launch_bounds__(RtCfg<T, LOG2L>::BLOCK, 1)
+k_czt_rt(const void* __restrict__ xin, int complex_in, long long x_stride, long long N, long long M, long long batch,
+         int nseg, long long seg_len, long long cin_stride, cx_t<T>* __restrict__ out, long long out_stride,
+         const cx_t<T>* __restrict__ tw, const cx_t<T>* __restrict__ cin, const cx_t<T>* __restrict__ khat,
+         const cx_t<T>* __restrict__ cout) {
+    using C = cx_t<T>;
+    using G = FftGeom<LOG2L>;
+    constexpr int RG = RtCfg<T, LOG2L>::RG;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int gid = threadIdx.x / G::NT;
+    const int tid = threadIdx.x % G::NT;
+    C* sm = reinterpret_cast<C*>(smraw) + gid * G::SMEM;
+    C* tws = reinterpret_cast<C*>(smraw) + RG * G::SMEM;
+    C* s_cin = tws + G::TW_ALLOC;
+    C* s_kh = s_cin + N;
+    C* s_co = s_kh + G::L;
+    // this CTA serves one output segment; its traces are strided over the CTAs of that segment
+    const int sg = blockIdx.x % nseg;
+    const long long team = gridDim.x / nseg;           // CTAs per segment
+    const long long first = blockIdx.x / nseg;
+    const long long m_here = min(seg_len, M - sg * seg_len);
+    load_twiddles<LOG2L>(tws, tw);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) s_cin[i] = __ldg(cin + sg * cin_stride + i);
+    for (int i = threadIdx.x; i < G::L; i += blockDim.x) s_kh[i] = __ldg(khat + i);
+    for (int i = threadIdx.x; i < m_here; i += blockDim.x) s_co[i] = __ldg(cout + i);
+    __syncthreads();
+    const GroupSync gsync{1 + gid, G::NT};
+    const size_t xes = complex_in ? sizeof(C) : sizeof(T);
+    for (long long b = first * RG + gid; b < batch; b += team * RG) {
+        {   // the group's next trace into L2 while this one is transformed
+            const long long bn = b + team * RG;
+            if (bn < batch) {
+                const char* xn = reinterpret_cast<const char*>(xin) + (size_t)(bn * x_stride) * xes;
+#pragma unroll
+                for (int q = 0; q < G::EPT; ++q) {
+                    const long long pos = tid + (long long)G::NT * q;
+                    if (q < NZ && pos < N) prefetch_l2(xn + pos * xes);
+                }
+            }
+        }
+        C v[G::EPT];
+#pragma unroll
+        for (int q = 0; q < G::EPT; ++q) {
+            v[q] = czero<C>();
+            const long long pos = tid + (long long)G::NT * q;
+            if (q < NZ && pos < N) {
+                const C ch = s_cin[pos];
+                if (complex_in) v[q] = cmul(__ldg(reinterpret_cast<const C*>(xin) + b * x_stride + pos), ch);
+                else v[q] = rmul(__ldg(reinterpret_cast<const T*>(xin) + b * x_stride + pos), ch);
+            }
+        }
+        block_fft<false, LOG2L, NZ>(v, sm, tws, tid, true, gsync);
+#pragma unroll
+        for (int q = 0; q < G::EPT; ++q) {
+            v[q] = cmul(v[q], s_kh[tid + G::NT * q]);
+            if ((q & 3) == 3) asm volatile("" ::: "memory");   // bound the K̂ loads in flight (registers)
+        }
+        block_fft<true, LOG2L, 16, NO>(v, sm, tws, tid, true, gsync);
+        C* o = out + b * out_stride + sg * seg_len;
+#pragma unroll
+        for (int q = 0; q < G::EPT; ++q) {
+            const long long pos = tid + (long long)G::NT * q;
+            if (q < NO && pos < m_here) o[pos] = cmul(v[q], s_co[pos]);
+            if ((q & 3) == 3) asm volatile("" ::: "memory");
+        }
+        gsync();   // the next trace's first exchange must not overwrite this one's last reads
+    }
+}
+
+template <typename T, int LOG2L>
+inline size_t rt_smem_bytes(long long N, long long seg_len) {
+    using G = FftGeom<LOG2L>;
+    return ((size_t)RtCfg<T, LOG2L>::RG * G::SMEM + G::TW_ALLOC + (size_t)N + G::L + (size_t)seg_len) * sizeof(cx_t<T>);
+}
+
+// ---------------------------------------------------------------------------------------
 // launch plumbing
 
 template <typename T, int LOG2L, bool INV>
@@ -275,12 +365,39 @@ cudaError_t run_r2c(long long N, const T* x, long long x_stride, long long batch
     return cudaGetLastError();
 }
 
+inline int smem_optin() {
+    static int v = 0;
+    if (!v) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    }
+    return v;
+}
+
 template <typename T, int LOG2L, int NZ, int NO>
 cudaError_t run_czt(long long N, long long M, bool complex_in, const void* x, long long x_stride, long long batch,
                     int nseg, long long seg_len, long long cin_stride, void* out, long long out_stride,
                     const void* tw, const void* cin, const void* khat, const void* cout, cudaStream_t st) {
     using K = KCfg<T, LOG2L>;
     using C = cx_t<T>;
+    if constexpr (FftGeom<LOG2L>::NT >= 32) {
+        const size_t rts = rt_smem_bytes<T, LOG2L>(N, seg_len);
+        static const bool rt_off = getenv("SKG_CZT_NO_RT") != nullptr;
+        if (!rt_off && rts <= (size_t)smem_optin() && batch >= 8) {
+            auto kern = k_czt_rt<T, LOG2L, NZ, NO>;
+            cudaError_t e = prep_smem(kern, rts);
+            if (e != cudaSuccess) return e;
+            constexpr int RG = RtCfg<T, LOG2L>::RG;
+            // grid: resident CTAs, a multiple of nseg so every CTA owns one segment
+            long long g = persistent_grid(kern, RtCfg<T, LOG2L>::BLOCK, rts, (batch + RG - 1) / RG * nseg);
+            g = std::max<long long>(nseg, g / nseg * nseg);
+            kern<<<(unsigned)g, RtCfg<T, LOG2L>::BLOCK, rts, st>>>(
+                x, complex_in ? 1 : 0, x_stride, N, M, batch, nseg, seg_len, cin_stride, (C*)out, out_stride,
+                (const C*)tw, (const C*)cin, (const C*)khat, (const C*)cout);
+            return cudaGetLastError();
+        }
+    }
     auto kern = k_czt<T, LOG2L, NZ, NO>;
     cudaError_t e = prep_smem(kern, K::SMEM_BYTES);
     if (e != cudaSuccess) return e;
