@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "fft_device.cuh"
 #include "kernels.hpp"
@@ -257,9 +258,9 @@ template <typename T, int LOG2L> struct RtCfg {
     static constexpr int BLOCK = G::NT * RG;
 };
 
-template <typename T, int LOG2L, int NZ, int NO>
+template <typename T, int LOG2L, int NZ, int NO, bool CPLX>
 __global__ void __launch_bounds__(RtCfg<T, LOG2L>::BLOCK, 1)
-k_czt_rt(const void* __restrict__ xin, int complex_in, long long x_stride, long long N, long long M, long long batch,
+k_czt_rt(const void* __restrict__ xin, long long x_stride, long long N, long long M, long long batch,
          int nseg, long long seg_len, long long cin_stride, cx_t<T>* __restrict__ out, long long out_stride,
          const cx_t<T>* __restrict__ tw, const cx_t<T>* __restrict__ cin, const cx_t<T>* __restrict__ khat,
          const cx_t<T>* __restrict__ cout) {
@@ -285,30 +286,32 @@ k_czt_rt(const void* __restrict__ xin, int complex_in, long long x_stride, long 
     for (int i = threadIdx.x; i < m_here; i += blockDim.x) s_co[i] = __ldg(cout + i);
     __syncthreads();
     const GroupSync gsync{1 + gid, G::NT};
-    const size_t xes = complex_in ? sizeof(C) : sizeof(T);
-    for (long long b = first * RG + gid; b < batch; b += team * RG) {
-        {   // the group's next trace into L2 while this one is transformed
-            const long long bn = b + team * RG;
-            if (bn < batch) {
-                const char* xn = reinterpret_cast<const char*>(xin) + (size_t)(bn * x_stride) * xes;
+    // raw samples of the group's current trace, loaded one trace ahead (register double buffer)
+    constexpr int NX = NZ < G::EPT ? NZ : G::EPT;
+    using XT = typename std::conditional<CPLX, C, T>::type;
+    XT xr[NX];
+    auto load_x = [&](long long bb) {
 #pragma unroll
-                for (int q = 0; q < G::EPT; ++q) {
-                    const long long pos = tid + (long long)G::NT * q;
-                    if (q < NZ && pos < N) prefetch_l2(xn + pos * xes);
-                }
-            }
+        for (int q = 0; q < NX; ++q) {
+            const long long pos = tid + (long long)G::NT * q;
+            if constexpr (CPLX) xr[q] = czero<C>();
+            else xr[q] = (T)0;
+            if (bb < batch && pos < N) xr[q] = __ldg(reinterpret_cast<const XT*>(xin) + bb * x_stride + pos);
         }
+    };
+    load_x(first * RG + gid);
+    for (long long b = first * RG + gid; b < batch; b += team * RG) {
         C v[G::EPT];
 #pragma unroll
         for (int q = 0; q < G::EPT; ++q) {
             v[q] = czero<C>();
             const long long pos = tid + (long long)G::NT * q;
-            if (q < NZ && pos < N) {
-                const C ch = s_cin[pos];
-                if (complex_in) v[q] = cmul(__ldg(reinterpret_cast<const C*>(xin) + b * x_stride + pos), ch);
-                else v[q] = rmul(__ldg(reinterpret_cast<const T*>(xin) + b * x_stride + pos), ch);
+            if (q < NX && pos < N) {
+                if constexpr (CPLX) v[q] = cmul(xr[q], s_cin[pos]);
+                else v[q] = rmul(xr[q], s_cin[pos]);
             }
         }
+        load_x(b + team * RG);   // in flight during this trace's two transforms
         block_fft<false, LOG2L, NZ>(v, sm, tws, tid, true, gsync);
 #pragma unroll
         for (int q = 0; q < G::EPT; ++q) {
@@ -385,17 +388,19 @@ cudaError_t run_czt(long long N, long long M, bool complex_in, const void* x, lo
         const size_t rts = rt_smem_bytes<T, LOG2L>(N, seg_len);
         static const bool rt_off = getenv("SKG_CZT_NO_RT") != nullptr;
         if (!rt_off && rts <= (size_t)smem_optin() && batch >= 8) {
-            auto kern = k_czt_rt<T, LOG2L, NZ, NO>;
-            cudaError_t e = prep_smem(kern, rts);
-            if (e != cudaSuccess) return e;
-            constexpr int RG = RtCfg<T, LOG2L>::RG;
-            // grid: resident CTAs, a multiple of nseg so every CTA owns one segment
-            long long g = persistent_grid(kern, RtCfg<T, LOG2L>::BLOCK, rts, (batch + RG - 1) / RG * nseg);
-            g = std::max<long long>(nseg, g / nseg * nseg);
-            kern<<<(unsigned)g, RtCfg<T, LOG2L>::BLOCK, rts, st>>>(
-                x, complex_in ? 1 : 0, x_stride, N, M, batch, nseg, seg_len, cin_stride, (C*)out, out_stride,
-                (const C*)tw, (const C*)cin, (const C*)khat, (const C*)cout);
-            return cudaGetLastError();
+            auto launch = [&](auto kern) {
+                cudaError_t e = prep_smem(kern, rts);
+                if (e != cudaSuccess) return e;
+                constexpr int RG = RtCfg<T, LOG2L>::RG;
+                // grid: resident CTAs, a multiple of nseg so every CTA owns one segment
+                long long g = persistent_grid(kern, RtCfg<T, LOG2L>::BLOCK, rts, (batch + RG - 1) / RG * nseg);
+                g = std::max<long long>(nseg, g / nseg * nseg);
+                kern<<<(unsigned)g, RtCfg<T, LOG2L>::BLOCK, rts, st>>>(
+                    x, x_stride, N, M, batch, nseg, seg_len, cin_stride, (C*)out, out_stride, (const C*)tw,
+                    (const C*)cin, (const C*)khat, (const C*)cout);
+                return cudaGetLastError();
+            };
+            return complex_in ? launch(k_czt_rt<T, LOG2L, NZ, NO, true>) : launch(k_czt_rt<T, LOG2L, NZ, NO, false>);
         }
     }
     auto kern = k_czt<T, LOG2L, NZ, NO>;
