@@ -243,7 +243,9 @@ struct FourStep {
     // traces per chunk so the work buffer stays L2 resident (~48 MB)
     long long chunk(bool f32) const {
         const long long bytes = L * (f32 ? 8 : 16);
-        return std::max<long long>(1, (48LL << 20) / bytes);
+        const char* e = std::getenv("SKG_4STEP_CHUNK_MB");
+        const long long mb = e ? std::atoll(e) : 96;
+        return std::max<long long>(1, (mb << 20) / bytes);
     }
 };
 

@@ -102,7 +102,7 @@ k_zoom(const T* __restrict__ x, long long x_stride, long long batch, ZoomArgs a,
                         const int n = i * V + e;
                         const int ph = dpow2 ? (n & (D - 1)) : n % D;
                         const int r = dpow2 ? (n >> ld) : n / D;
-                        xs[ph * a.rs + zpad(r + a.pre)] = buf[u][e];
+                        xs[ph * a.rs + zpad(r + a.pre + (ph != 0))] = buf[u][e];
                     }
                 }
             }
@@ -110,7 +110,7 @@ k_zoom(const T* __restrict__ x, long long x_stride, long long batch, ZoomArgs a,
         for (int n = nv * V + tid; n < U; n += NTH) {   // tail (or the whole row when unaligned)
             const int ph = dpow2 ? (n & (D - 1)) : n % D;
             const int r = dpow2 ? (n >> ld) : n / D;
-            xs[ph * a.rs + zpad(r + a.pre)] = __ldg(xr + n);
+            xs[ph * a.rs + zpad(r + a.pre + (ph != 0))] = __ldg(xr + n);
         }
     }
     __syncthreads();
@@ -127,7 +127,7 @@ k_zoom(const T* __restrict__ x, long long x_stride, long long batch, ZoomArgs a,
                 const int tm = dpow2 ? (t & (D - 1)) : t % D;
                 const int trow = tm ? D - tm : 0;   // phase row holding tap t
                 const C g = __ldg(gph + trow * a.lh + (dpow2 ? (t >> ld) : t / D));
-                acc = cadd(acc, rmul(xs[ph * a.rs + zpad(r + a.pre)], g));
+                acc = cadd(acc, rmul(xs[ph * a.rs + zpad(r + a.pre + (ph != 0))], g));
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
@@ -146,30 +146,59 @@ k_zoom(const T* __restrict__ x, long long x_stride, long long batch, ZoomArgs a,
 #pragma unroll
         for (int c = 0; c < ZK; ++c) acc[c] = czero<C>();
         const int m0 = chunk * ZK + a.trim;
-        for (int ph = 0; ph < D; ++ph) {
-            const T* row = xs + ph * a.rs;
-            const int delta = ph != 0 ? 1 : 0;
-            const C* gr = gph + ph * a.lh;
-            // window w[c] = row[m0 + c - l - delta] at tap l, slid by one sample per tap
-            T w[ZK];
-            const int base = m0 - delta + a.pre;
+        // rows with ph != 0 are stored one slot later, so every row is read at m - l (+ pre); when
+        // m0 + pre is a multiple of ZK the window is one padded group: a single address per ZK taps
+        const int base = m0 + a.pre;
+        if ((base & (ZK - 1)) == 0) {
+            const int gb = zpad(base);
+            for (int ph = 0; ph < D; ++ph) {
+                const T* row = xs + ph * a.rs + gb;
+                const C* gr = gph + ph * a.lh;
+                T w[ZK];
 #pragma unroll
-            for (int c = 0; c < ZK; ++c) w[c] = row[zpad(base + c)];
-            for (int l0 = 0; l0 < a.lh; l0 += ZK) {
-                T nw[ZK];
+                for (int c = 0; c < ZK; ++c) w[c] = row[c];
+                for (int l0 = 0; l0 < a.lh; l0 += ZK) {
+                    const T* nr = row - (ZK + 1) * (l0 / ZK + 1);
+                    T nw[ZK];
 #pragma unroll
-                for (int c = 0; c < ZK; ++c) nw[c] = row[zpad(base - l0 - ZK + c)];
+                    for (int c = 0; c < ZK; ++c) nw[c] = nr[c];
 #pragma unroll
-                for (int s = 0; s < ZK; ++s) {
-                    const C g = __ldg(gr + l0 + s);
+                    for (int s2 = 0; s2 < ZK; ++s2) {
+                        const C g = __ldg(gr + l0 + s2);
 #pragma unroll
-                    for (int c = 0; c < ZK; ++c) {
-                        acc[c].x = fma(g.x, w[c], acc[c].x);
-                        acc[c].y = fma(g.y, w[c], acc[c].y);
+                        for (int c = 0; c < ZK; ++c) {
+                            acc[c].x = fma(g.x, w[c], acc[c].x);
+                            acc[c].y = fma(g.y, w[c], acc[c].y);
+                        }
+#pragma unroll
+                        for (int c = ZK - 1; c > 0; --c) w[c] = w[c - 1];
+                        w[0] = nw[ZK - 1 - s2];
                     }
+                }
+            }
+        } else {
+            for (int ph = 0; ph < D; ++ph) {
+                const T* row = xs + ph * a.rs;
+                const C* gr = gph + ph * a.lh;
+                T w[ZK];
 #pragma unroll
-                    for (int c = ZK - 1; c > 0; --c) w[c] = w[c - 1];
-                    w[0] = nw[ZK - 1 - s];
+                for (int c = 0; c < ZK; ++c) w[c] = row[zpad(base + c)];
+                for (int l0 = 0; l0 < a.lh; l0 += ZK) {
+                    T nw[ZK];
+#pragma unroll
+                    for (int c = 0; c < ZK; ++c) nw[c] = row[zpad(base - l0 - ZK + c)];
+#pragma unroll
+                    for (int s2 = 0; s2 < ZK; ++s2) {
+                        const C g = __ldg(gr + l0 + s2);
+#pragma unroll
+                        for (int c = 0; c < ZK; ++c) {
+                            acc[c].x = fma(g.x, w[c], acc[c].x);
+                            acc[c].y = fma(g.y, w[c], acc[c].y);
+                        }
+#pragma unroll
+                        for (int c = ZK - 1; c > 0; --c) w[c] = w[c - 1];
+                        w[0] = nw[ZK - 1 - s2];
+                    }
                 }
             }
         }
