@@ -38,24 +38,29 @@ k_zoom(const T* __restrict__ x, long long x_stride, long long batch, ZoomArgs a,
        const cx_t<T>* __restrict__ gph,     // taps by phase row: gph[ph * lh + l] = g[l D + (D - ph) % D]
        const cx_t<T>* __restrict__ S,       // S[m], m < nout (already offset by trim)
        const cx_t<T>* __restrict__ tw, const cx_t<T>* __restrict__ band, cx_t<T>* __restrict__ out,
-       long long out_stride) {
+       long long out_stride, int groups, int gbytes) {
     using C = cx_t<T>;
     using G = FftGeom<LOG2N>;
-    constexpr int NTH = ZoomCfg<LOG2N>::NTH;
+    // the CTA carries `groups` traces, one per group of GT threads (small records: several per CTA)
+    const int GT = ZoomCfg<LOG2N>::NTH / groups;
+    const int gi = threadIdx.x / GT;
     extern __shared__ __align__(16) unsigned char smraw[];
-    // shared layout: [FFT buffer][twiddles][wrap terms: mwrap complex][polyphase rows]
-    C* fb = reinterpret_cast<C*>(smraw);
-    C* tws = fb + (G::L + (G::L >> 4) + 1);
-    C* cw = tws + G::TW_ALLOC;
+    // shared layout: [twiddles][per group: FFT buffer | wrap terms (mwrap complex) | polyphase rows]
+    C* tws = reinterpret_cast<C*>(smraw);
+    C* fb = reinterpret_cast<C*>(smraw + ((G::TW_ALLOC * sizeof(C) + 15) / 16 * 16) + (size_t)gi * gbytes);
+    C* cw = fb + (G::L + (G::L >> 4) + 1);
     T* xs = reinterpret_cast<T*>(cw + (a.mwrap + 1));
-    const long long b = blockIdx.x;
-    const int tid = threadIdx.x;
+    const long long b_raw = (long long)blockIdx.x * groups + gi;
+    const bool active = b_raw < batch;
+    const long long b = active ? b_raw : batch - 1;   // inactive groups recompute the last trace, store nothing
+    const int tid = threadIdx.x % GT;
     const int lane = tid & 31, warp = tid >> 5;
     const T* xr = x + b * x_stride;
     const int D = a.D;
     const int U = (int)a.U;
     const bool dpow2 = (D & (D - 1)) == 0;
     const int ld = 31 - __clz(D);
+    const int NTH = GT;
 
     // 1. trace -> polyphase rows (zero prefix and tail); clear the FFT buffer; twiddles
     if constexpr (G::L >= 16) load_twiddles<LOG2N>(tws, tw);
@@ -64,8 +69,8 @@ k_zoom(const T* __restrict__ x, long long x_stride, long long batch, ZoomArgs a,
     for (int i = tid; i < G::L; i += NTH) fb[pad16(i)] = czero<C>();
     __syncthreads();
     // the CTA that takes the next trace (blockIdx + gridDim) gets its row pulled into L2 now
-    if (b + gridDim.x < batch) {
-        const T* xn = x + (b + gridDim.x) * x_stride;
+    if (b_raw + (long long)gridDim.x * groups < batch) {
+        const T* xn = x + (b_raw + (long long)gridDim.x * groups) * x_stride;
         for (int n = tid * (128 / (int)sizeof(T)); n < U; n += NTH * (128 / (int)sizeof(T))) prefetch_l2(xn + n);
     }
     {
@@ -230,6 +235,7 @@ k_zoom(const T* __restrict__ x, long long x_stride, long long batch, ZoomArgs a,
 
     // 5. signed band window x D x group-delay phase (zoomfft.cpp:209-234)
     C* o = out + b * out_stride;
+    if (active)
     for (int i = tid; i < a.nbins; i += NTH) {
         const int k = a.k_lo + i;
         const int idx = ((k % G::L) + G::L) % G::L;
@@ -244,13 +250,21 @@ static cudaError_t run_zoom(const ZoomArgs& a, const T* x, long long x_stride, l
     using C = cx_t<T>;
     using G = FftGeom<LOG2N>;
     constexpr int NTH = ZoomCfg<LOG2N>::NTH;
-    constexpr int kFb = G::L + (G::L >> 4) + 1 + G::TW_ALLOC;
-    const size_t smem = (size_t)(kFb + a.mwrap + 1) * sizeof(C) + (size_t)a.D * a.rs * sizeof(T);
+    const size_t twb = (G::TW_ALLOC * sizeof(C) + 15) / 16 * 16;
+    const size_t per = ((size_t)(G::L + (G::L >> 4) + 1 + a.mwrap + 1) * sizeof(C) + (size_t)a.D * a.rs * sizeof(T) +
+                        15) / 16 * 16;
+    // several small records per CTA (one per >= 32-thread group) while a CTA stays <= ~56 KB
+    int groups = 1;
+    while (groups < 4 && NTH / (groups * 2) >= 32 && NTH / (groups * 2) >= G::NT &&
+           twb + per * groups * 2 <= 56 * 1024 && (long long)groups * 2 * 32 <= batch * 32)
+        groups *= 2;
+    const size_t smem = twb + per * groups;
     auto kern = k_zoom<T, LOG2N>;
     cudaError_t e = prep_smem(kern, smem);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)batch, NTH, smem, st>>>(x, x_stride, batch, a, (const C*)g, (const C*)S, (const C*)tw,
-                                             (const C*)band, (C*)out, out_stride);
+    kern<<<(unsigned)((batch + groups - 1) / groups), NTH, smem, st>>>(x, x_stride, batch, a, (const C*)g, (const C*)S,
+                                                                       (const C*)tw, (const C*)band, (C*)out,
+                                                                       out_stride, groups, (int)per);
     return cudaGetLastError();
 }
 
@@ -305,7 +319,7 @@ size_t zoom_smem_bytes(const ZoomArgs& a, int log2n, bool f32) {
         tw = FftGeom<decltype(lg)::value>::TW_ALLOC;
         return cudaSuccess;
     });
-    return (L + (L >> 4) + 1 + tw + a.mwrap + 1) * cs + (size_t)a.D * a.rs * rs;
+    return ((size_t)tw * cs + 15) / 16 * 16 + ((L + (L >> 4) + 1 + a.mwrap + 1) * cs + (size_t)a.D * a.rs * rs + 15) / 16 * 16;
 }
 }  // namespace skg
 
