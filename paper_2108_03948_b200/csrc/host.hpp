@@ -133,10 +133,22 @@ struct ZoomOptionsG {                 // ZoomOptions, zoomfft.hpp:17-26
     bool pad_pow2 = true;
 };
 
+struct ZoomFields {                   // the public fields of ZoomFftPlan (zoomfft.hpp:34-50)
+    double f1_hz = 0, f2_hz = 0, center_hz = 0, sample_rate_hz = 0, cutoff_hz = 0;
+    size_t decimation = 1;
+    std::vector<double> filter_taps;
+    double group_delay_samples = 0;
+    bool circular = true, trim_transient = false, pad_pow2 = true;
+    size_t input_len = 0, usable_len = 0, trim_samples = 0, decimated_len = 0, n_fft = 0;
+};
+
 class ZoomPlanG {                     // ZoomFftPlan + make_zoom_plan, zoomfft.hpp:33-56
   public:
     ZoomPlanG(size_t input_len, double f1, double f2, double fs, const ZoomOptionsG& o,
               size_t n_fft_override = 0, const double* taps = nullptr, size_t num_taps = 0);
+    // a plan whose public fields were set (or edited) directly, as the reference's ZoomFftPlan allows
+    // (zoomfft.hpp:33-56): band window and chirp-route plan are derived from the fields
+    static std::unique_ptr<ZoomPlanG> from_fields(const ZoomFields& fields);
     double f1_hz, f2_hz, center_hz, sample_rate_hz, cutoff_hz;
     size_t decimation = 1;
     std::vector<double> filter_taps;
@@ -151,6 +163,7 @@ class ZoomPlanG {                     // ZoomFftPlan + make_zoom_plan, zoomfft.h
                  bool f32, cudaStream_t st) const;
 
   private:
+    ZoomPlanG() = default;
     struct Dev {
         DevMem g, sdec, wrap, band;
     };

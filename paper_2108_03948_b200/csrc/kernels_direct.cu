@@ -88,3 +88,45 @@ cudaError_t launch_czt_direct(const void* x, long long n, double a_logm, double 
 }
 
 }  // namespace skg
+
+// ---- zoom helper stages exposed by the reference's C++ API (zoomfft.hpp:63-75) --------------
+namespace skg {
+
+__global__ void k_freq_shift(const double* __restrict__ xr, const double2* __restrict__ xc, long long n, double q,
+                             double2* __restrict__ y) {
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double2 c = d_cis_cycles(q, (double)i);   // zoomfft.cpp:44-64 per-sample phase
+    y[i] = xr ? make_double2(xr[i] * c.x, xr[i] * c.y) : cmul(xc[i], c);
+}
+
+__global__ void k_filter_decimate(const double2* __restrict__ x, long long n, const double* __restrict__ taps, int T,
+                                  int d, int circular, double2* __restrict__ out, long long nout) {
+    const long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (m >= nout) return;
+    const long long base = m * d;
+    double2 acc = make_double2(0.0, 0.0);
+    const long long t_end = circular ? T : (T < base + 1 ? T : base + 1);
+    for (long long t = 0; t < t_end; ++t) {   // zoomfft.cpp:66-104
+        const long long j = base >= t ? base - t : base + n - t;
+        const double h = __ldg(taps + t);
+        const double2 v = __ldg(x + j);
+        acc.x += h * v.x;
+        acc.y += h * v.y;
+    }
+    out[m] = acc;
+}
+
+cudaError_t launch_freq_shift(const double* xr, const void* xc, long long n, double q, void* y, cudaStream_t st) {
+    k_freq_shift<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(xr, (const double2*)xc, n, q, (double2*)y);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_filter_decimate(const void* x, long long n, const double* taps, int T, int d, int circular,
+                                   void* out, long long nout, cudaStream_t st) {
+    k_filter_decimate<<<(unsigned)((nout + 127) / 128), 128, 0, st>>>((const double2*)x, n, taps, T, d, circular,
+                                                                      (double2*)out, nout);
+    return cudaGetLastError();
+}
+
+}  // namespace skg

@@ -69,6 +69,33 @@ ZoomPlanG::ZoomPlanG(size_t in_len, double f1, double f2, double fs, const ZoomO
                                                 cis_cycles(-1.0 / static_cast<double>(n_fft), 1.0), n_fft);
 }
 
+std::unique_ptr<ZoomPlanG> ZoomPlanG::from_fields(const ZoomFields& f) {
+    std::unique_ptr<ZoomPlanG> p(new ZoomPlanG());
+    p->f1_hz = f.f1_hz;
+    p->f2_hz = f.f2_hz;
+    p->center_hz = f.center_hz;
+    p->sample_rate_hz = f.sample_rate_hz;
+    p->cutoff_hz = f.cutoff_hz;
+    p->decimation = f.decimation;
+    p->filter_taps = f.filter_taps;
+    p->group_delay_samples = f.group_delay_samples;
+    p->circular = f.circular;
+    p->trim_transient = f.trim_transient;
+    p->pad_pow2 = f.pad_pow2;
+    p->input_len = f.input_len;
+    p->usable_len = f.usable_len;
+    p->trim_samples = f.trim_samples;
+    p->decimated_len = f.decimated_len;
+    p->n_fft = f.n_fft;
+    if (p->decimation == 0 || p->filter_taps.empty() || p->n_fft < p->decimated_len || p->decimated_len == 0)
+        throw std::invalid_argument("zoom_fft: inconsistent plan fields");
+    p->compute_band();
+    if (!is_pow2(p->n_fft))
+        p->bluestein_ = std::make_unique<CztPlanG>(p->n_fft, cd(1.0, 0.0),
+                                                   cis_cycles(-1.0 / static_cast<double>(p->n_fft), 1.0), p->n_fft);
+    return p;
+}
+
 double ZoomPlanG::f_step_hz() const {   // zoomfft.cpp:11-13
     return sample_rate_hz / (static_cast<double>(decimation) * static_cast<double>(n_fft));
 }
