@@ -102,8 +102,15 @@ int main() {
     CHECK(s500.size() == 500);
     for (const auto& v : s500.bins) CHECK(std::abs(std::abs(v) - 1.0) < 1e-9);
     CHECK(throws_invalid([&] { fft_spectrum(imp, 499); }));
-    const Spectrum cut = slice_band(s512, 1e12, 2e12);
-    CHECK(cut.f_start_hz >= 1e12 && cut.f_end_hz() <= 2e12 && cut.source_n == 512);
+    // slice_band keeps inclusive edges (test_spectra.cpp:61-80). Note the reference's edge slack is
+    // 0.5 * f_step * 1e-9 in BIN units (spectra.cpp:44), i.e. many bins for THz steps; we keep it.
+    Spectrum lin11;
+    lin11.f_step_hz = 10.0;
+    lin11.source_n = 64;
+    for (int k = 0; k < 11; ++k) lin11.bins.push_back(cplx(k, 0));
+    const Spectrum cut = slice_band(lin11, 20.0, 50.0);
+    CHECK(cut.size() == 4 && cut.f_start_hz == 20.0 && cut.bins[3].real() == 5.0 && cut.source_n == 64);
+    CHECK(throws_invalid([&] { slice_band(lin11, 500.0, 600.0); }));
     const Spectrum cs = czt_spectrum(imp, 0.0, 2.5e12, 125);
     CHECK(cs.size() == 125 && std::abs(cs.f_step_hz - 2e10) < 1e-3);
     // zoom: default plan sizing, helpers, degenerate zoom, edited public fields
