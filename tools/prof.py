@@ -32,6 +32,17 @@ def run(name, steps):
         p = sk.TransferPlanGPU(ref, 8192, sk.SKG_F32)
         xd = torch.from_numpy(cube).to(dev)
         fn = lambda: p.execute(xd)  # noqa: E731
+    elif name.startswith("spec4step"):
+        f32 = name.endswith("32")
+        x = W.sample_traces(2048, 16384).astype(np.float32 if f32 else np.float64)
+        xd = torch.from_numpy(x).to(dev)
+        fn = lambda: sk.fft_spectrum_batch(xd, 65536)  # noqa: E731
+    elif name == "czt4step":
+        x = W.sample_traces(1024, 16384)
+        a, w = W.cfg2_czt_params(16384)
+        p = sk.CztPlanGPU(16384, a, w, 16384, sk.SKG_F64)
+        xd = torch.from_numpy(x).to(dev)
+        fn = lambda: p.execute(xd)  # noqa: E731
     elif name == "spec64":
         x = W.sample_traces(32768, 1024)
         xd = torch.from_numpy(x).to(dev)

@@ -74,12 +74,18 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1_cfg5_sweep.json"))
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--max-seconds", type=float, default=1.5, help="cap on one batch's kernel time")
+    ap.add_argument("--ns", default="", help="comma list of N to run (default: all)")
+    ap.add_argument("--kinds", default="fft,czt,zoom")
+    ap.add_argument("--precs", default="f64,f32")
     args = ap.parse_args()
     pk = peaks()
     fp = {"f64": fp_peak_tflops(torch.float64), "f32": fp_peak_tflops(torch.float32)}
     rows = []
     Ns = [1000, 1024, 3000, 4096, 16384, 65536] if not args.quick else [1000, 4096]
-    for prec in ("f64", "f32"):
+    if args.ns:
+        Ns = [int(v) for v in args.ns.split(",")]
+    kinds = set(args.kinds.split(","))
+    for prec in args.precs.split(","):
         dt = torch.float64 if prec == "f64" else torch.float32
         s = 8 if prec == "f64" else 4
         P = sk.SKG_F64 if prec == "f64" else sk.SKG_F32
@@ -89,11 +95,14 @@ def main():
             xh2 = x[:2].double().cpu().numpy()
             jobs = []
             L = 4 * O.next_pow2(N)
-            jobs.append(("fft", {"L": L}))
-            for M in (N // 4, N, 4 * N):
-                jobs.append(("czt", {"M": M}))
-            for D in (4, 16):
-                jobs.append(("zoom", {"D": D}))
+            if "fft" in kinds:
+                jobs.append(("fft", {"L": L}))
+            if "czt" in kinds:
+                for M in (N // 4, N, 4 * N):
+                    jobs.append(("czt", {"M": M}))
+            if "zoom" in kinds:
+                for D in (4, 16):
+                    jobs.append(("zoom", {"D": D}))
             for kind, kw in jobs:
                 torch.cuda.empty_cache()
                 if kind == "fft":
