@@ -205,10 +205,11 @@ template <int R, bool INV, int NZ, int NO, typename C> __device__ __forceinline_
 }
 
 // ---- geometry of an L = 2^LOG2L transform ------------------------------------------------
-// Twiddles of pass s (p = 16^s) are W_{pR}^{jk}, k < p. They are stored factorised by the base-16
-// digits of k: W_{pR}^{jk} = prod_d W_{pR/16^d}^{j k_d}, one (R-1) x 16 table per digit, so a
-// whole transform needs only sum_s s*(R_s-1)*16 entries (720 for L = 4096) and the tables live in
-// shared memory next to the data (no global loads inside the passes).
+// Twiddles of pass s (p = 16^s) are W_{pR}^{jk}, k < p, j < R. Only W_{pR}^{k} is stored, factorised
+// by the base-16 digits of k (W_{pR}^{k} = prod_d W_{pR/16^d}^{k_d}: one 16-entry table per digit,
+// 48 entries for L = 4096) in shared memory; the powers j = 2..R-1 are formed in registers by
+// balanced products (depth <= 4). The passes are shared-memory-bandwidth bound (LDS.128 costs four
+// wavefronts whatever the broadcast), so trading table reads for FP instructions pays.
 template <int LOG2L> struct FftGeom {
     static constexpr int L = 1 << LOG2L;
     static constexpr int EPT = L < 16 ? L : 16;        // elements per thread
@@ -218,17 +219,48 @@ template <int LOG2L> struct FftGeom {
     static constexpr int SMEM = L < 16 ? 0 : L + (L >> 4);   // padded elements per transform
     __host__ __device__ static constexpr int radix(int s) { return L < 16 ? L : (s < P - 1 ? 16 : RLAST); }
     __host__ __device__ static constexpr int pval(int s) { return 1 << (4 * s); }
-    // offset of the digit-d table of pass s
+    // offset of the digit-d table of pass s (16 entries: W_{pR/16^d}^{kd}, kd < 16)
     __host__ __device__ static constexpr int tw_off(int s, int d) {
         int o = 0;
-        for (int t = 1; t < s; ++t) o += t * (radix(t) - 1) * 16;
-        return o + d * (radix(s) - 1) * 16;
+        for (int t = 1; t < s; ++t) o += t * 16;
+        return o + d * 16;
     }
     static constexpr int TW_SIZE = tw_off(P, 0);   // entries (pass 0 needs none)
     static constexpr int TW_ALLOC = TW_SIZE > 0 ? TW_SIZE : 1;
 };
 
 __device__ __forceinline__ int pad16(int a) { return a + (a >> 4); }
+
+// u[j] *= W^{jk}, j = 1..R-1, from w1 = W^{k} alone: squarings give w2, w4, w8 and the rest are
+// single products applied as soon as they are formed (few twiddles live; product depth <= 4)
+template <bool INV, int R, typename C> __device__ __forceinline__ void apply_twiddles(C (&u)[R], C w1) {
+    if constexpr (R >= 2) u[1] = twmul<INV>(u[1], w1);
+    if constexpr (R >= 4) {
+        const C w2 = cmul(w1, w1);
+        const C w3 = cmul(w2, w1);
+        u[2] = twmul<INV>(u[2], w2);
+        u[3] = twmul<INV>(u[3], w3);
+        if constexpr (R >= 8) {
+            const C w4 = cmul(w2, w2);
+            u[4] = twmul<INV>(u[4], w4);
+            const C w5 = cmul(w4, w1), w6 = cmul(w4, w2), w7 = cmul(w4, w3);
+            u[5] = twmul<INV>(u[5], w5);
+            u[6] = twmul<INV>(u[6], w6);
+            u[7] = twmul<INV>(u[7], w7);
+            if constexpr (R >= 16) {
+                const C w8 = cmul(w4, w4);
+                u[8] = twmul<INV>(u[8], w8);
+                u[9] = twmul<INV>(u[9], cmul(w8, w1));
+                u[10] = twmul<INV>(u[10], cmul(w8, w2));
+                u[11] = twmul<INV>(u[11], cmul(w8, w3));
+                u[12] = twmul<INV>(u[12], cmul(w8, w4));
+                u[13] = twmul<INV>(u[13], cmul(w8, w5));
+                u[14] = twmul<INV>(u[14], cmul(w8, w6));
+                u[15] = twmul<INV>(u[15], cmul(w8, w7));
+            }
+        }
+    }
+}
 
 // cache-line prefetches (no registers consumed; the data waits in L1 / L2 for the real load)
 __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
@@ -277,13 +309,10 @@ __device__ __forceinline__ void stockham_pass(C (&v)[FftGeom<LOG2L>::EPT], C* sm
         const int i = tid + G::NT * b;
         const int k = i & (p - 1);
         if constexpr (p > 1) {
+            C w1 = tw[G::tw_off(S, 0) + (k & 15)];
 #pragma unroll
-            for (int j = 1; j < R; ++j) {
-                C w = tw[G::tw_off(S, 0) + (j - 1) * 16 + (k & 15)];
-#pragma unroll
-                for (int d = 1; d < S; ++d) w = cmul(w, tw[G::tw_off(S, d) + (j - 1) * 16 + ((k >> (4 * d)) & 15)]);
-                u[j] = twmul<INV>(u[j], w);
-            }
+            for (int d = 1; d < S; ++d) w1 = cmul(w1, tw[G::tw_off(S, d) + ((k >> (4 * d)) & 15)]);
+            apply_twiddles<INV, R>(u, w1);
         }
         dft_r<R, INV, (S == 0 ? NZ : 16), (last ? NO : 16)>(u);
         if constexpr (last) {

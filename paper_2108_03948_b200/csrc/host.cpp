@@ -160,12 +160,10 @@ template <int LG> void stockham_host(std::vector<cd>& out) {
         for (int s = 1; s < G::P; ++s) {
             const int R = G::radix(s);
             for (int d = 0; d < s; ++d) {
-                // digit d of k carries weight 16^d: W_{pR}^{j kd 16^d} = W_{M}^{j kd}, M = R 16^{s-d}
+                // digit d of k carries weight 16^d: W_{pR}^{kd 16^d} = W_{M}^{kd}, M = R 16^{s-d}
                 const double M = static_cast<double>(R) * static_cast<double>(1 << (4 * (s - d)));
                 const double q = -1.0 / M;   // exact power of two
-                for (int j = 1; j < R; ++j)
-                    for (int kd = 0; kd < 16; ++kd)
-                        out[G::tw_off(s, d) + (j - 1) * 16 + kd] = cis_cycles(q, static_cast<double>(j * kd));
+                for (int kd = 0; kd < 16; ++kd) out[G::tw_off(s, d) + kd] = cis_cycles(q, static_cast<double>(kd));
             }
         }
     }
@@ -244,7 +242,7 @@ struct FourStep {
     long long chunk(bool f32) const {
         const long long bytes = L * (f32 ? 8 : 16);
         const char* e = std::getenv("SKG_4STEP_CHUNK_MB");
-        const long long mb = e ? std::atoll(e) : 96;
+        const long long mb = e ? std::atoll(e) : 32;
         return std::max<long long>(1, (mb << 20) / bytes);
     }
 };
