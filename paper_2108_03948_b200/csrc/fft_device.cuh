@@ -219,11 +219,12 @@ template <int LOG2L> struct FftGeom {
     static constexpr int SMEM = L < 16 ? 0 : L + (L >> 4);   // padded elements per transform
     __host__ __device__ static constexpr int radix(int s) { return L < 16 ? L : (s < P - 1 ? 16 : RLAST); }
     __host__ __device__ static constexpr int pval(int s) { return 1 << (4 * s); }
-    // offset of the digit-d table of pass s (16 entries: W_{pR/16^d}^{kd}, kd < 16)
+    // offset of the digit-d table of pass s: 4 x 16 entries W_{pR/16^d}^{j kd}, j in {1, 2, 4, 8}
+    // (fp64 reads only j = 1; fp32 reads the four so no twiddle carries more than 4 roundings)
     __host__ __device__ static constexpr int tw_off(int s, int d) {
         int o = 0;
-        for (int t = 1; t < s; ++t) o += t * 16;
-        return o + d * 16;
+        for (int t = 1; t < s; ++t) o += t * 64;
+        return o + d * 64;
     }
     static constexpr int TW_SIZE = tw_off(P, 0);   // entries (pass 0 needs none)
     static constexpr int TW_ALLOC = TW_SIZE > 0 ? TW_SIZE : 1;
@@ -233,22 +234,25 @@ __device__ __forceinline__ int pad16(int a) { return a + (a >> 4); }
 
 // u[j] *= W^{jk}, j = 1..R-1, from w1 = W^{k} alone: squarings give w2, w4, w8 and the rest are
 // single products applied as soon as they are formed (few twiddles live; product depth <= 4)
-template <bool INV, int R, typename C> __device__ __forceinline__ void apply_twiddles(C (&u)[R], C w1) {
+template <bool INV, int R, typename C>
+__device__ __forceinline__ void apply_twiddles(C (&u)[R], C w1, C l2 = C(), C l4 = C(), C l8 = C()) {
+    // fp32: w2, w4, w8 come from the tables (l2, l4, l8); fp64: by squaring
+    constexpr bool loaded = sizeof(sc_t<C>) == 4;
     if constexpr (R >= 2) u[1] = twmul<INV>(u[1], w1);
     if constexpr (R >= 4) {
-        const C w2 = cmul(w1, w1);
+        const C w2 = loaded ? l2 : cmul(w1, w1);
         const C w3 = cmul(w2, w1);
         u[2] = twmul<INV>(u[2], w2);
         u[3] = twmul<INV>(u[3], w3);
         if constexpr (R >= 8) {
-            const C w4 = cmul(w2, w2);
+            const C w4 = loaded ? l4 : cmul(w2, w2);
             u[4] = twmul<INV>(u[4], w4);
             const C w5 = cmul(w4, w1), w6 = cmul(w4, w2), w7 = cmul(w4, w3);
             u[5] = twmul<INV>(u[5], w5);
             u[6] = twmul<INV>(u[6], w6);
             u[7] = twmul<INV>(u[7], w7);
             if constexpr (R >= 16) {
-                const C w8 = cmul(w4, w4);
+                const C w8 = loaded ? l8 : cmul(w4, w4);
                 u[8] = twmul<INV>(u[8], w8);
                 u[9] = twmul<INV>(u[9], cmul(w8, w1));
                 u[10] = twmul<INV>(u[10], cmul(w8, w2));
@@ -309,10 +313,19 @@ __device__ __forceinline__ void stockham_pass(C (&v)[FftGeom<LOG2L>::EPT], C* sm
         const int i = tid + G::NT * b;
         const int k = i & (p - 1);
         if constexpr (p > 1) {
-            C w1 = tw[G::tw_off(S, 0) + (k & 15)];
+            // W^{jk} for j = 1 (and 2, 4, 8 in fp32) from the per-digit tables
+            auto wj = [&](int jj) {
+                C w = tw[G::tw_off(S, 0) + jj * 16 + (k & 15)];
 #pragma unroll
-            for (int d = 1; d < S; ++d) w1 = cmul(w1, tw[G::tw_off(S, d) + ((k >> (4 * d)) & 15)]);
-            apply_twiddles<INV, R>(u, w1);
+                for (int d = 1; d < S; ++d) w = cmul(w, tw[G::tw_off(S, d) + jj * 16 + ((k >> (4 * d)) & 15)]);
+                return w;
+            };
+            if constexpr (sizeof(sc_t<C>) == 8) {
+                apply_twiddles<INV, R>(u, wj(0));
+            } else {
+                apply_twiddles<INV, R>(u, wj(0), R >= 4 ? wj(1) : czero<C>(), R >= 8 ? wj(2) : czero<C>(),
+                                       R >= 16 ? wj(3) : czero<C>());
+            }
         }
         dft_r<R, INV, (S == 0 ? NZ : 16), (last ? NO : 16)>(u);
         if constexpr (last) {

@@ -163,7 +163,9 @@ template <int LG> void stockham_host(std::vector<cd>& out) {
                 // digit d of k carries weight 16^d: W_{pR}^{kd 16^d} = W_{M}^{kd}, M = R 16^{s-d}
                 const double M = static_cast<double>(R) * static_cast<double>(1 << (4 * (s - d)));
                 const double q = -1.0 / M;   // exact power of two
-                for (int kd = 0; kd < 16; ++kd) out[G::tw_off(s, d) + kd] = cis_cycles(q, static_cast<double>(kd));
+                for (int jj = 0; jj < 4; ++jj)
+                    for (int kd = 0; kd < 16; ++kd)
+                        out[G::tw_off(s, d) + jj * 16 + kd] = cis_cycles(q, static_cast<double>((1 << jj) * kd));
             }
         }
     }
