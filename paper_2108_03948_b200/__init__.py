@@ -24,7 +24,7 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libspectralkit_b200.so")
+LIB_PATH = os.environ.get("SKG_LIB_PATH") or os.path.join(HERE, "lib", "libspectralkit_b200.so")
 
 SK_OK, SK_ERR_INVALID_ARGUMENT, SK_ERR_INTERNAL = 0, 1, 6
 SKG_F64, SKG_F32 = 0, 1

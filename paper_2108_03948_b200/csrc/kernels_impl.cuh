@@ -299,8 +299,22 @@ k_czt_rt(const void* __restrict__ xin, long long x_stride, long long N, long lon
             if (bb < batch && pos < N) xr[q] = __ldg(reinterpret_cast<const XT*>(xin) + bb * x_stride + pos);
         }
     };
-    load_x(first * RG + gid);
+#ifndef SKG_RT_XPREFETCH
+#define SKG_RT_XPREFETCH 0   // register double buffer measured slower (spills) than an L2 prefetch
+#endif
+    if (SKG_RT_XPREFETCH) load_x(first * RG + gid);
     for (long long b = first * RG + gid; b < batch; b += team * RG) {
+        if (!SKG_RT_XPREFETCH) {
+            load_x(b);
+            const long long bn = b + team * RG;   // and the group's next trace into L2
+            if (bn < batch) {
+#pragma unroll
+                for (int q = 0; q < NX; ++q) {
+                    const long long pos = tid + (long long)G::NT * q;
+                    if (pos < N) prefetch_l2(reinterpret_cast<const XT*>(xin) + bn * x_stride + pos);
+                }
+            }
+        }
         C v[G::EPT];
 #pragma unroll
         for (int q = 0; q < G::EPT; ++q) {
@@ -311,7 +325,7 @@ k_czt_rt(const void* __restrict__ xin, long long x_stride, long long N, long lon
                 else v[q] = rmul(xr[q], s_cin[pos]);
             }
         }
-        load_x(b + team * RG);   // in flight during this trace's two transforms
+        if (SKG_RT_XPREFETCH) load_x(b + team * RG);   // in flight during this trace's two transforms
         block_fft<false, LOG2L, NZ>(v, sm, tws, tid, true, gsync);
 #pragma unroll
         for (int q = 0; q < G::EPT; ++q) {
