@@ -215,15 +215,31 @@ template <int LOG2L> struct FftGeom {
     static constexpr int EPT = L < 16 ? L : 16;        // elements per thread
     static constexpr int NT = L / EPT;                  // threads per transform
     static constexpr int P = L < 16 ? 1 : (LOG2L + 3) / 4;   // passes
-    static constexpr int RLAST = L < 16 ? L : (1 << (LOG2L - 4 * (P - 1)));
+    static constexpr int RSMALL = L < 16 ? L : (1 << (LOG2L - 4 * (P - 1)));   // the one non-16 radix
     static constexpr int SMEM = L < 16 ? 0 : L + (L >> 4);   // padded elements per transform
-    __host__ __device__ static constexpr int radix(int s) { return L < 16 ? L : (s < P - 1 ? 16 : RLAST); }
-    __host__ __device__ static constexpr int pval(int s) { return 1 << (4 * s); }
+    // radix of pass s: 16 everywhere except one pass of RSMALL, placed second when there are >= 3
+    // passes so that the first (zero-input pruning) and the last (unneeded-output pruning) stay radix 16
+    __host__ __device__ static constexpr int radix(int s) {
+        if (L < 16) return L;
+        if (RSMALL == 16) return 16;
+#ifndef SKG_SMALL_RADIX_MID
+#define SKG_SMALL_RADIX_MID 0
+#endif
+        if (SKG_SMALL_RADIX_MID && P >= 3) return s == 1 ? RSMALL : 16;
+        return s < P - 1 ? 16 : RSMALL;
+    }
+    __host__ __device__ static constexpr int lg(int v) { return v <= 1 ? 0 : 1 + lg(v / 2); }
+    __host__ __device__ static constexpr int pval(int s) {   // product of the radices before pass s
+        int p = 1;
+        for (int t = 0; t < s; ++t) p *= radix(t);
+        return p;
+    }
+    __host__ __device__ static constexpr int digits(int s) { return (lg(pval(s)) + 3) / 4; }   // base-16 digits of k < p
     // offset of the digit-d table of pass s: 4 x 16 entries W_{pR/16^d}^{j kd}, j in {1, 2, 4, 8}
     // (fp64 reads only j = 1; fp32 reads the four so no twiddle carries more than 4 roundings)
     __host__ __device__ static constexpr int tw_off(int s, int d) {
         int o = 0;
-        for (int t = 1; t < s; ++t) o += t * 64;
+        for (int t = 1; t < s; ++t) o += digits(t) * 64;
         return o + d * 64;
     }
     static constexpr int TW_SIZE = tw_off(P, 0);   // entries (pass 0 needs none)
@@ -317,7 +333,7 @@ __device__ __forceinline__ void stockham_pass(C (&v)[FftGeom<LOG2L>::EPT], C* sm
             auto wj = [&](int jj) {
                 C w = tw[G::tw_off(S, 0) + jj * 16 + (k & 15)];
 #pragma unroll
-                for (int d = 1; d < S; ++d) w = cmul(w, tw[G::tw_off(S, d) + jj * 16 + ((k >> (4 * d)) & 15)]);
+                for (int d = 1; d < G::digits(S); ++d) w = cmul(w, tw[G::tw_off(S, d) + jj * 16 + ((k >> (4 * d)) & 15)]);
                 return w;
             };
             if constexpr (sizeof(sc_t<C>) == 8) {

@@ -159,9 +159,9 @@ template <int LG> void stockham_host(std::vector<cd>& out) {
     if constexpr (G::L >= 16) {
         for (int s = 1; s < G::P; ++s) {
             const int R = G::radix(s);
-            for (int d = 0; d < s; ++d) {
-                // digit d of k carries weight 16^d: W_{pR}^{kd 16^d} = W_{M}^{kd}, M = R 16^{s-d}
-                const double M = static_cast<double>(R) * static_cast<double>(1 << (4 * (s - d)));
+            for (int d = 0; d < G::digits(s); ++d) {
+                // digit d of k carries weight 16^d: W_{pR}^{kd 16^d} = W_{M}^{kd}, M = p R / 16^d
+                const double M = static_cast<double>(G::pval(s)) * R / static_cast<double>(1 << (4 * d));
                 const double q = -1.0 / M;   // exact power of two
                 for (int jj = 0; jj < 4; ++jj)
                     for (int kd = 0; kd < 16; ++kd)
