@@ -234,6 +234,14 @@ class Spectrum:
         return self.f_start_hz + k * self.f_step_hz
 
 
+def _release(fn, h):
+    """free a native handle; quiet at interpreter teardown (module globals may already be gone)"""
+    try:
+        getattr(lib(), fn)(h)
+    except Exception:
+        pass
+
+
 class Trace:
     """Owning wrapper of sk_trace (samples, fs, t0)."""
 
@@ -254,9 +262,9 @@ class Trace:
     def sample_rate_hz(self):
         return float(lib().sk_trace_sample_rate(self._h))
 
-    def __del__(self):
+    def __del__(self, _rel=_release):
         if getattr(self, "_h", None):
-            lib().sk_trace_free(self._h)
+            _rel("sk_trace_free", self._h)
             self._h = None
 
 
@@ -341,9 +349,9 @@ class ZoomPlan:
         _chk(lib().sk_zoom_spectrum(self._h, t.handle, C.byref(h)))
         return _take_spectrum(h)
 
-    def __del__(self):
+    def __del__(self, _rel=_release):
         if getattr(self, "_h", None):
-            lib().sk_zoom_plan_free(self._h)
+            _rel("sk_zoom_plan_free", self._h)
             self._h = None
 
 
@@ -434,9 +442,9 @@ class CztPlanGPU:
                                    out.stride(0), _stream()))
         return out
 
-    def __del__(self):
+    def __del__(self, _rel=_release):
         if getattr(self, "_h", None):
-            lib().skg_czt_plan_free(self._h)
+            _rel("skg_czt_plan_free", self._h)
             self._h = None
 
 
@@ -469,9 +477,9 @@ class TransferPlanGPU:
                                         h.stride(0) if h is not None else 0, _stream()))
         return mag, phase
 
-    def __del__(self):
+    def __del__(self, _rel=_release):
         if getattr(self, "_h", None):
-            lib().skg_transfer_plan_free(self._h)
+            _rel("skg_transfer_plan_free", self._h)
             self._h = None
 
 
@@ -506,7 +514,7 @@ class ZoomPlanGPU:
                                     _stream()))
         return out
 
-    def __del__(self):
+    def __del__(self, _rel=_release):
         if getattr(self, "_h", None):
-            lib().skg_zoom_plan_free(self._h)
+            _rel("skg_zoom_plan_free", self._h)
             self._h = None

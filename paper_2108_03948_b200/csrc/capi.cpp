@@ -1,7 +1,10 @@
 // capi.cpp — the drop-in sk_* C ABI (include/spectralkit.h) and the batched skg_* extension
 // (include/spectralkit_gpu.h). Error convention follows the reference's capi.cpp:44-83:
 // exceptions are mapped to status codes, the message goes to a thread-local string.
+#include <algorithm>
 #include <cmath>
+#include <memory>
+#include <mutex>
 #include <cstring>
 #include <new>
 #include <string>
@@ -95,18 +98,61 @@ void split(const std::vector<cd>& x, double* re, double* im) {
 }
 
 // one-shot staging: host -> device -> host on the per-thread default stream
+// Host-call staging: each calling thread keeps grow-only pinned host and device buffers, so a
+// single-trace C-ABI call costs two small copies and one kernel — no cudaMalloc/cudaFree (which
+// synchronise the device) and no pageable-memory bounce per call. Buffers are per device.
+struct Workspace {
+    struct Buf {
+        void* p = nullptr;
+        size_t cap = 0;
+    };
+    int dev = -1;
+    Buf hin, hout, din, dout;
+    static void grow(Buf& b, size_t bytes, bool host) {
+        if (bytes <= b.cap) return;
+        if (b.p) host ? cudaFreeHost(b.p) : cudaFree(b.p);
+        b.p = nullptr;
+        b.cap = 0;
+        const size_t cap = std::max<size_t>(bytes, 1 << 16);
+        skg::check(host ? cudaHostAlloc(&b.p, cap, cudaHostAllocDefault) : cudaMalloc(&b.p, cap),
+                   host ? "cudaHostAlloc" : "cudaMalloc");
+        b.cap = cap;
+    }
+    void bind() {
+        int d = 0;
+        skg::check(cudaGetDevice(&d), "cudaGetDevice");
+        if (d != dev) {   // a different device than last time: drop the old buffers' capacities
+            hin = hout = din = dout = Buf{};
+            dev = d;
+        }
+    }
+};
+thread_local Workspace t_ws;
+
 struct Stage {
+    struct Ptr {
+        void* p = nullptr;
+    };
     cudaStream_t st = cudaStreamPerThread;
-    skg::DevMem in, out;
+    Ptr in, out;
     void put(const void* h, size_t bytes) {
         skg::require_device();
-        in = skg::DevMem(bytes);
-        skg::check(cudaMemcpyAsync(in.p, h, bytes, cudaMemcpyHostToDevice, st), "H2D");
+        t_ws.bind();
+        Workspace::grow(t_ws.hin, bytes, true);
+        Workspace::grow(t_ws.din, bytes, false);
+        std::memcpy(t_ws.hin.p, h, bytes);
+        skg::check(cudaMemcpyAsync(t_ws.din.p, t_ws.hin.p, bytes, cudaMemcpyHostToDevice, st), "H2D");
+        in.p = t_ws.din.p;
     }
-    void alloc_out(size_t bytes) { out = skg::DevMem(bytes); }
+    void alloc_out(size_t bytes) {
+        Workspace::grow(t_ws.dout, bytes, false);
+        out.p = t_ws.dout.p;
+    }
     void get(void* h, size_t bytes) {
-        skg::check(cudaMemcpyAsync(h, out.p, bytes, cudaMemcpyDeviceToHost, st), "D2H");
+        Workspace::grow(t_ws.hout, bytes, true);
+        skg::check(cudaMemcpyAsync(t_ws.hout.p, out.p, bytes, cudaMemcpyDeviceToHost, st), "D2H");
         skg::check(cudaStreamSynchronize(st), "sync");
+        std::memcpy(h, t_ws.hout.p, bytes);
     }
 };
 
@@ -119,14 +165,45 @@ void fft_inplace(double* re, double* im, size_t n, bool inverse) {   // numerics
     Stage s;
     s.put(x.data(), n * sizeof(cd));
     skg::fft_c2c(n, inverse, false, s.in.p, 0, s.in.p, 0, 1, s.st);
-    s.out = std::move(s.in);
+    s.out = s.in;
     s.get(x.data(), n * sizeof(cd));
     split(x, re, im);
 }
 
+// The one-shot calls (sk_czt, sk_czt_spectrum) build a plan per call in the reference
+// (czt.cpp:139-142, 155-175); here the last few plans are kept, keyed on the exact bits of
+// (n, a, w, m), so a repeated call skips the O(L log L) table build and the uploads.
+const skg::CztPlanG& czt_plan_cached(size_t n, cd a, cd w, size_t m) {
+    struct Key {
+        size_t n, m;
+        double ar, ai, wr, wi;
+        bool operator==(const Key& o) const { return std::memcmp(this, &o, sizeof(Key)) == 0; }
+    };
+    static std::mutex mu;
+    static std::vector<std::pair<Key, std::shared_ptr<skg::CztPlanG>>> lru;   // front = most recent
+    thread_local std::shared_ptr<skg::CztPlanG> hold;   // keeps the returned plan alive for this call
+    Key k{};
+    k.n = n, k.m = m, k.ar = a.real(), k.ai = a.imag(), k.wr = w.real(), k.wi = w.imag();
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (size_t i = 0; i < lru.size(); ++i)
+            if (lru[i].first == k) {
+                std::rotate(lru.begin(), lru.begin() + i, lru.begin() + i + 1);
+                hold = lru.front().second;
+                return *hold;
+            }
+    }
+    auto plan = std::make_shared<skg::CztPlanG>(n, a, w, m);   // validates; may throw
+    std::lock_guard<std::mutex> lk(mu);
+    lru.insert(lru.begin(), {k, plan});
+    if (lru.size() > 8) lru.pop_back();
+    hold = plan;
+    return *hold;
+}
+
 std::vector<cd> czt_gpu(const std::vector<cd>& x, cd a, cd w, size_t m) {   // czt.cpp:139-142
     if (x.empty()) throw std::invalid_argument("czt: empty input");
-    skg::CztPlanG plan(x.size(), a, w, m);
+    const skg::CztPlanG& plan = czt_plan_cached(x.size(), a, w, m);
     Stage s;
     s.put(x.data(), x.size() * sizeof(cd));
     s.alloc_out(m * sizeof(cd));
@@ -302,7 +379,7 @@ sk_status sk_czt_spectrum(const sk_trace* t, double f1, double f2, size_t m, sk_
         if (sk_czt_params_for_band(f1, f2, t->fs, m, &ar, &ai, &wr, &wi) != SK_OK)
             throw std::invalid_argument(g_err);
         const size_t n = t->samples.size();
-        skg::CztPlanG plan(n, cd(ar, ai), cd(wr, wi), m);
+        const skg::CztPlanG& plan = czt_plan_cached(n, cd(ar, ai), cd(wr, wi), m);
         Stage s;
         s.put(t->samples.data(), n * sizeof(double));
         s.alloc_out(m * sizeof(cd));

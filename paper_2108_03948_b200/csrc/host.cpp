@@ -6,6 +6,7 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <mutex>
 #include <numbers>
 
 #include "fft_device.cuh"
@@ -29,6 +30,26 @@ void require_device() {
                         (e == cudaSuccess ? "0 devices" : cudaGetErrorString(e)) +
                         "); the B200 spectral library has no CPU fallback");
     }
+}
+
+// Stream-ordered work buffers come from the device's default memory pool. Its release threshold is
+// raised once per device so freed blocks stay cached in the pool: without it every synchronisation
+// returns the memory to the driver and the next cudaMallocAsync re-maps it (hundreds of us).
+void* stream_alloc(size_t bytes, cudaStream_t st) {
+    static std::once_flag once[64];
+    int dev = 0;
+    check(cudaGetDevice(&dev), "cudaGetDevice");
+    std::call_once(once[dev & 63], [dev] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = 8ull << 30;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+    });
+    void* p = nullptr;
+    check(cudaMallocAsync(&p, bytes, st), "cudaMallocAsync");
+    return p;
 }
 
 int current_device() {
@@ -252,7 +273,7 @@ struct FourStep {
 struct Scratch {   // stream-ordered work buffer
     void* p = nullptr;
     cudaStream_t st;
-    Scratch(size_t bytes, cudaStream_t s) : st(s) { check(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync"); }
+    Scratch(size_t bytes, cudaStream_t s) : st(s) { p = stream_alloc(bytes, s); }
     ~Scratch() {
         if (p) cudaFreeAsync(p, st);
     }

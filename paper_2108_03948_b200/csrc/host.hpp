@@ -28,6 +28,8 @@ struct CudaError : std::runtime_error {
 void check(cudaError_t e, const char* what);
 void require_device();          // throws CudaError when no usable CUDA device exists
 int current_device();
+// stream-ordered work buffer from the default pool (kept cached across synchronisations); free with cudaFreeAsync
+void* stream_alloc(size_t bytes, cudaStream_t st);
 std::atomic<uint64_t>& launch_counter();
 inline void count_launch(int n = 1) { launch_counter().fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
@@ -165,7 +167,7 @@ class ZoomPlanG {                     // ZoomFftPlan + make_zoom_plan, zoomfft.h
   private:
     ZoomPlanG() = default;
     struct Dev {
-        DevMem g, sdec, wrap, band;
+        DevMem g, gn, sdec, wrap, band;
     };
     const Dev& dev(bool f32) const;
     void compute_band();

@@ -83,6 +83,19 @@ cudaError_t launch_zoom_fir(const ZoomArgs& a, bool f32, const void* x, long lon
 cudaError_t launch_zoom_band(bool f32, const void* Z, long long z_stride, long long n_fft, int k_lo, int nbins,
                              const void* band, void* out, long long out_stride, long long batch, cudaStream_t st);
 int zoom_chunk_rowlen(const ZoomArgs& a);
+// split zoom: warp-chunk FIR into work rows (z_stride >= nout), then FFT + band gather per row
+bool zoom_wfir_fits(const ZoomArgs& a, bool f32, const void* x, long long x_stride);
+cudaError_t launch_zoom_wfir(const ZoomArgs& a, bool f32, const void* x, long long xs, long long batch, const void* g,
+                             const void* S, void* zb, long long z_stride, cudaStream_t st);
+cudaError_t launch_zoom_fftband(int log2n, bool f32, const void* zb, long long z_stride, int nout, long long batch,
+                                int k_lo, int nbins, const void* tw, const void* band, void* out, long long out_stride,
+                                cudaStream_t st);
+// phase-lane FIR (power-of-two D <= 16, short phase rows): zoom_pfir_lh(a) > 0 when available;
+// gnat = the taps in natural order g[t] (wrap terms)
+int zoom_pfir_lh(const ZoomArgs& a);
+cudaError_t launch_zoom_pfir(const ZoomArgs& a, bool f32, const void* x, long long xs, long long batch,
+                             const void* gph, const void* gnat, const void* S, void* zb, long long z_stride,
+                             cudaStream_t st);
 // shared bytes the fused zoom kernel needs for this geometry
 size_t zoom_smem_bytes(const ZoomArgs& a, int log2n, bool f32);
 

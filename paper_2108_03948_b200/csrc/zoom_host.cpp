@@ -5,6 +5,9 @@
 
 #include "host.hpp"
 
+#include <cstdlib>
+#include <string>
+
 namespace skg {
 
 ZoomPlanG::ZoomPlanG(size_t in_len, double f1, double f2, double fs, const ZoomOptionsG& opts,
@@ -161,6 +164,9 @@ const ZoomPlanG::Dev& ZoomPlanG::dev(bool f32) const {
             }
         }
         d.g = to_device(g, f32);
+        std::vector<cd> gn(static_cast<size_t>(std::max(T, 1)), cd(0.0, 0.0));   // natural order (wrap terms)
+        for (int t = 0; t < T; ++t) gn[static_cast<size_t>(t)] = filter_taps[t] * cis_cycles(-qc, static_cast<double>(t));
+        d.gn = to_device(gn, f32);
         // S[m] = e^{i 2pi qc (m + trim) D} (the shift table sampled at the decimation points)
         std::vector<cd> S(decimated_len);
         for (size_t m = 0; m < decimated_len; ++m)
@@ -187,7 +193,37 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
     int dev_id = current_device();
     int smem_max = 0;
     check(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev_id), "attr");
-    const bool fused = is_pow2(n_fft) && lg <= single_cta_max_log2(f32) &&
+    // SKG_ZOOM_PATH=fused|unfused forces a route (A/B measurements); the default is the split route
+    static const char* force = getenv("SKG_ZOOM_PATH");
+    const bool single = is_pow2(n_fft) && lg <= single_cta_max_log2(f32);
+    const bool wfir = zoom_wfir_fits(a, f32, x, x_stride);
+    static const bool no_pfir = getenv("SKG_ZOOM_NO_PFIR") != nullptr;
+    const bool pfir = !no_pfir && zoom_pfir_lh(a) > 0;
+    if (single && (wfir || pfir) && !force) {
+        // warp-chunk FIR -> work rows (L2-resident chunk of records) -> FFT + band gather
+        const size_t cs = f32 ? 8 : 16, es = f32 ? 4 : 8;
+        const long long zrow = a.nout;
+        const long long chunk = std::max<long long>(1, (48ll << 20) / (zrow * (long long)cs));
+        const long long nb0 = std::min(chunk, batch);
+        void* zb = nullptr;
+        zb = stream_alloc((size_t)nb0 * zrow * cs, st);
+        const void* tw = stockham_twiddles(lg, f32);
+        for (long long b0 = 0; b0 < batch; b0 += chunk) {
+            const long long nb = std::min(chunk, batch - b0);
+            const void* xb = static_cast<const char*>(x) + b0 * x_stride * (long long)es;
+            if (pfir)
+                check(launch_zoom_pfir(a, f32, xb, x_stride, nb, d.g.p, d.gn.p, d.sdec.p, zb, zrow, st), "zoom fir");
+            else
+                check(launch_zoom_wfir(a, f32, xb, x_stride, nb, d.g.p, d.sdec.p, zb, zrow, st), "zoom fir");
+            check(launch_zoom_fftband(lg, f32, zb, zrow, a.nout, nb, (int)k_lo, (int)bins(), tw, d.band.p,
+                                      static_cast<char*>(out) + b0 * out_stride * (long long)cs, out_stride, st),
+                  "zoom fft+band");
+            count_launch(2);
+        }
+        check(cudaFreeAsync(zb, st), "free");
+        return;
+    }
+    const bool fused = !(force && std::string(force) == "unfused") && single &&
                        zoom_smem_bytes(a, lg, f32) <= static_cast<size_t>(smem_max);
     if (!fused) {
         // FIR/decimate by output chunks -> work buffer (zero padded to n_fft) -> FFT -> band gather
@@ -198,15 +234,18 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
         c.rs = rs;
         const size_t cs = f32 ? 8 : 16;
         void* zb = nullptr;
-        check(cudaMallocAsync(&zb, (size_t)batch * n_fft * cs, st), "cudaMallocAsync");
+        zb = stream_alloc((size_t)batch * n_fft * cs, st);
         check(cudaMemsetAsync(zb, 0, (size_t)batch * n_fft * cs, st), "memset");
-        check(launch_zoom_fir(c, f32, x, x_stride, batch, d.g.p, d.sdec.p, zb, (long long)n_fft, st), "zoom fir");
+        if (wfir)
+            check(launch_zoom_wfir(a, f32, x, x_stride, batch, d.g.p, d.sdec.p, zb, (long long)n_fft, st), "zoom fir");
+        else
+            check(launch_zoom_fir(c, f32, x, x_stride, batch, d.g.p, d.sdec.p, zb, (long long)n_fft, st), "zoom fir");
         count_launch();
         if (is_pow2(n_fft)) {
             fft_c2c(n_fft, false, f32, zb, (long long)n_fft, zb, (long long)n_fft, batch, st);
         } else {   // dft_any's chirp route (zoomfft.cpp:204-207)
             void* zf = nullptr;
-            check(cudaMallocAsync(&zf, (size_t)batch * n_fft * cs, st), "cudaMallocAsync");
+            zf = stream_alloc((size_t)batch * n_fft * cs, st);
             bluestein_->execute(zb, true, (long long)n_fft, batch, zf, (long long)n_fft, f32, st);
             check(cudaFreeAsync(zb, st), "free");
             zb = zf;

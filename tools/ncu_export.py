@@ -1,5 +1,5 @@
 """Export per-kernel ncu metrics (one --set full capture) to a JSON summary under profiles/.
-usage: python tools/ncu_export.py REPORT OUT.json"""
+usage: python tools/ncu_export.py OUT.json REPORT_OR_RAW_CSV [...]"""
 import csv
 import json
 import subprocess
@@ -26,8 +26,22 @@ UNIT = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "ms": 1.0, "us": 
         "Mhz": 1e6, "hz": 1.0}
 
 
-def main(rep, out):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+def main(out, *reps):
+    """reps: .ncu-rep files or their `--page raw --csv` exports; all launches go into one summary."""
+    res = []
+    for rep in reps:
+        res += launches(rep)
+    with open(out, "w") as f:
+        json.dump({"reports": list(reps), "launches": res}, f, indent=1)
+    for d in res:
+        print(f"{d['kernel']:40s} {d.get('time_ms', 0):8.4f} ms  dram {d.get('dram_bytes', 0) / 1e6:9.1f} MB")
+
+
+def launches(rep):
+    if rep.endswith(".csv"):
+        txt = open(rep).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(txt.splitlines()))
     hdr, units = rows[0], rows[1]
     res = []
@@ -45,10 +59,7 @@ def main(rep, out):
         if "dram_read_bytes" in d and "dram_write_bytes" in d:
             d["dram_bytes"] = d["dram_read_bytes"] + d["dram_write_bytes"]
         res.append(d)
-    with open(out, "w") as f:
-        json.dump({"report": rep, "launches": res}, f, indent=1)
-    for d in res:
-        print(f"{d['kernel']:40s} {d.get('time_ms', 0):8.4f} ms  dram {d.get('dram_bytes', 0) / 1e6:9.1f} MB")
+    return res
 
 
 if __name__ == "__main__":

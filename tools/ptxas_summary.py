@@ -1,16 +1,22 @@
 """Summarise `nvcc -Xptxas -v` output: kernel, registers, spills (reads stdin)."""
 import re, subprocess, sys
 cur = None
+mangled = None
 rows = {}
 for line in sys.stdin:
     m = re.search(r"Compiling entry function '(\S+)'", line)
     if m:
-        cur = m.group(1)
+        cur = mangled = m.group(1)
         try:
             cur = subprocess.run(["c++filt"], input=cur, capture_output=True, text=True).stdout.strip()
         except Exception:
             pass
         rows[cur] = {}
+        continue
+    m = re.search(r"Function properties for (\S+)", line)
+    if m:   # non-entry functions have their own property blocks: do not charge them to the kernel
+        prop = m.group(1)
+        cur = cur if cur is not None and mangled == prop else None
         continue
     m = re.search(r"(\d+) bytes spill stores, (\d+) bytes spill loads", line)
     if m and cur:
