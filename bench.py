@@ -405,6 +405,7 @@ def bench_extras(args, sk, W, dev, world, pk):
     tp1 = sk.TransferPlanGPU(r1, 4096, sk.SKG_F64)
     sd = torch.from_numpy(s1[None]).to(dev)
     t, per = time_device(lambda: tp1.execute(sd), 20, 5, world)
+    sk.fft_spectrum(s1, W.FS, 4096)   # first call: per-thread staging buffers, tables
     t0 = time.perf_counter()
     for _ in range(20):
         sk.fft_spectrum(s1, W.FS, 4096)

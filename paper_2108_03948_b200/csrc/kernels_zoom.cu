@@ -856,8 +856,11 @@ cudaError_t launch_zoom_fftband(int log2n, bool f32, const void* zb, long long z
 // halving the outputs a lane carries), which leaves every lane with MB / D finished outputs.
 namespace skg {
 
+#ifndef SKG_PFIR_MINB64
+#define SKG_PFIR_MINB64 3
+#endif
 template <typename T, int D, int LH>
-__global__ void __launch_bounds__(128, sizeof(T) == 8 ? 3 : 4)
+__global__ void __launch_bounds__(128, sizeof(T) == 8 ? SKG_PFIR_MINB64 : 4)
 k_zoom_pfir(const T* __restrict__ x, long long x_stride, long long batch, ZoomArgs a, int gchunk, int tasks_per_rec,
             const cx_t<T>* __restrict__ gph, const cx_t<T>* __restrict__ gnat, const cx_t<T>* __restrict__ S,
             cx_t<T>* __restrict__ zb, long long z_stride) {
@@ -946,17 +949,22 @@ k_zoom_pfir(const T* __restrict__ x, long long x_stride, long long batch, ZoomAr
 #pragma unroll
                 for (int j = 0; j < MB; ++j) nx2[j] = sample(mf + 2 * MB - delta + j);
             }
-            // tap-outer order: 2 MB independent FMA chains between dependent issues
+            // even and odd taps accumulate separately: four FMA chains per output, so the
+            // compiler's two-outputs-at-a-time schedule still has eight chains in flight
             C P[MB];
 #pragma unroll
-            for (int j = 0; j < MB; ++j) P[j] = czero<C>();
+            for (int j = 0; j < MB; ++j) {
+                C e = czero<C>(), o = czero<C>();
 #pragma unroll
-            for (int l = 0; l < LH; ++l) {
-#pragma unroll
-                for (int j = 0; j < MB; ++j) {
-                    P[j].x = fma(tp[l].x, buf[LH - 1 + j - l], P[j].x);
-                    P[j].y = fma(tp[l].y, buf[LH - 1 + j - l], P[j].y);
+                for (int l = 0; l < LH; l += 2) {
+                    e.x = fma(tp[l].x, buf[LH - 1 + j - l], e.x);
+                    e.y = fma(tp[l].y, buf[LH - 1 + j - l], e.y);
+                    if (l + 1 < LH) {
+                        o.x = fma(tp[l + 1].x, buf[LH - 2 + j - l], o.x);
+                        o.y = fma(tp[l + 1].y, buf[LH - 2 + j - l], o.y);
+                    }
                 }
+                P[j] = cadd(e, o);
             }
             // sum over the D phase-lanes of the group through shared memory: lane (g, ph) posts its
             // MB partials, then finishes outputs ph K + j (j < K) from the D phase partials

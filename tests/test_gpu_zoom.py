@@ -157,3 +157,49 @@ def test_unfused_linear_trim_long():
     got = sk.ZoomPlanGPU(40000, 0.4e12, 1.2e12, W.FS, **kw).execute(_dev(x, "f64")).cpu().numpy()
     ref = O.ZoomPlan(40000, 0.4e12, 1.2e12, W.FS, **kw)
     assert rel_max_rows(got, [ref(r)[0] for r in x]) <= TOL_F64
+
+
+_ROUTE_SNIPPET = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import paper_2108_03948_b200 as sk
+from paper_2108_03948_b200 import workloads as W
+x = W.cfg3_batch(6, 4096)
+outs = []
+for prec in ("f64", "f32"):
+    for kw in ({{"decimation": 8, "num_taps": 65}}, {{"decimation": 4, "circular": 0, "trim_transient": 1}},
+               {{"decimation": 5}}, {{"decimation": 16}}):
+        p = sk.ZoomPlanGPU(4096, 0.4e12, 1.2e12, W.FS, sk.SKG_F64 if prec == "f64" else sk.SKG_F32, **kw)
+        xd = torch.from_numpy(x).to(torch.float64 if prec == "f64" else torch.float32).cuda()
+        outs.append(p.execute(xd).cpu().numpy().astype(np.complex128))
+np.savez({out!r}, *outs)
+"""
+
+
+@pytest.mark.parametrize("env", [{}, {"SKG_ZOOM_NO_PFIR": "1"}, {"SKG_ZOOM_PATH": "fused"},
+                                 {"SKG_ZOOM_PATH": "unfused"}], ids=["split-pfir", "split-wfir", "fused", "unfused"])
+def test_zoom_routes_match_oracle(env, tmp_path):
+    """Every zoom route (phase-lane FIR, warp-window FIR, fused single kernel, unfused FIR + FFT +
+    gather) on linear/circular, power-of-two and odd decimations, against the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = str(tmp_path / "routes.npz")
+    e = dict(os.environ)
+    e.update(env)
+    subprocess.run([sys.executable, "-c", _ROUTE_SNIPPET.format(root=root, out=out)], check=True, env=e, timeout=600)
+    got = np.load(out)
+    x = W.cfg3_batch(6, 4096)
+    i = 0
+    for prec in ("f64", "f32"):
+        for kw in ({"decimation": 8, "num_taps": 65}, {"decimation": 4, "circular": 0, "trim_transient": 1},
+                   {"decimation": 5}, {"decimation": 16}):
+            ref = O.ZoomPlan(4096, 0.4e12, 1.2e12, W.FS, **kw)
+            want = np.array([ref(r)[0] for r in x])
+            g = got[f"arr_{i}"]
+            i += 1
+            if prec == "f64":
+                assert rel_max_rows(g, want) <= TOL_F64, (env, kw)
+            else:
+                assert rel_l2_rows(g, want) <= TOL_F32, (env, kw)
