@@ -1,0 +1,97 @@
+"""GPU memory-safety checks (compute-sanitizer cannot attach on the GPU pool): every batched entry
+point runs on strided input rows whose gaps hold poison values and writes into strided output
+rows whose gaps hold a canary. The result must equal the contiguous run bit for bit (any read of a
+gap would change it) and every canary must survive (any stray write would overwrite one)."""
+import numpy as np
+import pytest
+
+import paper_2108_03948_b200 as sk
+from paper_2108_03948_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+CANARY = 7.25 - 3.5j
+POISON = 1e30
+
+
+def _strided_in(x, pad=5):
+    """rows of x inside a wider buffer whose gaps are poison"""
+    b, n = x.shape
+    buf = torch.full((b, n + pad), POISON, dtype=x.dtype, device=x.device)
+    buf[:, 2:2 + n] = x
+    return buf[:, 2:2 + n]
+
+
+def _strided_out(b, n, dtype, pad=7, off=3):
+    buf = torch.full((b, n + pad), CANARY if dtype.is_complex else CANARY.real, dtype=dtype, device="cuda")
+    return buf, buf[:, off:off + n], off, n
+
+
+def _canaries_ok(buf, off, n):
+    host = buf.cpu().numpy()
+    want = CANARY if np.iscomplexobj(host) else CANARY.real
+    mask = np.ones(host.shape, bool)
+    mask[:, off:off + n] = False
+    return bool(np.all(host[mask] == want))
+
+
+def _same(a, b):
+    return np.array_equal(a.cpu().numpy(), b.cpu().numpy())
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("n,L,layout", [(1000, 4096, sk.SKG_FULL), (1024, 4096, sk.SKG_HALF), (3000, 16384, sk.SKG_FULL),
+                                        (20000, 65536, sk.SKG_HALF), (700, 1000, sk.SKG_FULL)])
+def test_fft_spectrum_guards(prec, n, L, layout):
+    x = torch.from_numpy(W.sample_traces(37, n)).cuda()
+    x = x if prec == "f64" else x.float()
+    ref = sk.fft_spectrum_batch(x, L, layout)
+    buf, out, off, nb = _strided_out(37, ref.shape[1], ref.dtype)
+    sk.fft_spectrum_batch(_strided_in(x), L, layout, out=out)
+    torch.cuda.synchronize()
+    assert _same(out, ref) and _canaries_ok(buf, off, nb)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("n,m", [(1024, 2048), (1000, 1000), (1024, 333), (4096, 4096), (16384, 16384), (77, 5)])
+def test_czt_guards(prec, n, m):
+    x = torch.from_numpy(W.sample_traces(29, n)).cuda()
+    x = x if prec == "f64" else x.float()
+    a, w = W.cfg2_czt_params(m)
+    p = sk.CztPlanGPU(n, a, w, m, sk.SKG_F64 if prec == "f64" else sk.SKG_F32)
+    ref = p.execute(x)
+    buf, out, off, nb = _strided_out(29, m, ref.dtype)
+    p.execute(_strided_in(x), out=out)
+    torch.cuda.synchronize()
+    assert _same(out, ref) and _canaries_ok(buf, off, nb)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("kw", [{"decimation": 8, "num_taps": 65}, {"decimation": 5}, {"decimation": 4, "circular": 0,
+                                                                                         "trim_transient": 1}])
+def test_zoom_guards(prec, kw):
+    x = torch.from_numpy(W.cfg3_batch(23, 4096)).cuda()
+    x = x if prec == "f64" else x.float()
+    p = sk.ZoomPlanGPU(4096, 0.4e12, 1.2e12, W.FS, sk.SKG_F64 if prec == "f64" else sk.SKG_F32, **kw)
+    ref = p.execute(x)
+    buf, out, off, nb = _strided_out(23, p.bins, ref.dtype)
+    p.execute(_strided_in(x, pad=6), out=out)
+    torch.cuda.synchronize()
+    assert _same(out, ref) and _canaries_ok(buf, off, nb)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_transfer_guards(prec):
+    ref_t, smp = W.cfg1_pair()
+    x = torch.from_numpy(np.stack([smp] * 19)).cuda()
+    x = x if prec == "f64" else x.float()
+    tp = sk.TransferPlanGPU(ref_t, 4096, sk.SKG_F64 if prec == "f64" else sk.SKG_F32)
+    m0, p0 = tp.execute(x)
+    rdt = m0.dtype
+    bm, mag, off, nb = _strided_out(19, tp.bins, rdt)
+    bp, ph, _, _ = _strided_out(19, tp.bins, rdt)
+    tp.execute(_strided_in(x), mag=mag, phase=ph)
+    torch.cuda.synchronize()
+    assert _same(mag, m0) and _same(ph, p0)
+    assert _canaries_ok(bm, off, nb) and _canaries_ok(bp, off, nb)
