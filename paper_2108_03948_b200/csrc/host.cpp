@@ -261,11 +261,14 @@ struct FourStep {
         twC = stockham_twiddles(lC, f32);
         twL = fourstep_twiddles(lR, lC, f32);
     }
-    // traces per chunk so the work buffer stays L2 resident (~48 MB)
+    // traces per launch pair. Chunking to keep the work buffer L2 resident was measured SLOWER at every
+    // size (configs[4] rows, 4 MB .. 4 GB chunks: the pass kernels are latency bound and a bigger grid
+    // amortises their ramp/tail better than L2 residency saves), so the chunk only caps the work
+    // buffer at 2 GB.
     long long chunk(bool f32) const {
         const long long bytes = L * (f32 ? 8 : 16);
         const char* e = std::getenv("SKG_4STEP_CHUNK_MB");
-        const long long mb = e ? std::atoll(e) : 32;
+        const long long mb = e ? std::atoll(e) : 2048;
         return std::max<long long>(1, (mb << 20) / bytes);
     }
 };
