@@ -10,7 +10,7 @@
 //   mode 1: the whole Bluestein middle in shared memory: FFT_C, x khat (stored permuted as
 //           khat_p[k1][k2]), IFFT_C, x conj twiddle, back into Y — one read and one write of Y;
 // then an inverse column pass (input Y) finishes the CZT with the output chirp on the store.
-// The batch is processed in chunks small enough that Y stays resident in the 126 MB L2.
+// Both passes are persistent (grid = resident CTAs) and pull the next tile into L2 while transforming.
 #pragma once
 
 #include "kernels_impl.cuh"
@@ -46,42 +46,63 @@ k4_col(const void* __restrict__ xin, int in_kind, int conj_in, long long x_strid
     __syncthreads();
     const long long Cn = 1LL << log2C;
     const long long tiles = Cn / TC;
-    const long long b = blockIdx.x / tiles;
-    const long long n2 = (blockIdx.x % tiles) * TC + g;
     const long long L = Cn << LOG2R;
-    C v[G::EPT];
+    const long long units = tiles * batch;
+    // persistent: the CTA walks tiles with stride gridDim.x; the next tile's column segments are
+    // pulled into L2 while this one is transformed (the pass is latency bound, not bandwidth bound)
+    auto prefetch = [&](long long u) {
+        if (u >= units || g != 0) return;   // one lane per 8/16-column segment
+        const long long bb = u / tiles, nn2 = (u % tiles) * TC;
 #pragma unroll
-    for (int q = 0; q < G::EPT; ++q) {
-        const long long n1 = tid + (long long)G::NT * q;
-        const long long n = n1 * Cn + n2;
-        C val = czero<C>();
-        if (in_kind == IN_WORK) {
-            val = Y[b * L + n];   // Y[k1][n2] with k1 = n1
-        } else if (n < N) {
-            if (in_kind == IN_REAL || in_kind == IN_REAL_CHIRP)
-                val = mk<C>(__ldg(reinterpret_cast<const T*>(xin) + b * x_stride + n), (T)0);
-            else
-                val = __ldg(reinterpret_cast<const C*>(xin) + b * x_stride + n);
-            if (conj_in) val = cconj(val);
-            if (in_kind == IN_REAL_CHIRP || in_kind == IN_CPLX_CHIRP) val = cmul(val, __ldg(cin + n));
+        for (int q = 0; q < G::EPT; ++q) {
+            const long long n = (tid + (long long)G::NT * q) * Cn + nn2;
+            if (in_kind == IN_WORK) prefetch_l2(Y + bb * L + n);
+            else if (n < N) {
+                if (in_kind == IN_REAL || in_kind == IN_REAL_CHIRP)
+                    prefetch_l2(reinterpret_cast<const T*>(xin) + bb * x_stride + n);
+                else
+                    prefetch_l2(reinterpret_cast<const C*>(xin) + bb * x_stride + n);
+            }
         }
-        v[q] = val;
-    }
-    block_fft<INV, LOG2R>(v, sm, tws, tid);
+    };
+    for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+        const long long b = u / tiles;
+        const long long n2 = (u % tiles) * TC + g;
+        prefetch(u + gridDim.x);
+        C v[G::EPT];
 #pragma unroll
-    for (int q = 0; q < G::EPT; ++q) {
-        const long long k1 = tid + (long long)G::NT * q;
-        if (out_kind == OUT_WORK_TW) {
-            // Y[k1][n2] = v * W_L^{n2 k1} (forward twiddle of the four-step split)
-            Y[b * L + k1 * Cn + n2] = cmul(v[q], __ldg(twL + k1 * Cn + n2));
-        } else {
-            const long long n = k1 * Cn + n2;   // output sample index C n1 + n2
-            if (out_kind == OUT_CHIRP) {
-                if (n < M) reinterpret_cast<C*>(out)[b * out_stride + n] = cmul(v[q], __ldg(cout + n));
+        for (int q = 0; q < G::EPT; ++q) {
+            const long long n1 = tid + (long long)G::NT * q;
+            const long long n = n1 * Cn + n2;
+            C val = czero<C>();
+            if (in_kind == IN_WORK) {
+                val = Y[b * L + n];   // Y[k1][n2] with k1 = n1
+            } else if (n < N) {
+                if (in_kind == IN_REAL || in_kind == IN_REAL_CHIRP)
+                    val = mk<C>(__ldg(reinterpret_cast<const T*>(xin) + b * x_stride + n), (T)0);
+                else
+                    val = __ldg(reinterpret_cast<const C*>(xin) + b * x_stride + n);
+                if (conj_in) val = cconj(val);
+                if (in_kind == IN_REAL_CHIRP || in_kind == IN_CPLX_CHIRP) val = cmul(val, __ldg(cin + n));
+            }
+            v[q] = val;
+        }
+        block_fft<INV, LOG2R>(v, sm, tws, tid);
+#pragma unroll
+        for (int q = 0; q < G::EPT; ++q) {
+            const long long k1 = tid + (long long)G::NT * q;
+            if (out_kind == OUT_WORK_TW) {
+                // Y[k1][n2] = v * W_L^{n2 k1} (forward twiddle of the four-step split)
+                Y[b * L + k1 * Cn + n2] = cmul(v[q], __ldg(twL + k1 * Cn + n2));
             } else {
-                C r = cscale(v[q], scale);
-                if (conj_out) r = cconj(r);
-                reinterpret_cast<C*>(out)[b * out_stride + n] = r;
+                const long long n = k1 * Cn + n2;   // output sample index C n1 + n2
+                if (out_kind == OUT_CHIRP) {
+                    if (n < M) reinterpret_cast<C*>(out)[b * out_stride + n] = cmul(v[q], __ldg(cout + n));
+                } else {
+                    C r = cscale(v[q], scale);
+                    if (conj_out) r = cconj(r);
+                    reinterpret_cast<C*>(out)[b * out_stride + n] = r;
+                }
             }
         }
     }
@@ -115,32 +136,43 @@ k4_row(cx_t<T>* __restrict__ Y, int log2R, long long batch, const cx_t<T>* __res
     load_twiddles<LOG2C>(tws, tw);
     __syncthreads();
     const long long tiles = R / rows_per_cta;
-    const long long b = blockIdx.x / tiles;
-    const long long k1 = (blockIdx.x % tiles) * rows_per_cta + g;
-    C* row = Y + b * L + k1 * Cn;
-    C v[G::EPT];
-#pragma unroll
-    for (int q = 0; q < G::EPT; ++q) v[q] = row[tid + G::NT * q];
-    block_fft<false, LOG2C>(v, sm, tws, tid);
-    if constexpr (MODE == 0) {
-        C* o = out + b * out_stride;
-#pragma unroll
-        for (int q = 0; q < G::EPT; ++q) {
-            const long long k2 = tid + (long long)G::NT * q;
-            C r = cscale(v[q], scale);
-            if (conj_out) r = cconj(r);
-            o[k1 + R * k2] = r;
+    const long long units = tiles * batch;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+        const long long b = u / tiles;
+        const long long k1 = (u % tiles) * rows_per_cta + g;
+        C* row = Y + b * L + k1 * Cn;
+        {   // the next unit's rows into L2 (one 128-byte line per lane and step)
+            const long long un = u + gridDim.x;
+            if (un < units) {
+                const C* rn = Y + (un / tiles) * L + ((un % tiles) * rows_per_cta + g) * Cn;
+                constexpr int per_line = 128 / (int)sizeof(C);
+                for (int i = tid * per_line; i < G::L; i += G::NT * per_line) prefetch_l2(rn + i);
+            }
         }
-    } else {
-        const C* kp = khat_p + k1 * Cn;
+        C v[G::EPT];
 #pragma unroll
-        for (int q = 0; q < G::EPT; ++q) v[q] = cmul(v[q], __ldg(kp + tid + G::NT * q));
-        block_fft<true, LOG2C>(v, sm, tws, tid);
-        const C* t = twL + k1 * Cn;
+        for (int q = 0; q < G::EPT; ++q) v[q] = row[tid + G::NT * q];
+        block_fft<false, LOG2C>(v, sm, tws, tid);
+        if constexpr (MODE == 0) {
+            C* o = out + b * out_stride;
 #pragma unroll
-        for (int q = 0; q < G::EPT; ++q) {
-            const int n2 = tid + G::NT * q;
-            row[n2] = cmulc(v[q], __ldg(t + n2));   // x conj(W_L^{n2 k1})
+            for (int q = 0; q < G::EPT; ++q) {
+                const long long k2 = tid + (long long)G::NT * q;
+                C r = cscale(v[q], scale);
+                if (conj_out) r = cconj(r);
+                o[k1 + R * k2] = r;
+            }
+        } else {
+            const C* kp = khat_p + k1 * Cn;
+#pragma unroll
+            for (int q = 0; q < G::EPT; ++q) v[q] = cmul(v[q], __ldg(kp + tid + G::NT * q));
+            block_fft<true, LOG2C>(v, sm, tws, tid);
+            const C* t = twL + k1 * Cn;
+#pragma unroll
+            for (int q = 0; q < G::EPT; ++q) {
+                const int n2 = tid + G::NT * q;
+                row[n2] = cmulc(v[q], __ldg(t + n2));   // x conj(W_L^{n2 k1})
+            }
         }
     }
 }
@@ -148,6 +180,13 @@ k4_row(cx_t<T>* __restrict__ Y, int log2R, long long batch, const cx_t<T>* __res
 }  // namespace skg
 
 namespace skg {
+
+// SKG_4STEP_PERSIST=0: one CTA per tile (A/B against the persistent grid)
+template <typename K> inline unsigned grid_4step(K kern, int block, size_t smem, long long units) {
+    static const char* e = std::getenv("SKG_4STEP_PERSIST");
+    if (e && e[0] == '0') return (unsigned)units;
+    return persistent_grid(kern, block, smem, units);
+}
 
 template <typename T>
 cudaError_t launch_4step_col_impl(int log2R, bool inverse, int in_kind, int conj_in, const void* x, long long x_stride,
@@ -164,7 +203,7 @@ cudaError_t launch_4step_col_impl(int log2R, bool inverse, int in_kind, int conj
         auto launch = [&](auto kern) {
             cudaError_t e = prep_smem(kern, smem);
             if (e != cudaSuccess) return e;
-            kern<<<(unsigned)(tiles * batch), G::NT * TC, smem, st>>>(
+            kern<<<grid_4step(kern, G::NT * TC, smem, tiles * batch), G::NT * TC, smem, st>>>(
                 x, in_kind, conj_in, x_stride, N, (const C*)cin, (C*)Y, log2C, batch, (const C*)tw, (const C*)twL,
                 out_kind, out, out_stride, M, (const C*)cout, scale, conj_out);
             return cudaGetLastError();
@@ -188,7 +227,7 @@ cudaError_t launch_4step_row_impl(int log2C, int mode, void* Y, int log2R, long 
             auto kern = k4_row<T, LG, 0>;
             cudaError_t e = prep_smem(kern, smem);
             if (e != cudaSuccess) return e;
-            kern<<<(unsigned)(R / TR * batch), G::NT * TR, smem, st>>>((C*)Y, log2R, batch, (const C*)tw,
+            kern<<<grid_4step(kern, G::NT * TR, smem, R / TR * batch), G::NT * TR, smem, st>>>((C*)Y, log2R, batch, (const C*)tw,
                                                                        (const C*)twL, (const C*)khat_p, (C*)out,
                                                                        out_stride, scale, conj_out);
         } else {
@@ -197,7 +236,7 @@ cudaError_t launch_4step_row_impl(int log2C, int mode, void* Y, int log2R, long 
             auto kern = k4_row<T, LG, 1>;
             cudaError_t e = prep_smem(kern, smem);
             if (e != cudaSuccess) return e;
-            kern<<<(unsigned)(R / K::GROUPS * batch), K::BLOCK, smem, st>>>((C*)Y, log2R, batch, (const C*)tw,
+            kern<<<grid_4step(kern, K::BLOCK, smem, R / K::GROUPS * batch), K::BLOCK, smem, st>>>((C*)Y, log2R, batch, (const C*)tw,
                                                                            (const C*)twL, (const C*)khat_p, (C*)out,
                                                                            out_stride, scale, conj_out);
         }
