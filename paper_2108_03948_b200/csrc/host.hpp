@@ -168,6 +168,7 @@ class ZoomPlanG {                     // ZoomFftPlan + make_zoom_plan, zoomfft.h
     ZoomPlanG() = default;
     struct Dev {
         DevMem g, gn, sdec, wrap, band;
+        std::vector<cd> gh;   // host copy of g (phase rows, fp64) for the constant-bank FIR
     };
     const Dev& dev(bool f32) const;
     void compute_band();

@@ -96,6 +96,12 @@ int zoom_pfir_lh(const ZoomArgs& a);
 cudaError_t launch_zoom_pfir(const ZoomArgs& a, bool f32, const void* x, long long xs, long long batch,
                              const void* gph, const void* gnat, const void* S, void* zb, long long z_stride,
                              cudaStream_t st);
+// constant-bank FIR specialised on (D, T) (kernels_zoom_cfir.cu); gph_host = the plan's phase-row
+// taps as interleaved fp64 complex (D x lh)
+bool zoom_cfir_available(const ZoomArgs& a);
+cudaError_t launch_zoom_cfir(const ZoomArgs& a, bool f32, const void* x, long long xs, long long batch,
+                             const void* gph_host, const void* gnat, const void* S, void* zb, long long z_stride,
+                             cudaStream_t st);
 // shared bytes the fused zoom kernel needs for this geometry
 size_t zoom_smem_bytes(const ZoomArgs& a, int log2n, bool f32);
 

@@ -28,7 +28,7 @@ enum : int { OUT_WORK_TW = 0, OUT_CHIRP = 1, OUT_SCALE = 2 };
 template <typename T, int LOG2R, bool INV>
 __global__ void __launch_bounds__(FftGeom<LOG2R>::NT * Tile<T>::W,
                                   (FftGeom<LOG2R>::NT * Tile<T>::W) >= 512 ? 1
-                                  : (512 / (FftGeom<LOG2R>::NT * Tile<T>::W) > 32 ? 32 : 512 / (FftGeom<LOG2R>::NT * Tile<T>::W)))
+                                  : 512 / ((FftGeom<LOG2R>::NT * Tile<T>::W) < 32 ? 32 : (FftGeom<LOG2R>::NT * Tile<T>::W)))
 k4_col(const void* __restrict__ xin, int in_kind, int conj_in, long long x_stride, long long N,
        const cx_t<T>* __restrict__ cin, cx_t<T>* __restrict__ Y, int log2C, long long batch,
        const cx_t<T>* __restrict__ tw, const cx_t<T>* __restrict__ twL, int out_kind, void* __restrict__ out,

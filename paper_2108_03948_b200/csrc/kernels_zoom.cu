@@ -572,9 +572,10 @@ constexpr int WF_OUT = 32 * WZK;  // outputs per warp task
 __device__ __forceinline__ int wsw(int p) { return p ^ ((p >> 4) & 7); }
 
 int zoom_wfir_rs(const ZoomArgs& a) {
-    const int span = a.pre + WF_OUT + 2 * ZK + 1;
-    int rs = (span + 15) / 16 * 16 + 2;
-    if (rs - 16 >= span) rs -= 16;
+    // positions 0..span are written and the swizzle permutes within aligned groups of 8
+    const int need = ((a.pre + WF_OUT + 2 * ZK) | 7) + 1;
+    int rs = (need + 15) / 16 * 16 + 2;
+    if (rs - 16 >= need) rs -= 16;
     return rs;
 }
 

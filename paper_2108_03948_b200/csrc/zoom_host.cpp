@@ -164,6 +164,7 @@ const ZoomPlanG::Dev& ZoomPlanG::dev(bool f32) const {
             }
         }
         d.g = to_device(g, f32);
+        d.gh = g;
         std::vector<cd> gn(static_cast<size_t>(std::max(T, 1)), cd(0.0, 0.0));   // natural order (wrap terms)
         for (int t = 0; t < T; ++t) gn[static_cast<size_t>(t)] = filter_taps[t] * cis_cycles(-qc, static_cast<double>(t));
         d.gn = to_device(gn, f32);
@@ -199,7 +200,9 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
     const bool wfir = zoom_wfir_fits(a, f32, x, x_stride);
     static const bool no_pfir = getenv("SKG_ZOOM_NO_PFIR") != nullptr;
     const bool pfir = !no_pfir && zoom_pfir_lh(a) > 0;
-    if (single && (wfir || pfir) && !force) {
+    static const bool no_cfir = getenv("SKG_ZOOM_NO_CFIR") != nullptr;
+    const bool cfir = !no_cfir && zoom_cfir_available(a);
+    if (single && (wfir || pfir || cfir) && !force) {
         // warp-chunk FIR -> work rows (L2-resident chunk of records) -> FFT + band gather
         const size_t cs = f32 ? 8 : 16, es = f32 ? 4 : 8;
         const long long zrow = a.nout;
@@ -211,8 +214,14 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
         for (long long b0 = 0; b0 < batch; b0 += chunk) {
             const long long nb = std::min(chunk, batch - b0);
             const void* xb = static_cast<const char*>(x) + b0 * x_stride * (long long)es;
+            // phase-lane FIR where it exists (power-of-two D <= 16), else the constant-bank FIR for the
+            // specialised (D, T) pairs, else the warp-window FIR (all three measured within a few
+            // percent of each other on cfg3)
             if (pfir)
                 check(launch_zoom_pfir(a, f32, xb, x_stride, nb, d.g.p, d.gn.p, d.sdec.p, zb, zrow, st), "zoom fir");
+            else if (cfir)
+                check(launch_zoom_cfir(a, f32, xb, x_stride, nb, d.gh.data(), d.gn.p, d.sdec.p, zb, zrow, st),
+                      "zoom fir");
             else
                 check(launch_zoom_wfir(a, f32, xb, x_stride, nb, d.g.p, d.sdec.p, zb, zrow, st), "zoom fir");
             check(launch_zoom_fftband(lg, f32, zb, zrow, a.nout, nb, (int)k_lo, (int)bins(), tw, d.band.p,

@@ -68,8 +68,9 @@ def test_czt_guards(prec, n, m):
 
 
 @pytest.mark.parametrize("prec", ["f64", "f32"])
-@pytest.mark.parametrize("kw", [{"decimation": 8, "num_taps": 65}, {"decimation": 5}, {"decimation": 4, "circular": 0,
-                                                                                         "trim_transient": 1}])
+@pytest.mark.parametrize("kw", [{"decimation": 8, "num_taps": 65}, {"decimation": 5}, {"decimation": 3},
+                                {"decimation": 6}, {"decimation": 16}, {"decimation": 4, "circular": 0,
+                                                                        "trim_transient": 1}])
 def test_zoom_guards(prec, kw):
     x = torch.from_numpy(W.cfg3_batch(23, 4096)).cuda()
     x = x if prec == "f64" else x.float()

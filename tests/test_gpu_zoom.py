@@ -168,7 +168,7 @@ x = W.cfg3_batch(6, 4096)
 outs = []
 for prec in ("f64", "f32"):
     for kw in ({{"decimation": 8, "num_taps": 65}}, {{"decimation": 4, "circular": 0, "trim_transient": 1}},
-               {{"decimation": 5}}, {{"decimation": 16}}):
+               {{"decimation": 5}}, {{"decimation": 16}}, {{"decimation": 3}}):
         p = sk.ZoomPlanGPU(4096, 0.4e12, 1.2e12, W.FS, sk.SKG_F64 if prec == "f64" else sk.SKG_F32, **kw)
         xd = torch.from_numpy(x).to(torch.float64 if prec == "f64" else torch.float32).cuda()
         outs.append(p.execute(xd).cpu().numpy().astype(np.complex128))
@@ -176,11 +176,12 @@ np.savez({out!r}, *outs)
 """
 
 
-@pytest.mark.parametrize("env", [{}, {"SKG_ZOOM_NO_PFIR": "1"}, {"SKG_ZOOM_PATH": "fused"},
-                                 {"SKG_ZOOM_PATH": "unfused"}], ids=["split-pfir", "split-wfir", "fused", "unfused"])
+@pytest.mark.parametrize("env", [{}, {"SKG_ZOOM_NO_PFIR": "1"}, {"SKG_ZOOM_NO_PFIR": "1", "SKG_ZOOM_NO_CFIR": "1"},
+                                 {"SKG_ZOOM_PATH": "fused"}, {"SKG_ZOOM_PATH": "unfused"}],
+                         ids=["split-pfir", "split-cfir", "split-wfir", "fused", "unfused"])
 def test_zoom_routes_match_oracle(env, tmp_path):
-    """Every zoom route (phase-lane FIR, warp-window FIR, fused single kernel, unfused FIR + FFT +
-    gather) on linear/circular, power-of-two and odd decimations, against the oracle."""
+    """Every zoom route (phase-lane FIR, constant-bank FIR, warp-window FIR, fused single kernel,
+    unfused FIR + FFT + gather) on linear/circular, power-of-two and odd decimations, against the oracle."""
     import os
     import subprocess
     import sys
@@ -194,7 +195,7 @@ def test_zoom_routes_match_oracle(env, tmp_path):
     i = 0
     for prec in ("f64", "f32"):
         for kw in ({"decimation": 8, "num_taps": 65}, {"decimation": 4, "circular": 0, "trim_transient": 1},
-                   {"decimation": 5}, {"decimation": 16}):
+                   {"decimation": 5}, {"decimation": 16}, {"decimation": 3}):
             ref = O.ZoomPlan(4096, 0.4e12, 1.2e12, W.FS, **kw)
             want = np.array([ref(r)[0] for r in x])
             g = got[f"arr_{i}"]
@@ -203,3 +204,22 @@ def test_zoom_routes_match_oracle(env, tmp_path):
                 assert rel_max_rows(g, want) <= TOL_F64, (env, kw)
             else:
                 assert rel_l2_rows(g, want) <= TOL_F32, (env, kw)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("D", list(range(2, 18)))
+def test_zoom_decimation_sweep(prec, D):
+    """Every decimation 2..17 (power-of-two, odd, composite: each FIR route and its window sizing)
+    with the reference's default 101-tap filter, circular, vs the oracle."""
+    x = W.cfg3_batch(5, 4096)
+    try:
+        ref = O.ZoomPlan(4096, 0.4e12, 1.2e12, W.FS, decimation=D)
+    except O.OracleError:
+        pytest.skip("the reference rejects this decimation for the band")
+    p = sk.ZoomPlanGPU(4096, 0.4e12, 1.2e12, W.FS, sk.SKG_F64 if prec == "f64" else sk.SKG_F32, decimation=D)
+    got = p.execute(_dev(x, prec)).cpu().numpy()
+    want = np.array([ref(r)[0] for r in x])
+    if prec == "f64":
+        assert rel_max_rows(got, want) <= TOL_F64
+    else:
+        assert rel_l2_rows(got, want) <= TOL_F32

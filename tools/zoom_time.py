@@ -12,9 +12,22 @@ import paper_2108_03948_b200 as sk  # noqa: E402
 from paper_2108_03948_b200 import workloads as W  # noqa: E402
 
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 20
+pad = int(sys.argv[2]) if len(sys.argv) > 2 else 0   # extra elements per row (row stride 4096 + pad)
 dev = torch.device("cuda", 0)
 x64 = torch.from_numpy(W.cfg3_batch(4096, 4096)).to(dev)
-for prec, x in (("f64", x64), ("f32", x64.float())):
+if pad:
+    buf = torch.zeros((4096, 4096 + pad), dtype=torch.float64, device=dev)
+    buf[:, :4096] = x64
+    x64 = buf[:, :4096]
+def f32_rows(x):
+    if not pad:
+        return x.float()
+    b = torch.zeros((x.shape[0], 4096 + pad), dtype=torch.float32, device=dev)
+    b[:, :4096] = x
+    return b[:, :4096]
+
+
+for prec, x in (("f64", x64), ("f32", f32_rows(x64))):
     for nf in (0, 2048):   # bench.py's cfg3 rows: D = 8, 65 taps, n_fft 512 (auto) and 2048
         p = sk.ZoomPlanGPU(4096, 0.4e12, 1.2e12, W.FS, sk.SKG_F32 if prec == "f32" else sk.SKG_F64, n_fft=nf,
                            decimation=8, num_taps=65)
@@ -28,4 +41,4 @@ for prec, x in (("f64", x64), ("f32", x64.float())):
             b.record()
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))
-        print(f"{prec} n_fft={p.n_fft}: median {np.median(ts):.4f} ms  min {min(ts):.4f}  max {max(ts):.4f}")
+        print(f"pad={pad} {prec} n_fft={p.n_fft}: median {np.median(ts):.4f} ms  min {min(ts):.4f}  max {max(ts):.4f}")
