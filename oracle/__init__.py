@@ -277,8 +277,12 @@ def fft_spectrum(samples, fs, transform_len=0):
 
 
 def fft_spectrum_batch(x_real, L, threads=1):
+    """fft_spectrum of each row (bench helper: power-of-two L; other lengths go through the
+    per-trace fft_spectrum, i.e. dft_any's chirp route)."""
     x_real = f64(x_real)
     count, n = x_real.shape
+    if L & (L - 1):
+        return np.stack([fft_spectrum(r, 1.0, L)[0] for r in x_real])
     out = np.empty((count, L), np.complex128)
     port().sko_bench_fft_spectrum(L, _p(x_real), n, count, threads, _p(out.view(np.float64)))
     return out

@@ -684,6 +684,7 @@ double sko_bench_czt(const sko_czt_plan* p, const double* x_real, size_t n, size
 double sko_bench_fft_spectrum(size_t L, const double* x_real, size_t n, size_t count, int threads,
                               double* out) {
     sko_fft_plan* p = sko_fft_plan_create(L);
+    if (!p) return -1.0;   /* not a power of two: the caller uses the per-trace route */
     job_t j = {1, p, L, x_real, n, 0.0, 0, 0, out};
     double dt = run_threads(j, count, threads);
     sko_fft_plan_free(p);

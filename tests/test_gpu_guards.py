@@ -96,3 +96,63 @@ def test_transfer_guards(prec):
     torch.cuda.synchronize()
     assert _same(mag, m0) and _same(ph, p0)
     assert _canaries_ok(bm, off, nb) and _canaries_ok(bp, off, nb)
+
+
+def _sizes(seed, count, lo, hi):
+    rng = np.random.default_rng(seed)
+    return [int(v) for v in rng.integers(lo, hi, size=count)]
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("case", range(12))
+def test_czt_random_sizes_guarded(prec, case):
+    """Seeded random (N, M) from 1 to ~20000 (every kernel class: resident-table, per-trace,
+    multi-pass, segmented): parity vs the oracle on 2 rows and canaries around strided outputs."""
+    import oracle as O
+    from helpers import TOL_F32, TOL_F64, rel_l2_rows, rel_max_rows
+    rng = np.random.default_rng(1000 + case)
+    n = int(rng.integers(1, 20000)) if case % 3 else int(rng.integers(1, 300))
+    m = int(rng.integers(1, 20000)) if case % 2 else int(rng.integers(1, 300))
+    xs = W.sample_traces(3, n)
+    a, w = complex(np.exp(2j * np.pi * rng.uniform(0, 0.5))), complex(np.exp(-2j * np.pi * rng.uniform(1e-5, 1e-3)))
+    x = torch.from_numpy(xs).cuda()
+    x = x if prec == "f64" else x.float()
+    p = sk.CztPlanGPU(n, a, w, m, sk.SKG_F64 if prec == "f64" else sk.SKG_F32)
+    buf, out, off, nb = _strided_out(3, m, torch.complex128 if prec == "f64" else torch.complex64)
+    p.execute(_strided_in(x), out=out)
+    torch.cuda.synchronize()
+    assert _canaries_ok(buf, off, nb)
+    want = O.CztPlan(n, a, w, m).batch_real(xs[:2].astype(np.float32).astype(np.float64) if prec == "f32" else xs[:2])
+    got = out[:2].cpu().numpy()
+    if prec == "f64":
+        assert rel_max_rows(got, want) <= TOL_F64, (n, m)
+    else:
+        assert rel_l2_rows(got, want) <= TOL_F32, (n, m)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("case", range(10))
+def test_fft_spectrum_random_sizes_guarded(prec, case):
+    """Seeded random trace lengths and transform lengths (powers of two up to 2^18 and arbitrary
+    lengths through the chirp route), full and half layouts, vs the oracle, canaries intact."""
+    import oracle as O
+    from helpers import TOL_F32, TOL_F64, rel_l2_rows, rel_max_rows
+    rng = np.random.default_rng(2000 + case)
+    n = int(rng.integers(1, 40000))
+    L = 1 << int(rng.integers(max(0, int(np.ceil(np.log2(n)))), 19)) if case % 2 == 0 else int(rng.integers(n, n + 5000))
+    layout = sk.SKG_HALF if (case % 4 == 0 and L & (L - 1) == 0) else sk.SKG_FULL
+    xs = W.sample_traces(3, n)
+    x = torch.from_numpy(xs).cuda()
+    x = x if prec == "f64" else x.float()
+    nbins = L if layout == sk.SKG_FULL else L // 2 + 1
+    buf, out, off, nb = _strided_out(3, nbins, torch.complex128 if prec == "f64" else torch.complex64)
+    sk.fft_spectrum_batch(_strided_in(x), L, layout, out=out)
+    torch.cuda.synchronize()
+    assert _canaries_ok(buf, off, nb)
+    src = xs[:2].astype(np.float32).astype(np.float64) if prec == "f32" else xs[:2]
+    want = O.fft_spectrum_batch(src, L)[:, :nbins]
+    got = out[:2].cpu().numpy()
+    if prec == "f64":
+        assert rel_max_rows(got, want) <= TOL_F64, (n, L)
+    else:
+        assert rel_l2_rows(got, want) <= TOL_F32, (n, L)
