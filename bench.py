@@ -273,7 +273,7 @@ def bench_ours(args):
     achieved_tf = c["flops"] * B / kern_s / 1e12
     hbm_gbs = c["bytes"] * B / kern_s / 1e9
     roof_t = max(c["bytes"] * B / (pk["hbm_gbs"] * 1e9), c["flops"] * B / (fp64_peak * 1e12))
-    kname = "k_czt_rt<double, 11, 8, 8"   # S=2 output segments of the L=4096 plan, run at L'=2048 (resident-table kernel)
+    kname = "k_czt_sf<double, 11, 8, 8"   # S=2 blocks of the L=4096 plan at L'=2048, one shared forward FFT
     tr = ncu_traffic(kname)
 
     # ---- e2e: host buffers through the C ABI, H2D + kernel + D2H per step ---------------------

@@ -397,6 +397,25 @@ CztPlanG::CztPlanG(size_t n, cd a, cd w, size_t m) : n_(n), m_(m) {
         const double t = static_cast<double>(i);
         kern_[Ls_ - i] = W.pow(-0.5 * t * t);
     }
+    if (nseg_ > 1 && log2L_ <= single_cta_max_log2(false)) {
+        // shared-forward form (kernels_impl.cuh k_czt_sf): block s convolves the segment-0 chirped
+        // input with g_s[j] = W^{-(s M' + j)^2/2}, j in (-n, M'), and finishes with W^{(s M' + k)^2/2}
+        kern_sf_.assign(nseg_ * Ls_, cd(0.0, 0.0));
+        cout_sf_.assign(nseg_ * seg_, cd(0.0, 0.0));
+        for (size_t sg = 0; sg < nseg_; ++sg) {
+            const double k0 = static_cast<double>(sg * seg_);
+            cd* kr = kern_sf_.data() + sg * Ls_;
+            for (size_t j = 0; j < seg_; ++j) {
+                const double t = k0 + static_cast<double>(j);
+                kr[j] = W.pow(-0.5 * t * t);
+                cout_sf_[sg * seg_ + j] = W.pow(0.5 * t * t);
+            }
+            for (size_t i = 1; i < n; ++i) {
+                const double t = k0 - static_cast<double>(i);
+                kr[Ls_ - i] = W.pow(-0.5 * t * t);
+            }
+        }
+    }
 }
 
 const CztPlanG::Dev& CztPlanG::dev(bool f32) const {
@@ -428,6 +447,21 @@ const CztPlanG::Dev& CztPlanG::dev(bool f32) const {
             d.khat = std::move(k32);
         } else {
             d.khat = std::move(k64);
+        }
+        if (!kern_sf_.empty()) {   // the per-block kernel spectra, same fp64 FFT + 1/L scale
+            DevMem ks = to_device(kern_sf_, false);
+            fft_c2c(Ls_, false, false, ks.p, (long long)Ls_, ks.p, (long long)Ls_, (long long)nseg_, nullptr);
+            check(launch_scale_c64(ks.p, (long long)(nseg_ * Ls_), 1.0 / static_cast<double>(Ls_), nullptr), "scale");
+            count_launch();
+            if (f32) {
+                DevMem k32(nseg_ * Ls_ * 2 * sizeof(float));
+                check(launch_c64_to_c32(ks.p, k32.p, (long long)(nseg_ * Ls_), nullptr), "convert");
+                count_launch();
+                d.khat_sf = std::move(k32);
+            } else {
+                d.khat_sf = std::move(ks);
+            }
+            d.cout_sf = to_device(cout_sf_, f32);
         }
         check(cudaStreamSynchronize(nullptr), "czt plan upload");
     });
@@ -478,6 +512,19 @@ void CztPlanG::execute(const void* x, bool complex_in, long long x_stride, long 
     }
     const void* tw = stockham_twiddles(log2L_, f32);
     cudaError_t e;
+    static const bool no_sf = std::getenv("SKG_CZT_NO_SF") != nullptr;
+    if (!kern_sf_.empty() && !no_sf) {
+        e = f32 ? launch_czt_sf<float>(log2L_, N, (long long)m_, complex_in, x, x_stride, batch, (int)nseg_,
+                                       (long long)seg_, out, out_stride, tw, d.cin.p, d.khat_sf.p, d.cout_sf.p, st)
+                : launch_czt_sf<double>(log2L_, N, (long long)m_, complex_in, x, x_stride, batch, (int)nseg_,
+                                        (long long)seg_, out, out_stride, tw, d.cin.p, d.khat_sf.p, d.cout_sf.p, st);
+        if (e != cudaErrorNotSupported) {
+            check(e, "czt launch");
+            count_launch();
+            return;
+        }
+        cudaGetLastError();
+    }
     if (f32)
         e = launch_czt<float>(log2L_, N, (long long)m_, complex_in, x, x_stride, batch, (int)nseg_, (long long)seg_,
                               (long long)n_, out, out_stride, tw,

@@ -93,12 +93,14 @@ class CztPlanG {
   private:
     struct Dev {
         DevMem cin, cout, khat;
+        DevMem khat_sf, cout_sf;   // shared-forward tables (nseg > 1): per-block kernel spectra / out chirps
     };
     const Dev& dev(bool f32) const;
     size_t n_, m_, L_;
     size_t nseg_ = 1, seg_ = 0, Ls_ = 0;
     int log2L_;   // of Ls_
     std::vector<cd> cin_, cout_, kern_;
+    std::vector<cd> kern_sf_, cout_sf_;   // nseg x Ls kernel segments, nseg x seg output chirps
     mutable std::once_flag once_[2];
     mutable Dev dev_[2];
     mutable DevMem work_;   // four-step scratch (lazily sized)

@@ -38,6 +38,15 @@ cudaError_t launch_czt(int log2L, long long N, long long M, bool complex_in, con
                        void* out, long long out_stride, const void* tw, const void* cin, const void* khat,
                        const void* cout, cudaStream_t st);
 
+// shared-forward segmented CZT: one forward FFT of x*cin (cin = segment 0's chirp) serves all nseg
+// blocks; khat = nseg x L kernel spectra (block s: g[j] = W^{-(s seg + j)^2/2}, prescaled 1/L),
+// cout = nseg x seg_len output chirps W^{(s seg + k)^2/2}. cudaErrorNotSupported when the
+// geometry has no instantiation or the per-CTA shared memory does not fit (caller falls back).
+template <typename T>
+cudaError_t launch_czt_sf(int log2L, long long N, long long M, bool complex_in, const void* x, long long x_stride,
+                          long long batch, int nseg, long long seg_len, void* out, long long out_stride,
+                          const void* tw, const void* cin, const void* khat, const void* cout, cudaStream_t st);
+
 // ---- four-step passes for L = R * C beyond one CTA (kernels_4step.cuh) ----------------------
 // in_kind: 0 complex x, 1 real x, 2 real x * chirp, 3 complex x * chirp, 4 work buffer Y
 // out_kind: 0 Y with the W_L twiddle, 1 out * chirp_out (n < M), 2 out * scale (conj optional)

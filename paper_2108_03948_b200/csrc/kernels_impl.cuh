@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 
@@ -344,6 +345,118 @@ k_czt_rt(const void* __restrict__ xin, long long x_stride, long long N, long lon
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Shared-forward segmented Bluestein CZT. The M bins run as S blocks of M' = seg_len; block s is
+// the linear convolution of the SAME chirped input y = x·cin (cin = A^{-n} W^{n^2/2}) with the
+// kernel segment g_s[j] = W^{-(sM' + j)^2/2}, j in (-N, M'), so ONE forward FFT serves all S
+// blocks:  X[sM' + k'] = cout_s[k'] · IFFT(FFT(y) · K̂_s)[k'],  cout_s[k'] = W^{(sM'+k')^2/2}.
+// Against per-segment start points (A_s = A W^{-sM'}: S forward + S inverse transforms) this does
+// 1 + S transforms per trace (configs[1]: 3 instead of 4). The spectrum Y is parked in a private
+// per-group shared buffer (each thread re-reads only its own positions: no barrier) while the
+// blocks' inverse transforms run. RG trace groups per CTA, named barriers per group.
+template <int LOG2L, int RG> struct SfCfg {
+    static constexpr int BLOCK = FftGeom<LOG2L>::NT * RG;
+};
+
+// TS: 0 kernel spectra and output chirps read through L1/L2, 1 kernel spectra in shared memory,
+// 2 both in shared memory
+template <typename T, int LOG2L, int NZ, int NO, bool CPLX, int RG, int TS>
+__global__ void __launch_bounds__(SfCfg<LOG2L, RG>::BLOCK, 1)
+k_czt_sf(const void* __restrict__ xin, long long x_stride, long long N, long long M, long long batch, int nseg,
+         long long seg_len, cx_t<T>* __restrict__ out, long long out_stride, const cx_t<T>* __restrict__ tw,
+         const cx_t<T>* __restrict__ cin, const cx_t<T>* __restrict__ khat, const cx_t<T>* __restrict__ cout) {
+    using C = cx_t<T>;
+    using G = FftGeom<LOG2L>;
+    constexpr bool KS = TS >= 1, CS = TS >= 2;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int gid = threadIdx.x / G::NT;
+    const int tid = threadIdx.x % G::NT;
+    C* sm = reinterpret_cast<C*>(smraw) + gid * G::SMEM;
+    C* yb = reinterpret_cast<C*>(smraw) + RG * G::SMEM + gid * G::L;
+    C* tws = reinterpret_cast<C*>(smraw) + RG * (G::SMEM + G::L);
+    C* s_cin = tws + G::TW_ALLOC;
+    C* s_kh = s_cin + N;                       // KS: nseg x L
+    C* s_co = s_kh + (KS ? nseg * G::L : 0);   // CS: nseg x seg_len
+    load_twiddles<LOG2L>(tws, tw);
+    for (int i = threadIdx.x; i < N; i += blockDim.x) s_cin[i] = __ldg(cin + i);
+    if constexpr (KS)
+        for (int i = threadIdx.x; i < nseg * G::L; i += blockDim.x) s_kh[i] = __ldg(khat + i);
+    if constexpr (CS)
+        for (long long i = threadIdx.x; i < nseg * seg_len; i += blockDim.x) s_co[i] = __ldg(cout + i);
+    __syncthreads();
+    const C* kh_all = KS ? s_kh : khat;
+    const C* co_all = CS ? s_co : cout;
+    const GroupSync gsync{1 + gid, G::NT};
+    constexpr int NX = NZ < G::EPT ? NZ : G::EPT;
+    using XT = typename std::conditional<CPLX, C, T>::type;
+    for (long long b = (long long)blockIdx.x * RG + gid; b < batch; b += (long long)gridDim.x * RG) {
+        XT xr[NX];
+#pragma unroll
+        for (int q = 0; q < NX; ++q) {
+            const long long pos = tid + (long long)G::NT * q;
+            if constexpr (CPLX) xr[q] = czero<C>();
+            else xr[q] = (T)0;
+            if (pos < N) xr[q] = __ldg(reinterpret_cast<const XT*>(xin) + b * x_stride + pos);
+        }
+        {   // the group's next trace into L2
+            const long long bn = b + (long long)gridDim.x * RG;
+            if (bn < batch) {
+#pragma unroll
+                for (int q = 0; q < NX; ++q) {
+                    const long long pos = tid + (long long)G::NT * q;
+                    if (pos < N) prefetch_l2(reinterpret_cast<const XT*>(xin) + bn * x_stride + pos);
+                }
+            }
+        }
+        C v[G::EPT];
+#pragma unroll
+        for (int q = 0; q < G::EPT; ++q) {
+            v[q] = czero<C>();
+            const long long pos = tid + (long long)G::NT * q;
+            if (q < NX && pos < N) {
+                if constexpr (CPLX) v[q] = cmul(xr[q], s_cin[pos]);
+                else v[q] = rmul(xr[q], s_cin[pos]);
+            }
+        }
+        block_fft<false, LOG2L, NZ>(v, sm, tws, tid, true, gsync);
+        for (int sg = 0; sg < nseg; ++sg) {
+            if (sg == 0) {
+                if (nseg > 1) {
+#pragma unroll
+                    for (int q = 0; q < G::EPT; ++q) yb[q * G::NT + tid] = v[q];
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < G::EPT; ++q) v[q] = yb[q * G::NT + tid];
+            }
+            const C* kh = kh_all + (long long)sg * G::L;
+#pragma unroll
+            for (int q = 0; q < G::EPT; ++q) {
+                v[q] = cmul(v[q], KS ? kh[tid + G::NT * q] : __ldg(kh + tid + G::NT * q));
+                if ((q & 3) == 3) asm volatile("" ::: "memory");
+            }
+            block_fft<true, LOG2L, 16, NO>(v, sm, tws, tid, true, gsync);
+            const long long m_here = min(seg_len, M - sg * seg_len);
+            const C* co = co_all + sg * seg_len;
+            C* o = out + b * out_stride + sg * seg_len;
+#pragma unroll
+            for (int q = 0; q < G::EPT; ++q) {
+                const long long pos = tid + (long long)G::NT * q;
+                if (q < NO && pos < m_here) o[pos] = cmul(v[q], CS ? co[pos] : __ldg(co + pos));
+                if ((q & 3) == 3) asm volatile("" ::: "memory");
+            }
+            gsync();   // the next transform's first exchange must not overwrite this one's last reads
+        }
+    }
+}
+
+template <typename T, int LOG2L>
+inline size_t sf_smem_bytes(int rg, int ts, long long N, int nseg, long long seg_len) {
+    using G = FftGeom<LOG2L>;
+    return ((size_t)rg * (G::SMEM + G::L) + G::TW_ALLOC + (size_t)N + (ts >= 1 ? (size_t)nseg * G::L : 0) +
+            (ts >= 2 ? (size_t)nseg * seg_len : 0)) * sizeof(cx_t<T>);
+}
+
 template <typename T, int LOG2L>
 inline size_t rt_smem_bytes(long long N, long long seg_len) {
     using G = FftGeom<LOG2L>;
@@ -488,6 +601,71 @@ cudaError_t launch_fft_r2c_impl(int log2M, long long N, const T* x, long long x_
             return run_r2c<T, LG, NZ, 2>(N, x, x_stride, batch, tw, post, out, out_stride, rtab, mag, phase,
                                          mp_stride, st);
         });
+    });
+}
+
+template <typename T, int LOG2L, int NZ, int NO>
+cudaError_t run_czt_sf(long long N, long long M, bool complex_in, const void* x, long long x_stride, long long batch,
+                       int nseg, long long seg_len, void* out, long long out_stride, const void* tw, const void* cin,
+                       const void* khat, const void* cout, cudaStream_t st) {
+    using C = cx_t<T>;
+    if constexpr (FftGeom<LOG2L>::NT < 32) {
+        return cudaErrorNotSupported;
+    } else {
+        const size_t lim = (size_t)smem_optin();
+        if (batch < 8) return cudaErrorNotSupported;
+        // configurations in preference order (measured on configs[1]); SKG_CZT_SF_CFG="rg,ts" pins one
+        static const char* env = getenv("SKG_CZT_SF_CFG");
+        int want_rg = 0, want_ts = -1;
+        if (env) sscanf(env, "%d,%d", &want_rg, &want_ts);
+        auto go = [&](auto rgc, auto tsc) -> cudaError_t {
+            constexpr int RG = decltype(rgc)::value, TS = decltype(tsc)::value;
+            if (want_rg && (want_rg != RG || want_ts != TS)) return cudaErrorNotSupported;
+            const size_t smem = sf_smem_bytes<T, LOG2L>(RG, TS, N, nseg, seg_len);
+            if (smem > lim) return cudaErrorNotSupported;
+            auto launch = [&](auto kern) {
+                cudaError_t e = prep_smem(kern, smem);
+                if (e != cudaSuccess) return e;
+                const unsigned g = persistent_grid(kern, SfCfg<LOG2L, RG>::BLOCK, smem, (batch + RG - 1) / RG);
+                kern<<<g, SfCfg<LOG2L, RG>::BLOCK, smem, st>>>(x, x_stride, N, M, batch, nseg, seg_len, (C*)out,
+                                                               out_stride, (const C*)tw, (const C*)cin, (const C*)khat,
+                                                               (const C*)cout);
+                return cudaGetLastError();
+            };
+            return complex_in ? launch(k_czt_sf<T, LOG2L, NZ, NO, true, RG, TS>)
+                              : launch(k_czt_sf<T, LOG2L, NZ, NO, false, RG, TS>);
+        };
+        cudaError_t e;
+        if ((e = go(IC<4>{}, IC<2>{})) != cudaErrorNotSupported) return e;
+        if ((e = go(IC<3>{}, IC<2>{})) != cudaErrorNotSupported) return e;
+        if ((e = go(IC<3>{}, IC<0>{})) != cudaErrorNotSupported) return e;
+        if ((e = go(IC<2>{}, IC<1>{})) != cudaErrorNotSupported) return e;
+        if ((e = go(IC<2>{}, IC<0>{})) != cudaErrorNotSupported) return e;
+        return cudaErrorNotSupported;
+    }
+}
+
+template <typename T>
+cudaError_t launch_czt_sf_impl(int log2L, long long N, long long M, bool complex_in, const void* x, long long x_stride,
+                               long long batch, int nseg, long long seg_len, void* out, long long out_stride,
+                               const void* tw, const void* cin, const void* khat, const void* cout, cudaStream_t st) {
+    if (log2L < 9 || log2L > 12) return cudaErrorNotSupported;   // instantiated for 512..4096
+    return dispatch_log2<9, 12>(log2L, [&](auto lg) {
+        constexpr int LG = decltype(lg)::value;
+        if constexpr (LG > max_log2<T>()) {
+            return cudaErrorNotSupported;
+        } else {
+            const int nz = nz_class(N, FftGeom<LG>::NT);
+            const int no = no_class(seg_len, FftGeom<LG>::NT);
+            return dispatch_nz<LG>(nz, [&](auto z) {
+                constexpr int NZ = decltype(z)::value;
+                if (no == 8)
+                    return run_czt_sf<T, LG, NZ, 8>(N, M, complex_in, x, x_stride, batch, nseg, seg_len, out,
+                                                    out_stride, tw, cin, khat, cout, st);
+                return run_czt_sf<T, LG, NZ, 16>(N, M, complex_in, x, x_stride, batch, nseg, seg_len, out, out_stride,
+                                                 tw, cin, khat, cout, st);
+            });
+        }
     });
 }
 
