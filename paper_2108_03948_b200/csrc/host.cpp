@@ -514,10 +514,18 @@ void CztPlanG::execute(const void* x, bool complex_in, long long x_stride, long 
     cudaError_t e;
     static const bool no_sf = std::getenv("SKG_CZT_NO_SF") != nullptr;
     if (!kern_sf_.empty() && !no_sf) {
+        // spectrum parking slots: one per transform group that can be resident (4 per SM)
+        int sms = 0;
+        check(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, current_device()), "attr");
+        const long long slots = 4LL * sms;
+        void* yw = stream_alloc((size_t)slots * Ls_ * (f32 ? 8 : 16), st);
         e = f32 ? launch_czt_sf<float>(log2L_, N, (long long)m_, complex_in, x, x_stride, batch, (int)nseg_,
-                                       (long long)seg_, out, out_stride, tw, d.cin.p, d.khat_sf.p, d.cout_sf.p, st)
+                                       (long long)seg_, out, out_stride, tw, d.cin.p, d.khat_sf.p, d.cout_sf.p, yw,
+                                       slots, st)
                 : launch_czt_sf<double>(log2L_, N, (long long)m_, complex_in, x, x_stride, batch, (int)nseg_,
-                                        (long long)seg_, out, out_stride, tw, d.cin.p, d.khat_sf.p, d.cout_sf.p, st);
+                                        (long long)seg_, out, out_stride, tw, d.cin.p, d.khat_sf.p, d.cout_sf.p, yw,
+                                        slots, st);
+        cudaFreeAsync(yw, st);
         if (e != cudaErrorNotSupported) {
             check(e, "czt launch");
             count_launch();

@@ -358,22 +358,25 @@ template <int LOG2L, int RG> struct SfCfg {
     static constexpr int BLOCK = FftGeom<LOG2L>::NT * RG;
 };
 
-// TS: 0 kernel spectra and output chirps read through L1/L2, 1 kernel spectra in shared memory,
-// 2 both in shared memory
+// TS (bits): 0 kernel spectra and output chirps read through L1/L2, 1 kernel spectra in shared
+// memory, 2 both in shared memory; +4: the parked spectrum Y lives in a global (L2-resident)
+// workspace slot per group instead of shared memory (frees 32 KB per group for more groups)
 template <typename T, int LOG2L, int NZ, int NO, bool CPLX, int RG, int TS>
 __global__ void __launch_bounds__(SfCfg<LOG2L, RG>::BLOCK, 1)
 k_czt_sf(const void* __restrict__ xin, long long x_stride, long long N, long long M, long long batch, int nseg,
          long long seg_len, cx_t<T>* __restrict__ out, long long out_stride, const cx_t<T>* __restrict__ tw,
-         const cx_t<T>* __restrict__ cin, const cx_t<T>* __restrict__ khat, const cx_t<T>* __restrict__ cout) {
+         const cx_t<T>* __restrict__ cin, const cx_t<T>* __restrict__ khat, const cx_t<T>* __restrict__ cout,
+         cx_t<T>* __restrict__ ywork) {
     using C = cx_t<T>;
     using G = FftGeom<LOG2L>;
-    constexpr bool KS = TS >= 1, CS = TS >= 2;
+    constexpr bool KS = (TS & 3) >= 1, CS = (TS & 3) >= 2, YG = (TS & 4) != 0;
     extern __shared__ __align__(16) unsigned char smraw[];
     const int gid = threadIdx.x / G::NT;
     const int tid = threadIdx.x % G::NT;
     C* sm = reinterpret_cast<C*>(smraw) + gid * G::SMEM;
-    C* yb = reinterpret_cast<C*>(smraw) + RG * G::SMEM + gid * G::L;
-    C* tws = reinterpret_cast<C*>(smraw) + RG * (G::SMEM + G::L);
+    C* yb = YG ? ywork + ((long long)blockIdx.x * RG + gid) * G::L
+               : reinterpret_cast<C*>(smraw) + RG * G::SMEM + gid * G::L;
+    C* tws = reinterpret_cast<C*>(smraw) + RG * (G::SMEM + (YG ? 0 : G::L));
     C* s_cin = tws + G::TW_ALLOC;
     C* s_kh = s_cin + N;                       // KS: nseg x L
     C* s_co = s_kh + (KS ? nseg * G::L : 0);   // CS: nseg x seg_len
@@ -453,8 +456,9 @@ k_czt_sf(const void* __restrict__ xin, long long x_stride, long long N, long lon
 template <typename T, int LOG2L>
 inline size_t sf_smem_bytes(int rg, int ts, long long N, int nseg, long long seg_len) {
     using G = FftGeom<LOG2L>;
-    return ((size_t)rg * (G::SMEM + G::L) + G::TW_ALLOC + (size_t)N + (ts >= 1 ? (size_t)nseg * G::L : 0) +
-            (ts >= 2 ? (size_t)nseg * seg_len : 0)) * sizeof(cx_t<T>);
+    return ((size_t)rg * (G::SMEM + ((ts & 4) ? 0 : G::L)) + G::TW_ALLOC + (size_t)N +
+            ((ts & 3) >= 1 ? (size_t)nseg * G::L : 0) + ((ts & 3) >= 2 ? (size_t)nseg * seg_len : 0)) *
+           sizeof(cx_t<T>);
 }
 
 template <typename T, int LOG2L>
@@ -607,7 +611,7 @@ cudaError_t launch_fft_r2c_impl(int log2M, long long N, const T* x, long long x_
 template <typename T, int LOG2L, int NZ, int NO>
 cudaError_t run_czt_sf(long long N, long long M, bool complex_in, const void* x, long long x_stride, long long batch,
                        int nseg, long long seg_len, void* out, long long out_stride, const void* tw, const void* cin,
-                       const void* khat, const void* cout, cudaStream_t st) {
+                       const void* khat, const void* cout, void* ywork, long long ywork_slots, cudaStream_t st) {
     using C = cx_t<T>;
     if constexpr (FftGeom<LOG2L>::NT < 32) {
         return cudaErrorNotSupported;
@@ -623,13 +627,15 @@ cudaError_t run_czt_sf(long long N, long long M, bool complex_in, const void* x,
             if (want_rg && (want_rg != RG || want_ts != TS)) return cudaErrorNotSupported;
             const size_t smem = sf_smem_bytes<T, LOG2L>(RG, TS, N, nseg, seg_len);
             if (smem > lim) return cudaErrorNotSupported;
+            if ((TS & 4) && (!ywork || nseg < 2)) return cudaErrorNotSupported;
             auto launch = [&](auto kern) {
                 cudaError_t e = prep_smem(kern, smem);
                 if (e != cudaSuccess) return e;
-                const unsigned g = persistent_grid(kern, SfCfg<LOG2L, RG>::BLOCK, smem, (batch + RG - 1) / RG);
+                unsigned g = persistent_grid(kern, SfCfg<LOG2L, RG>::BLOCK, smem, (batch + RG - 1) / RG);
+                if (TS & 4) g = (unsigned)std::min<long long>(g, ywork_slots / RG);   // one workspace slot per group
                 kern<<<g, SfCfg<LOG2L, RG>::BLOCK, smem, st>>>(x, x_stride, N, M, batch, nseg, seg_len, (C*)out,
                                                                out_stride, (const C*)tw, (const C*)cin, (const C*)khat,
-                                                               (const C*)cout);
+                                                               (const C*)cout, (C*)ywork);
                 return cudaGetLastError();
             };
             return complex_in ? launch(k_czt_sf<T, LOG2L, NZ, NO, true, RG, TS>)
@@ -637,6 +643,7 @@ cudaError_t run_czt_sf(long long N, long long M, bool complex_in, const void* x,
         };
         cudaError_t e;
         if ((e = go(IC<4>{}, IC<2>{})) != cudaErrorNotSupported) return e;
+        if ((e = go(IC<4>{}, IC<5>{})) != cudaErrorNotSupported) return e;
         if ((e = go(IC<3>{}, IC<2>{})) != cudaErrorNotSupported) return e;
         if ((e = go(IC<3>{}, IC<0>{})) != cudaErrorNotSupported) return e;
         if ((e = go(IC<2>{}, IC<1>{})) != cudaErrorNotSupported) return e;
@@ -648,7 +655,8 @@ cudaError_t run_czt_sf(long long N, long long M, bool complex_in, const void* x,
 template <typename T>
 cudaError_t launch_czt_sf_impl(int log2L, long long N, long long M, bool complex_in, const void* x, long long x_stride,
                                long long batch, int nseg, long long seg_len, void* out, long long out_stride,
-                               const void* tw, const void* cin, const void* khat, const void* cout, cudaStream_t st) {
+                               const void* tw, const void* cin, const void* khat, const void* cout, void* ywork,
+                               long long ywork_slots, cudaStream_t st) {
     if (log2L < 9 || log2L > 12) return cudaErrorNotSupported;   // instantiated for 512..4096
     return dispatch_log2<9, 12>(log2L, [&](auto lg) {
         constexpr int LG = decltype(lg)::value;
@@ -661,9 +669,9 @@ cudaError_t launch_czt_sf_impl(int log2L, long long N, long long M, bool complex
                 constexpr int NZ = decltype(z)::value;
                 if (no == 8)
                     return run_czt_sf<T, LG, NZ, 8>(N, M, complex_in, x, x_stride, batch, nseg, seg_len, out,
-                                                    out_stride, tw, cin, khat, cout, st);
+                                                    out_stride, tw, cin, khat, cout, ywork, ywork_slots, st);
                 return run_czt_sf<T, LG, NZ, 16>(N, M, complex_in, x, x_stride, batch, nseg, seg_len, out, out_stride,
-                                                 tw, cin, khat, cout, st);
+                                                 tw, cin, khat, cout, ywork, ywork_slots, st);
             });
         }
     });
