@@ -46,6 +46,23 @@ SK_API sk_status skg_fft_spectrum_batch(size_t n, size_t transform_len, int prec
                                         const void* d_x, size_t x_stride, size_t batch,
                                         void* d_out, size_t out_stride, void* stream);
 
+/* Band slice + dB column. skg_band_bins restates slice_band's bin selection
+ * (spectra.cpp:40-61: 1e-9-step slack, clipped to the spectrum, same errors) for a spectrum of
+ * spectrum_size bins at f_start + k f_step. skg_fft_spectrum_band_batch writes only bins
+ * [k_lo, k_lo + count) of the full zero-padded spectrum (the sk_spectrum_slice_band result) as
+ * complex (d_bins, may be NULL) and/or magnitude_db (d_db, may be NULL; types.cpp:13-18:
+ * 20 log10|X|, -300 dB at |X| <= 1e-15), fused into the FFT store. skg_band_db_batch does the same
+ * slice/dB pass over complex rows already on the device (CZT and zoom outputs, full spectra). */
+SK_API sk_status skg_band_bins(size_t spectrum_size, double f_start_hz, double f_step_hz, double f_lo_hz,
+                               double f_hi_hz, size_t* k_lo, size_t* count, double* band_f_start_hz);
+SK_API sk_status skg_fft_spectrum_band_batch(size_t n, size_t transform_len, int precision, size_t k_lo,
+                                             size_t count, const void* d_x, size_t x_stride, size_t batch,
+                                             void* d_bins, size_t bins_stride, void* d_db, size_t db_stride,
+                                             void* stream);
+SK_API sk_status skg_band_db_batch(int precision, const void* d_in, size_t in_stride, size_t k_lo, size_t count,
+                                   size_t batch, void* d_bins, size_t bins_stride, void* d_db, size_t db_stride,
+                                   void* stream);
+
 /* Chirp-z transform plan (CztPlan, czt.cpp:85-137). */
 typedef struct skg_czt_plan skg_czt_plan;
 SK_API sk_status skg_czt_plan_create(size_t n, double a_re, double a_im, double w_re, double w_im,

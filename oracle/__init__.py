@@ -77,6 +77,7 @@ def port():
         L.sko_fft_spectrum.argtypes = [dp, sz, C.c_double, sz, C.POINTER(sz), dp]
         L.sko_slice_band.argtypes = [sz, C.c_double, C.c_double, C.c_double, C.c_double,
                                      C.POINTER(sz), C.POINTER(sz)]
+        L.sko_magnitude_db.argtypes = [dp, sz, dp]
         L.sko_design_lowpass.argtypes = [C.c_double, C.c_double, sz, dp]
         L.sko_zoom_options_defaults.argtypes = [C.POINTER(SkZoomOptions)]
         L.sko_zoom_plan_create.restype = C.c_void_p
@@ -292,6 +293,14 @@ def slice_band(n_bins, f_start, f_step, lo, hi):
     a, c = sz(0), sz(0)
     _chk(port().sko_slice_band(n_bins, f_start, f_step, lo, hi, C.byref(a), C.byref(c)))
     return a.value, c.value
+
+
+def magnitude_db(bins):
+    """types.cpp:13-18 per bin."""
+    v = c128(bins)
+    out = np.empty(v.size)
+    port().sko_magnitude_db(_p(v.view(np.float64)), v.size, _p(out))
+    return out
 
 
 def design_lowpass(cutoff, fs, taps):

@@ -355,6 +355,15 @@ int sko_slice_band(size_t n_bins, double f_start, double f_step, double f_lo, do
     return 0;
 }
 
+/* magnitude_db (types.cpp:13-18): 20 log10 |v| (|v| = hypot, as std::abs of std::complex), -300 dB
+ * floor at |v| <= 1e-15; interleaved complex in, n reals out */
+void sko_magnitude_db(const double* v, size_t n, double* out) {
+    for (size_t k = 0; k < n; ++k) {
+        const double mag = hypot(v[2 * k], v[2 * k + 1]);
+        out[k] = mag > 1e-15 ? 20.0 * log10(mag) : -300.0;
+    }
+}
+
 /* ---- zoomfft.cpp ----------------------------------------------------------------------- */
 void sko_zoom_options_defaults(sko_zoom_options* o) {   /* zoomfft.hpp:17-26 */
     memset(o, 0, sizeof *o);

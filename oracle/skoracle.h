@@ -55,6 +55,7 @@ int sko_fft_spectrum(const double* samples, size_t n, double fs, size_t transfor
                      size_t* out_len, double* out /* may be NULL to query */);
 int sko_slice_band(size_t n_bins, double f_start, double f_step, double f_lo, double f_hi,
                    size_t* k_first, size_t* k_count);
+void sko_magnitude_db(const double* v, size_t n, double* out);
 
 /* Zoom (zoomfft.hpp:17-86, zoomfft.cpp:11-239) */
 typedef struct sko_zoom_options {

@@ -100,6 +100,9 @@ def _declare(L):
         "skg_synchronize": (st, [vp]),
         "skg_fft_batch": (st, [sz, C.c_int, C.c_int, vp, sz, vp, sz, sz, vp]),
         "skg_fft_spectrum_batch": (st, [sz, sz, C.c_int, C.c_int, vp, sz, sz, vp, sz, vp]),
+        "skg_band_bins": (st, [sz, C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(sz), C.POINTER(sz), dp]),
+        "skg_fft_spectrum_band_batch": (st, [sz, sz, C.c_int, sz, sz, vp, sz, sz, vp, sz, vp, sz, vp]),
+        "skg_band_db_batch": (st, [C.c_int, vp, sz, sz, sz, sz, vp, sz, vp, sz, vp]),
         "skg_czt_plan_create": (st, [sz, C.c_double, C.c_double, C.c_double, C.c_double, sz, C.c_int,
                                      C.POINTER(vp)]),
         "skg_czt_plan_free": (None, [vp]),
@@ -417,6 +420,48 @@ def fft_spectrum_batch(x, transform_len=0, layout=SKG_FULL, out=None):
     _chk(lib().skg_fft_spectrum_batch(n, L, prec, layout, vp(x.data_ptr()), s, b, vp(out.data_ptr()),
                                       out.stride(0), _stream()))
     return out
+
+
+def band_bins(spectrum_size, f_start_hz, f_step_hz, f_lo_hz, f_hi_hz):
+    """(k_lo, count, band f_start) of slice_band on a spectrum of spectrum_size bins (skg_band_bins,
+    spectra.cpp:40-61)."""
+    k, c, f = sz(), sz(), C.c_double()
+    _chk(lib().skg_band_bins(spectrum_size, f_start_hz, f_step_hz, f_lo_hz, f_hi_hz, C.byref(k), C.byref(c),
+                             C.byref(f)))
+    return k.value, c.value, f.value
+
+
+def fft_spectrum_band_batch(x, sample_rate_hz, f_lo_hz, f_hi_hz, transform_len=0, bins=True, db=True):
+    """Band-sliced zero-padded spectra of real trace rows with the magnitude_db column, fused into the
+    FFT store (skg_fft_spectrum_band_batch). Returns (bins or None, db or None, f_start_hz, f_step_hz)."""
+    torch = _torch()
+    x, b, s = _rows(x)
+    prec = _prec(x)
+    n = x.shape[-1]
+    L = transform_len or next_pow2(n)
+    step = sample_rate_hz / L
+    k_lo, cnt, f0 = band_bins(L, 0.0, step, f_lo_hz, f_hi_hz)
+    ob = torch.empty((b, cnt), dtype=_cdtype(prec), device=x.device) if bins else None
+    od = torch.empty((b, cnt), dtype=x.dtype, device=x.device) if db else None
+    _chk(lib().skg_fft_spectrum_band_batch(n, L, prec, k_lo, cnt, vp(x.data_ptr()), s, b,
+                                           vp(ob.data_ptr()) if ob is not None else None, cnt,
+                                           vp(od.data_ptr()) if od is not None else None, cnt, _stream()))
+    return ob, od, f0, step
+
+
+def band_db_batch(spectra, k_lo, count, bins=True, db=True):
+    """Band slice [k_lo, k_lo + count) and magnitude_db of complex rows on the device
+    (skg_band_db_batch)."""
+    torch = _torch()
+    spectra, b, s = _rows(spectra)
+    prec = _prec(spectra)
+    real = torch.float64 if prec == SKG_F64 else torch.float32
+    ob = torch.empty((b, count), dtype=spectra.dtype, device=spectra.device) if bins else None
+    od = torch.empty((b, count), dtype=real, device=spectra.device) if db else None
+    _chk(lib().skg_band_db_batch(prec, vp(spectra.data_ptr()), s, k_lo, count, b,
+                                 vp(ob.data_ptr()) if ob is not None else None, count,
+                                 vp(od.data_ptr()) if od is not None else None, count, _stream()))
+    return ob, od
 
 
 class CztPlanGPU:

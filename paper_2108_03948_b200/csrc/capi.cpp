@@ -572,6 +572,40 @@ sk_status skg_fft_spectrum_batch(size_t n, size_t transform_len, int precision, 
     });
 }
 
+sk_status skg_band_bins(size_t size, double f_start, double f_step, double f_lo, double f_hi, size_t* k_lo,
+                        size_t* count, double* band_f_start) {
+    if (!k_lo || !count) return bad_arg("skg_band_bins: null output");
+    return guarded([&] {
+        const skg::BandBins r = skg::slice_band_bins(size, f_start, f_step, f_lo, f_hi);
+        *k_lo = (size_t)r.k_lo;
+        *count = (size_t)r.count;
+        if (band_f_start) *band_f_start = r.f_start;
+    });
+}
+
+sk_status skg_fft_spectrum_band_batch(size_t n, size_t transform_len, int precision, size_t k_lo, size_t count,
+                                      const void* d_x, size_t x_stride, size_t batch, void* d_bins, size_t bins_stride,
+                                      void* d_db, size_t db_stride, void* stream) {
+    if (!d_x || (!d_bins && !d_db)) return bad_arg("skg_fft_spectrum_band_batch: null buffer");
+    return guarded([&] {
+        if (n == 0) throw std::invalid_argument("trace: no samples");
+        skg::fft_spectrum_band_batch(n, transform_len, precision == SKG_F32, (long long)k_lo, (long long)count, d_x,
+                                     (long long)x_stride, (long long)batch, d_bins, (long long)bins_stride, d_db,
+                                     (long long)db_stride, (cudaStream_t)stream);
+    });
+}
+
+sk_status skg_band_db_batch(int precision, const void* d_in, size_t in_stride, size_t k_lo, size_t count, size_t batch,
+                            void* d_bins, size_t bins_stride, void* d_db, size_t db_stride, void* stream) {
+    if (!d_in || (!d_bins && !d_db)) return bad_arg("skg_band_db_batch: null buffer");
+    if (count == 0) return bad_arg("slice_band: no bins fall inside the requested band");
+    return guarded([&] {
+        skg::band_db_batch(precision == SKG_F32, d_in, (long long)in_stride, (long long)k_lo, (long long)count,
+                           (long long)batch, d_bins, (long long)bins_stride, d_db, (long long)db_stride,
+                           (cudaStream_t)stream);
+    });
+}
+
 sk_status skg_czt_plan_create(size_t n, double a_re, double a_im, double w_re, double w_im, size_t m, int precision,
                               skg_czt_plan** out) {
     if (!out) return bad_arg("skg_czt_plan_create: null output");

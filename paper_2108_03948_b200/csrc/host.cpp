@@ -228,7 +228,8 @@ const void* r2c_post_twiddles(int log2M, bool f32) {
         const size_t M = size_t{1} << log2M;
         std::vector<cd> v(M);
         const double q = -1.0 / (2.0 * static_cast<double>(M));
-        for (size_t k = 0; k < M; ++k) v[k] = cis_cycles(q, static_cast<double>(k));
+        // stored as W^k / 2: the split's 1/2 rides on the table (a power-of-two scale, exact)
+        for (size_t k = 0; k < M; ++k) v[k] = 0.5 * cis_cycles(q, static_cast<double>(k));
         return v;
     });
 }
@@ -607,12 +608,72 @@ void fft_spectrum_batch(size_t n, size_t len, bool f32, int layout, const void* 
     cudaError_t e;
     if (f32)
         e = launch_fft_r2c<float>(lgM, (long long)n, (const float*)x, x_stride, batch, tw, post, layout, out,
-                                  out_stride, nullptr, nullptr, nullptr, 0, st);
+                                  out_stride, nullptr, nullptr, nullptr, 0, 0, 0, st);
     else
         e = launch_fft_r2c<double>(lgM, (long long)n, (const double*)x, x_stride, batch, tw, post, layout, out,
-                                   out_stride, nullptr, nullptr, nullptr, 0, st);
+                                   out_stride, nullptr, nullptr, nullptr, 0, 0, 0, st);
     check(e, "fft_spectrum launch");
     count_launch();
+}
+
+// ---- band slice + magnitude_db ---------------------------------------------------------------------
+BandBins slice_band_bins(size_t size, double f_start, double f_step, double f_lo, double f_hi) {
+    // spectra.cpp:40-61, same checks in the same order
+    if (size == 0) throw std::invalid_argument("slice_band: empty spectrum");
+    if (!(f_step > 0.0)) throw std::invalid_argument("slice_band: non-positive step");
+    if (!(f_lo <= f_hi)) throw std::invalid_argument("slice_band: inverted band");
+    const double eps = 0.5 * f_step * 1e-9;
+    const double lo = (f_lo - f_start) / f_step;
+    const double hi = (f_hi - f_start) / f_step;
+    const long k_lo = static_cast<long>(std::ceil(lo - eps));
+    const long k_hi = static_cast<long>(std::floor(hi + eps));
+    const long last = static_cast<long>(size) - 1;
+    const long a = std::max(k_lo, 0L), b = std::min(k_hi, last);
+    if (a > b) throw std::invalid_argument("slice_band: no bins fall inside the requested band");
+    BandBins r;
+    r.k_lo = a;
+    r.count = b - a + 1;
+    r.f_start = f_start + static_cast<double>(a) * f_step;   // Spectrum::frequency(a)
+    return r;
+}
+
+void band_db_batch(bool f32, const void* in, long long in_stride, long long k_lo, long long count, long long batch,
+                   void* out, long long out_stride, void* db, long long db_stride, cudaStream_t st) {
+    if (batch <= 0 || count <= 0 || (!out && !db)) return;
+    check(launch_band_db(f32, in, in_stride, k_lo, count, batch, out, out_stride, db, db_stride, st), "band launch");
+    count_launch();
+}
+
+void fft_spectrum_band_batch(size_t n, size_t len, bool f32, long long k_lo, long long count, const void* x,
+                             long long x_stride, long long batch, void* out, long long out_stride, void* db,
+                             long long db_stride, cudaStream_t st) {
+    if (len == 0) len = next_pow2(n);
+    if (len < n) throw std::invalid_argument("fft_spectrum: transform length shorter than the trace");
+    if (k_lo < 0 || count <= 0 || (size_t)(k_lo + count) > len)
+        throw std::invalid_argument("fft_spectrum_band: band outside the spectrum");
+    if (batch <= 0 || (!out && !db)) return;
+    const int lgM = is_pow2(len) && len >= 2 ? ilog2(len) - 1 : -1;
+    if (lgM >= 0 && lgM <= single_cta_max_log2(f32)) {
+        // fused: the FFT store epilogue writes only the band (and its dB column)
+        const void* tw = stockham_twiddles(lgM, f32);
+        const void* post = r2c_post_twiddles(lgM, f32);
+        cudaError_t e;
+        if (f32)
+            e = launch_fft_r2c<float>(lgM, (long long)n, (const float*)x, x_stride, batch, tw, post, 3, out,
+                                      out_stride, nullptr, (float*)db, nullptr, db_stride, k_lo, k_lo + count - 1, st);
+        else
+            e = launch_fft_r2c<double>(lgM, (long long)n, (const double*)x, x_stride, batch, tw, post, 3, out,
+                                       out_stride, nullptr, (double*)db, nullptr, db_stride, k_lo, k_lo + count - 1,
+                                       st);
+        check(e, "fft_spectrum_band launch");
+        count_launch();
+        return;
+    }
+    // multi-pass / chirp routes: full spectrum into a work buffer, then the band pass
+    const size_t cs = f32 ? 8 : 16;
+    Scratch full((size_t)batch * len * cs, st);
+    fft_spectrum_batch(n, len, f32, 0, x, x_stride, batch, full.p, (long long)len, st);
+    band_db_batch(f32, full.p, (long long)len, k_lo, count, batch, out, out_stride, db, db_stride, st);
 }
 
 // ---- transfer function ---------------------------------------------------------------------------
@@ -652,10 +713,10 @@ void TransferPlanG::execute(const void* x, long long x_stride, long long batch, 
     cudaError_t e;
     if (f32_)
         e = launch_fft_r2c<float>(lgM, (long long)n_, (const float*)x, x_stride, batch, tw, post, 2, h, h_stride,
-                                  rtab_.p, (float*)mag, (float*)phase, mp_stride, st);
+                                  rtab_.p, (float*)mag, (float*)phase, mp_stride, 0, 0, st);
     else
         e = launch_fft_r2c<double>(lgM, (long long)n_, (const double*)x, x_stride, batch, tw, post, 2, h, h_stride,
-                                   rtab_.p, (double*)mag, (double*)phase, mp_stride, st);
+                                   rtab_.p, (double*)mag, (double*)phase, mp_stride, 0, 0, st);
     check(e, "transfer launch");
     count_launch();
 }

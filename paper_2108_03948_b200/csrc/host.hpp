@@ -63,7 +63,7 @@ DevMem to_device(const std::vector<cd>& h, bool f32);
 
 // cached per-device twiddle tables for the Stockham engine (FftGeom<log2L>)
 const void* stockham_twiddles(int log2L, bool f32);
-// W_{2M}^k, k < M: post-processing twiddles of the real-input transform
+// W_{2M}^k / 2, k < M: post-processing twiddles of the real-input transform (1/2 of the split folded in)
 const void* r2c_post_twiddles(int log2M, bool f32);
 // four-step tables: W_L^{r c} for the (R x C) split of L = R*C
 const void* fourstep_twiddles(int log2R, int log2C, bool f32);
@@ -110,6 +110,20 @@ class CztPlanG {
 // zero-padded spectrum of real traces; layout 0 full, 1 half (pow2 only)
 void fft_spectrum_batch(size_t n, size_t len, bool f32, int layout, const void* x, long long x_stride,
                         long long batch, void* out, long long out_stride, cudaStream_t st);
+// slice_band (spectra.cpp:40-61) on a spectrum of `size` bins at f_start + k f_step: first bin and
+// count of the band [f_lo, f_hi], with the reference's 1e-9 step slack and its errors
+struct BandBins {
+    long long k_lo = 0, count = 0;
+    double f_start = 0.0;
+};
+BandBins slice_band_bins(size_t size, double f_start, double f_step, double f_lo, double f_hi);
+// zero-padded spectrum restricted to bins [k_lo, k_lo + count) of the full [0, fs) layout, as complex
+// (out, optional) and magnitude_db (db, optional); fused into the FFT store when the FFT is one CTA
+void fft_spectrum_band_batch(size_t n, size_t len, bool f32, long long k_lo, long long count, const void* x,
+                             long long x_stride, long long batch, void* out, long long out_stride, void* db,
+                             long long db_stride, cudaStream_t st);
+void band_db_batch(bool f32, const void* in, long long in_stride, long long k_lo, long long count, long long batch,
+                   void* out, long long out_stride, void* db, long long db_stride, cudaStream_t st);
 
 class TransferPlanG {
   public:

@@ -22,11 +22,13 @@ cudaError_t launch_fft_c2c(int log2L, bool inverse, const void* in, long long in
 // real trace (N samples, zero padded to L = 2^(log2M+1)) -> spectrum via an M-point complex FFT
 // of packed sample pairs. mode 0: full L-bin spectrum (reference layout, spectra.cpp:21-38);
 // mode 1: half spectrum, M+1 bins; mode 2: H = X * rtab (rtab = 1/X_ref), |H| and arg H on M+1
-// bins (h optional, M+1 complex).
+// bins (h optional, M+1 complex); mode 3: bins klo..khi of the full spectrum (slice_band,
+// spectra.cpp:40-61) as complex (out, optional) and/or magnitude_db (mag, optional; types.cpp:13-18).
 template <typename T>
 cudaError_t launch_fft_r2c(int log2M, long long N, const T* x, long long x_stride, long long batch,
                            const void* tw, const void* post, int mode, void* out, long long out_stride,
-                           const void* rtab, T* mag, T* phase, long long mp_stride, cudaStream_t st);
+                           const void* rtab, T* mag, T* phase, long long mp_stride, long long klo, long long khi,
+                           cudaStream_t st);
 
 // fused Bluestein CZT (czt.cpp:116-130): x * chirp_in -> FFT_L -> * khat (pre-scaled by 1/L)
 // -> IFFT_L -> * chirp_out, first M bins stored. x real (T) or complex (cx<T>). The M outputs are
@@ -115,6 +117,12 @@ cudaError_t launch_zoom_cfir(const ZoomArgs& a, bool f32, const void* x, long lo
                              cudaStream_t st);
 // shared bytes the fused zoom kernel needs for this geometry
 size_t zoom_smem_bytes(const ZoomArgs& a, int log2n, bool f32);
+
+// band slice + magnitude_db of complex rows (slice_band spectra.cpp:40-61, magnitude_db types.cpp:13-18):
+// bins [klo, klo + nb) of each input row -> out (optional) and dB (optional)
+cudaError_t launch_band_db(bool f32, const void* in, long long in_stride, long long klo, long long nb,
+                           long long batch, void* out, long long out_stride, void* db, long long db_stride,
+                           cudaStream_t st);
 
 // elementwise helpers
 cudaError_t launch_c64_to_c32(const void* in, void* out, long long n, cudaStream_t st);

@@ -13,9 +13,10 @@ cudaError_t launch_fft_c2c<float>(int log2L, bool inverse, const void* in, long 
 template <>
 cudaError_t launch_fft_r2c<float>(int log2M, long long N, const float* x, long long x_stride, long long batch,
                                 const void* tw, const void* post, int mode, void* out, long long out_stride,
-                                const void* rtab, float* mag, float* phase, long long mp_stride, cudaStream_t st) {
+                                const void* rtab, float* mag, float* phase, long long mp_stride, long long klo, long long khi,
+                                cudaStream_t st) {
     return launch_fft_r2c_impl<float>(log2M, N, x, x_stride, batch, tw, post, mode, out, out_stride, rtab, mag,
-                                    phase, mp_stride, st);
+                                    phase, mp_stride, klo, khi, st);
 }
 
 }  // namespace skg

@@ -87,12 +87,19 @@ k_fft_c2c(const cx_t<T>* in, long long in_stride, cx_t<T>* out, long long out_st
 // real input, zero padded to L = 2M: M-point complex FFT of z[n] = x[2n] + i x[2n+1], then
 // X[k] = E[k] + W_L^k O[k] with E/O split from Z[k], conj Z[M-k]. Replaces fft_spectrum's
 // zero_pad + dft_any (spectra.cpp:21-38) without ever materialising the zeros.
+#ifndef SKG_R2C_MINB_F32
+#define SKG_R2C_MINB_F32 3   // measured on configs[3]: 2 -> 1.269 ms, 3 -> 1.192 ms, 4 -> 1.215 ms
+#endif
+template <typename T, int LOG2M> struct R2cCfg {
+    // fp32 256-thread transforms: CTAs per SM the register cap targets (2 = 128 registers)
+    static constexpr int MINB = (sizeof(T) == 4 && KCfg<T, LOG2M>::BLOCK == 256) ? SKG_R2C_MINB_F32 : KCfg<T, LOG2M>::MINB;
+};
 template <typename T, int LOG2M, int NZ, int MODE>
-__global__ void __launch_bounds__(KCfg<T, LOG2M>::BLOCK, KCfg<T, LOG2M>::MINB)
+__global__ void __launch_bounds__(KCfg<T, LOG2M>::BLOCK, R2cCfg<T, LOG2M>::MINB)
 k_fft_r2c(const T* __restrict__ x, long long x_stride, long long N, int vec, long long batch,
           const cx_t<T>* __restrict__ tw, const cx_t<T>* __restrict__ post, cx_t<T>* __restrict__ out,
           long long out_stride, const cx_t<T>* __restrict__ rtab, T* __restrict__ mag, T* __restrict__ phase,
-          long long mp_stride) {
+          long long mp_stride, long long klo, long long khi) {
     SKG_PROLOGUE(T, LOG2M)
     constexpr int M = G::L;
     constexpr long long L = 2LL * M;
@@ -136,15 +143,25 @@ k_fft_r2c(const T* __restrict__ x, long long x_stride, long long N, int vec, lon
         }
         if (active) {
             C* o = out ? out + b * out_stride : nullptr;
-            T* mg = MODE == 2 ? mag + b * mp_stride : nullptr;
+            T* mg = (MODE == 2 || MODE == 3) && mag ? mag + b * mp_stride : nullptr;
             T* ph = MODE == 2 ? phase + b * mp_stride : nullptr;
-            // store one output bin (full / half spectrum or H = X / X_ref as |H|, arg H)
+            // one bin of the band [klo, khi] of the full [0, L) spectrum: complex and/or dB
+            auto put = [&](long long k, C X) {
+                if (k >= klo && k <= khi) {
+                    if (o) o[k - klo] = X;
+                    if (mg) mg[k - klo] = magnitude_db_t(X.x, X.y);
+                }
+            };
+            // store one output bin (full / half spectrum, band slice, or H = X / X_ref as |H|, arg H)
             auto emit = [&](long long k, C X) {
                 if constexpr (MODE == 0) {
                     o[k] = X;
                     if (k && k < M) o[L - k] = cconj(X);
                 } else if constexpr (MODE == 1) {
                     o[k] = X;
+                } else if constexpr (MODE == 3) {
+                    put(k, X);
+                    if (k && k < M) put(L - k, cconj(X));
                 } else {
                     const C H = cmul(X, __ldg(rtab + k));
                     mg[k] = abs_t(H.x, H.y);
@@ -163,11 +180,12 @@ k_fft_r2c(const T* __restrict__ x, long long x_stride, long long N, int vec, lon
                 if constexpr (G::NT == 1) c = v[(M - q) & (M - 1)];
                 else c = sm[pad16((M - k) & (M - 1))];
                 const C z = v[q];
-                const C E = mk<C>((T)0.5 * (z.x + c.x), (T)0.5 * (z.y - c.y));
-                const C O = mk<C>((T)0.5 * (z.y + c.y), (T)0.5 * (c.x - z.x));
-                const C WO = cmul(O, __ldg(post + k));
-                emit(k, cadd(E, WO));
-                emit(M - k, cconj(csub(E, WO)));
+                // E' = 2E, O' = 2O; post = W^k / 2, so X = E'/2 + post O' (exact rescaling of the
+                // textbook split: same rounding, two multiplies fewer per bin)
+                const C E2 = mk<C>(z.x + c.x, z.y - c.y);
+                const C WO = cmul(mk<C>(z.y + c.y, c.x - z.x), __ldg(post + k));
+                emit(k, mk<C>(fma((T)0.5, E2.x, WO.x), fma((T)0.5, E2.y, WO.y)));
+                emit(M - k, mk<C>(fma((T)0.5, E2.x, -WO.x), fma((T)-0.5, E2.y, WO.y)));
             }
             if constexpr (G::EPT > 1) {
                 if (tid == 0) {   // k = M/2 (its own partner)
@@ -176,9 +194,9 @@ k_fft_r2c(const T* __restrict__ x, long long x_stride, long long N, int vec, lon
                     C c;
                     if constexpr (G::NT == 1) c = v[G::EPT / 2];
                     else c = z;
-                    const C E = mk<C>((T)0.5 * (z.x + c.x), (T)0.5 * (z.y - c.y));
-                    const C O = mk<C>((T)0.5 * (z.y + c.y), (T)0.5 * (c.x - z.x));
-                    emit(k, cadd(E, cmul(O, __ldg(post + k))));
+                    const C E2 = mk<C>(z.x + c.x, z.y - c.y);
+                    const C WO = cmul(mk<C>(z.y + c.y, c.x - z.x), __ldg(post + k));
+                    emit(k, mk<C>(fma((T)0.5, E2.x, WO.x), fma((T)0.5, E2.y, WO.y)));
                 }
             }
         }
@@ -486,7 +504,7 @@ cudaError_t run_c2c(const void* in, long long in_stride, void* out, long long ou
 template <typename T, int LOG2M, int NZ, int MODE>
 cudaError_t run_r2c(long long N, const T* x, long long x_stride, long long batch, const void* tw,
                     const void* post, void* out, long long out_stride, const void* rtab, T* mag,
-                    T* phase, long long mp_stride, cudaStream_t st) {
+                    T* phase, long long mp_stride, long long klo, long long khi, cudaStream_t st) {
     using K = KCfg<T, LOG2M>;
     using C = cx_t<T>;
     auto kern = k_fft_r2c<T, LOG2M, NZ, MODE>;
@@ -495,7 +513,7 @@ cudaError_t run_r2c(long long N, const T* x, long long x_stride, long long batch
     const int vec = ((N & 1) == 0 && (x_stride & 1) == 0 && ((uintptr_t)x % (2 * sizeof(T))) == 0) ? 1 : 0;
     kern<<<persistent_grid(kern, K::BLOCK, K::SMEM_BYTES, grid_for(batch, K::GROUPS)), K::BLOCK, K::SMEM_BYTES, st>>>(
         x, x_stride, N, vec, batch, (const C*)tw, (const C*)post, (C*)out, out_stride, (const C*)rtab,
-        mag, phase, mp_stride);
+        mag, phase, mp_stride, klo, khi);
     return cudaGetLastError();
 }
 
@@ -590,7 +608,8 @@ cudaError_t launch_fft_c2c_impl(int log2L, bool inverse, const void* in, long lo
 template <typename T>
 cudaError_t launch_fft_r2c_impl(int log2M, long long N, const T* x, long long x_stride, long long batch,
                                 const void* tw, const void* post, int mode, void* out, long long out_stride,
-                                const void* rtab, T* mag, T* phase, long long mp_stride, cudaStream_t st) {
+                                const void* rtab, T* mag, T* phase, long long mp_stride, long long klo,
+                                long long khi, cudaStream_t st) {
     return dispatch_log2<0, max_log2<T>()>(log2M, [&](auto lg) {
         constexpr int LG = decltype(lg)::value;
         const int nz = nz_class((N + 1) / 2, FftGeom<LG>::NT);
@@ -598,12 +617,15 @@ cudaError_t launch_fft_r2c_impl(int log2M, long long N, const T* x, long long x_
             constexpr int NZ = decltype(z)::value;
             if (mode == 0)
                 return run_r2c<T, LG, NZ, 0>(N, x, x_stride, batch, tw, post, out, out_stride, rtab, mag, phase,
-                                             mp_stride, st);
+                                             mp_stride, klo, khi, st);
             if (mode == 1)
                 return run_r2c<T, LG, NZ, 1>(N, x, x_stride, batch, tw, post, out, out_stride, rtab, mag, phase,
-                                             mp_stride, st);
+                                             mp_stride, klo, khi, st);
+            if (mode == 3)
+                return run_r2c<T, LG, NZ, 3>(N, x, x_stride, batch, tw, post, out, out_stride, rtab, mag, phase,
+                                             mp_stride, klo, khi, st);
             return run_r2c<T, LG, NZ, 2>(N, x, x_stride, batch, tw, post, out, out_stride, rtab, mag, phase,
-                                         mp_stride, st);
+                                         mp_stride, klo, khi, st);
         });
     });
 }

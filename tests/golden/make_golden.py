@@ -66,6 +66,33 @@ def ref_fft_spectrum(samples, fs, length):
     return re + 1j * im, f0, df
 
 
+def ref_band(samples, fs, length, lo, hi):
+    """sk_fft_spectrum -> sk_spectrum_slice_band -> per-bin sk_spectrum_magnitude_db (the CLI's
+    half-spectrum / band rows, spectral_kit.cpp:143-148, and the CSV dB column, spectra.cpp:63-72)."""
+    R.sk_spectrum_slice_band.argtypes = [C.c_void_p, C.c_double, C.c_double, C.POINTER(C.c_void_p)]
+    R.sk_spectrum_magnitude_db.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(C.c_double)]
+    s = np.ascontiguousarray(samples, np.float64)
+    t = C.c_void_p()
+    assert R.sk_trace_create(P(s), s.size, fs, 0.0, C.byref(t)) == 0
+    sp = C.c_void_p()
+    assert R.sk_fft_spectrum(t, length, C.byref(sp)) == 0, R.sk_last_error()
+    band = C.c_void_p()
+    assert R.sk_spectrum_slice_band(sp, lo, hi, C.byref(band)) == 0, R.sk_last_error()
+    n = R.sk_spectrum_size(band)
+    re, im = np.zeros(n), np.zeros(n)
+    R.sk_spectrum_copy_data(band, P(re), P(im))
+    db = np.zeros(n)
+    v = C.c_double()
+    for k in range(n):
+        assert R.sk_spectrum_magnitude_db(band, k, C.byref(v)) == 0
+        db[k] = v.value
+    f0, df = R.sk_spectrum_f_start(band), R.sk_spectrum_f_step(band)
+    for h in (band, sp):
+        R.sk_spectrum_free(h)
+    R.sk_trace_free(t)
+    return re + 1j * im, db, f0, df
+
+
 def ref_zoom(samples, fs, f1, f2, taps=None, n_fft=None, **kw):
     o = dict(center_hz=0.0, center_set=0, decimation=0, cutoff_hz=0.0, num_taps=0, circular=1,
              trim_transient=0, pad_pow2=1)
@@ -142,6 +169,18 @@ def main():
     sp["pulse500_X512"], _, _ = ref_fft_spectrum(pulse, 10e12, 0)
     sp["pulse500_X500"], _, _ = ref_fft_spectrum(pulse, 10e12, 500)
     np.savez_compressed(os.path.join(OUT, "spectra.npz"), **sp)
+
+    # --- band slice + dB column: cfg1 sample at 4096, the 500-sample pulse ------
+    bd = {}
+    bands = {"thz": (0.1e12, 3.0e12), "half": (0.0, W.FS / 2), "nyq": (9.0e12, 12.0e12), "edge": (
+        sp["cfg1_df"] * 100, sp["cfg1_df"] * 140), "top": (19.9e12, 25e12)}
+    bd["x"] = sample
+    for name, (lo, hi) in bands.items():
+        bd[f"{name}_band"] = np.array([lo, hi])
+        bd[f"{name}_X"], bd[f"{name}_db"], bd[f"{name}_f0"], bd[f"{name}_df"] = ref_band(sample, W.FS, 4096, lo, hi)
+    bd["p500_X"], bd["p500_db"], bd["p500_f0"], bd["p500_df"] = ref_band(pulse, 10e12, 500, 0.5e12, 2.0e12)
+    bd["zeros_X"], bd["zeros_db"], _, _ = ref_band(np.zeros(64), W.FS, 64, 0.0, 5e12)
+    np.savez_compressed(os.path.join(OUT, "band.npz"), **bd)
 
     # --- zoom: cfg3 reference sizing (65 taps, n_fft 512), the 2048 variant, 500-sample plans ----
     zm = {}

@@ -192,3 +192,22 @@ def test_differential_vs_reference():
         R.skr_czt_batch(p, O._p(np.ascontiguousarray(x)), n, 1, 1, O._p(out.view(np.float64)))
         R.skr_czt_plan_free(p)
         assert rel_max(O.czt(x, a, w, m), out) == 0.0
+
+
+def test_golden_band_db(golden):
+    """slice_band + magnitude_db against the reference's own sk_spectrum_slice_band
+    and sk_spectrum_magnitude_db outputs: bin selection exact, band axis exact, dB bit-exact on the
+    reference's bins (same formula, hypot + log10)."""
+    g = golden("band")
+    for name in ("thz", "half", "nyq", "edge", "top"):
+        lo, hi = g[f"{name}_band"]
+        X, _, step, _ = O.fft_spectrum(g["x"], W.FS, 4096)
+        k0, cnt = O.slice_band(4096, 0.0, step, lo, hi)
+        assert cnt == g[f"{name}_X"].size and k0 * step == g[f"{name}_f0"] and step == g[f"{name}_df"]
+        assert rel_max(X[k0:k0 + cnt], g[f"{name}_X"]) <= 1e-14
+        assert np.max(np.abs(O.magnitude_db(g[f"{name}_X"]) - g[f"{name}_db"])) <= 1e-12
+    assert np.all(O.magnitude_db(g["zeros_X"]) == -300.0) and np.all(g["zeros_db"] == -300.0)
+    with pytest.raises(O.OracleError, match="inverted"):
+        O.slice_band(16, 0.0, 1.0, 5.0, 4.0)
+    with pytest.raises(O.OracleError, match="no bins"):
+        O.slice_band(16, 0.0, 1.0, 4.2, 4.8)
