@@ -76,6 +76,12 @@ SK_API size_t sk_trace_size(const sk_trace* t);
 SK_API double sk_trace_sample_rate(const sk_trace* t);
 SK_API double sk_trace_t0(const sk_trace* t);
 SK_API const double* sk_trace_samples(const sk_trace* t);
+/* CSV "time_s,amplitude" (ref spectralkit.h:133-134, signals.cpp:125-189): optional header row,
+ * median-step sample rate with a 1e-6 uniformity check, SK_ERR_PARSE with the line number for a
+ * malformed row, SK_ERR_FORMAT for < 2 samples / non-increasing / non-uniform time, SK_ERR_IO for
+ * unopenable files; "-" = stdin / stdout. Rows written as %.17g. */
+SK_API sk_status sk_trace_read_csv(const char* path, sk_trace** out);
+SK_API sk_status sk_trace_write_csv(const sk_trace* t, const char* path);
 
 /* Spectra (ref spectralkit.h:138-161, capi.cpp:412-481). */
 typedef struct sk_spectrum sk_spectrum;
@@ -98,6 +104,9 @@ SK_API sk_status sk_spectrum_magnitude_db(const sk_spectrum* s, size_t k, double
 SK_API sk_status sk_spectrum_copy_data(const sk_spectrum* s, double* re, double* im);
 SK_API sk_status sk_spectrum_slice_band(const sk_spectrum* s, double f_lo_hz, double f_hi_hz,
                                         sk_spectrum** out);
+/* CSV "frequency_hz,re,im,magnitude_db", %.17g rows (ref spectralkit.h:163-165, spectra.cpp:63-78);
+ * byte-identical to the reference's writer */
+SK_API sk_status sk_spectrum_write_csv(const sk_spectrum* s, const char* path);
 
 /* Zoom pipeline (ref spectralkit.h:170-195, capi.cpp:515-564). Same struct layout. */
 typedef struct sk_zoom_options {

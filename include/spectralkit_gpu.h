@@ -63,6 +63,23 @@ SK_API sk_status skg_band_db_batch(int precision, const void* d_in, size_t in_st
                                    size_t batch, void* d_bins, size_t bins_stride, void* d_db, size_t db_stride,
                                    void* stream);
 
+/* Batched trace ingest and spectrum output. skg_traces_read_csv runs
+ * sk_trace_read_csv's parser and checks (signals.cpp:125-170) on `count` files in parallel host
+ * threads (threads 0 = all cores); every file must hold n samples (else SK_ERR_FORMAT). The rows land
+ * in pinned staging and go to d_out (row stride out_stride elements; SKG_F32 rounds) with one copy
+ * on `stream`; per-file sample rate / t0 go to fs_out / t0_out (host, may be NULL). On failure the
+ * lowest-index failing file's status and message are reported and nothing is copied.
+ * skg_spectra_write_csv copies `count` rows of nbins complex bins from the device and writes one
+ * reference-format CSV per path in parallel (f_start_hz: per-row start frequency, NULL = 0). Both
+ * calls return after the transfer completed. */
+SK_API sk_status skg_traces_read_csv(const char* const* paths, size_t count, size_t n, int precision,
+                                     void* d_out, size_t out_stride, double* fs_out, double* t0_out,
+                                     int threads, void* stream);
+SK_API sk_status skg_spectra_write_csv(const char* const* paths, size_t count, int precision,
+                                       const void* d_bins, size_t bins_stride, size_t nbins,
+                                       const double* f_start_hz, double f_step_hz, int threads,
+                                       void* stream);
+
 /* Chirp-z transform plan (CztPlan, czt.cpp:85-137). */
 typedef struct skg_czt_plan skg_czt_plan;
 SK_API sk_status skg_czt_plan_create(size_t n, double a_re, double a_im, double w_re, double w_im,

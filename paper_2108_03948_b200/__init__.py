@@ -103,6 +103,12 @@ def _declare(L):
         "skg_band_bins": (st, [sz, C.c_double, C.c_double, C.c_double, C.c_double, C.POINTER(sz), C.POINTER(sz), dp]),
         "skg_fft_spectrum_band_batch": (st, [sz, sz, C.c_int, sz, sz, vp, sz, sz, vp, sz, vp, sz, vp]),
         "skg_band_db_batch": (st, [C.c_int, vp, sz, sz, sz, sz, vp, sz, vp, sz, vp]),
+        "sk_trace_read_csv": (st, [C.c_char_p, C.POINTER(vp)]),
+        "sk_trace_write_csv": (st, [vp, C.c_char_p]),
+        "sk_spectrum_write_csv": (st, [vp, C.c_char_p]),
+        "skg_traces_read_csv": (st, [C.POINTER(C.c_char_p), sz, sz, C.c_int, vp, sz, dp, dp, C.c_int, vp]),
+        "skg_spectra_write_csv": (st, [C.POINTER(C.c_char_p), sz, C.c_int, vp, sz, sz, dp, C.c_double, C.c_int,
+                                       vp]),
         "skg_czt_plan_create": (st, [sz, C.c_double, C.c_double, C.c_double, C.c_double, sz, C.c_int,
                                      C.POINTER(vp)]),
         "skg_czt_plan_free": (None, [vp]),
@@ -269,6 +275,64 @@ class Trace:
         if getattr(self, "_h", None):
             _rel("sk_trace_free", self._h)
             self._h = None
+
+
+def trace_read_csv(path):
+    """sk_trace_read_csv (signals.cpp:125-170): (samples, sample_rate_hz, t0_s)."""
+    h = vp()
+    _chk(lib().sk_trace_read_csv(os.fsencode(path), C.byref(h)))
+    L = lib()
+    try:
+        n = int(L.sk_trace_size(h))
+        x = np.ctypeslib.as_array(L.sk_trace_samples(h), shape=(n,)).copy() if n else np.empty(0)
+        return x, float(L.sk_trace_sample_rate(h)), float(L.sk_trace_t0(h))
+    finally:
+        L.sk_trace_free(h)
+
+
+def trace_write_csv(samples, sample_rate_hz, t0_s, path):
+    """sk_trace_write_csv (signals.cpp:178-189)."""
+    t = Trace(samples, sample_rate_hz, t0_s)
+    _chk(lib().sk_trace_write_csv(t.handle, os.fsencode(path)))
+
+
+def spectrum_write_csv(bins, f_start_hz, f_step_hz, path):
+    """sk_spectrum_write_csv (spectra.cpp:63-78): reference-format CSV of a spectrum."""
+    b = np.ascontiguousarray(bins, np.complex128)
+    re, im = np.ascontiguousarray(b.real), np.ascontiguousarray(b.imag)
+    h = vp()
+    _chk(lib().sk_spectrum_create(_p(re), _p(im), b.size, f_start_hz, f_step_hz, C.byref(h)))
+    try:
+        _chk(lib().sk_spectrum_write_csv(h, os.fsencode(path)))
+    finally:
+        lib().sk_spectrum_free(h)
+
+
+def _paths(paths):
+    arr = (C.c_char_p * len(paths))(*[os.fsencode(p) for p in paths])
+    return arr
+
+
+def traces_read_csv(paths, n, dtype=None, device="cuda", threads=0):
+    """Batched ingest (skg_traces_read_csv): every file parsed like sk_trace_read_csv, in parallel,
+    into one (len(paths), n) device tensor. Returns (traces, fs[], t0[])."""
+    torch = _torch()
+    dtype = dtype or torch.float64
+    out = torch.empty((len(paths), n), dtype=dtype, device=device)
+    fs, t0 = np.zeros(len(paths)), np.zeros(len(paths))
+    prec = SKG_F64 if dtype == torch.float64 else SKG_F32
+    _chk(lib().skg_traces_read_csv(_paths(paths), len(paths), n, prec, vp(out.data_ptr()), n, _p(fs), _p(t0),
+                                   threads, _stream()))
+    return out, fs, t0
+
+
+def spectra_write_csv(paths, bins, f_start_hz, f_step_hz, threads=0):
+    """Batched writer (skg_spectra_write_csv): one reference-format CSV per row of a complex device
+    tensor; f_start_hz scalar or per row."""
+    bins, b, s = _rows(bins)
+    f0 = np.ascontiguousarray(np.broadcast_to(np.asarray(f_start_hz, np.float64), (b,)))
+    _chk(lib().skg_spectra_write_csv(_paths(paths), b, _prec(bins), vp(bins.data_ptr()), s, bins.shape[-1], _p(f0),
+                                     f_step_hz, threads, _stream()))
 
 
 def _take_spectrum(h) -> Spectrum:

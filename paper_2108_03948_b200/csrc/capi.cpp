@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "host.hpp"
+#include "io.hpp"
 #include "spectralkit.h"
 #include "spectralkit_gpu.h"
 
@@ -57,6 +58,15 @@ template <typename Fn> sk_status guarded(Fn&& fn) {
     } catch (const std::invalid_argument& e) {
         g_err = e.what();
         return SK_ERR_INVALID_ARGUMENT;
+    } catch (const skg::ParseError& e) {   // capi.cpp:56-67 of the reference
+        g_err = e.what();
+        return SK_ERR_PARSE;
+    } catch (const skg::FormatError& e) {
+        g_err = e.what();
+        return SK_ERR_FORMAT;
+    } catch (const skg::IoError& e) {
+        g_err = e.what();
+        return SK_ERR_IO;
     } catch (const std::bad_alloc&) {
         g_err = "out of memory";
         return SK_ERR_INTERNAL;
@@ -359,6 +369,118 @@ size_t sk_trace_size(const sk_trace* t) { return t ? t->samples.size() : 0; }
 double sk_trace_sample_rate(const sk_trace* t) { return t ? t->fs : 0.0; }
 double sk_trace_t0(const sk_trace* t) { return t ? t->t0 : 0.0; }
 const double* sk_trace_samples(const sk_trace* t) { return t ? t->samples.data() : nullptr; }
+
+// trace / spectrum CSV files (signals.cpp:125-189, spectra.cpp:63-78; capi.cpp:391-408, 483-501)
+sk_status sk_trace_read_csv(const char* path, sk_trace** out) {
+    if (!path || !out) return bad_arg("sk_trace_read_csv: null argument");
+    return guarded([&] {
+        skg::HostTrace h = skg::read_trace_csv_file(path);
+        auto* t = new sk_trace;
+        t->samples = std::move(h.samples);
+        t->fs = h.fs;
+        t->t0 = h.t0;
+        *out = t;
+    });
+}
+
+sk_status sk_trace_write_csv(const sk_trace* t, const char* path) {
+    if (!t || !path) return bad_arg("sk_trace_write_csv: null argument");
+    return guarded([&] { skg::write_trace_csv_file(t->samples.data(), t->samples.size(), t->fs, t->t0, path); });
+}
+
+sk_status sk_spectrum_write_csv(const sk_spectrum* s, const char* path) {
+    if (!s || !path) return bad_arg("sk_spectrum_write_csv: null argument");
+    return guarded([&] {
+        skg::write_spectrum_csv_file(reinterpret_cast<const double*>(s->bins.data()), s->bins.size(), s->f_start,
+                                     s->f_step, path);
+    });
+}
+
+namespace {
+// grow-only pinned staging for the batched file paths (one batch in flight per process)
+std::mutex g_io_mu;
+void* g_io_pin = nullptr;
+size_t g_io_cap = 0;
+void* io_pinned(size_t bytes) {
+    if (bytes > g_io_cap) {
+        if (g_io_pin) cudaFreeHost(g_io_pin);
+        g_io_pin = nullptr;
+        g_io_cap = 0;
+        skg::check(cudaHostAlloc(&g_io_pin, bytes, cudaHostAllocDefault), "cudaHostAlloc");
+        g_io_cap = bytes;
+    }
+    return g_io_pin;
+}
+}  // namespace
+
+sk_status skg_traces_read_csv(const char* const* paths, size_t count, size_t n, int precision, void* d_out,
+                              size_t out_stride, double* fs_out, double* t0_out, int threads, void* stream) {
+    if (!paths || !d_out) return bad_arg("skg_traces_read_csv: null argument");
+    if (n == 0) return bad_arg("skg_traces_read_csv: n must be the per-trace sample count");
+    if (out_stride < n) return bad_arg("skg_traces_read_csv: row stride shorter than the trace");
+    for (size_t i = 0; i < count; ++i)
+        if (!paths[i]) return bad_arg("skg_traces_read_csv: null path");
+    return guarded([&] {
+        if (count == 0) return;
+        skg::require_device();
+        std::lock_guard<std::mutex> lk(g_io_mu);
+        const bool f32 = precision == SKG_F32;
+        const size_t es = f32 ? sizeof(float) : sizeof(double);
+        unsigned char* pin = static_cast<unsigned char*>(io_pinned(count * n * es));
+        skg::parallel_for(count, threads, [&](size_t i) {
+            skg::HostTrace h = skg::read_trace_csv_file(paths[i]);
+            if (h.samples.size() != n)
+                throw skg::FormatError(std::string(paths[i]) + ": expected " + std::to_string(n) + " samples, got " +
+                                       std::to_string(h.samples.size()));
+            if (f32) {
+                float* dst = reinterpret_cast<float*>(pin) + i * n;
+                for (size_t k = 0; k < n; ++k) dst[k] = (float)h.samples[k];
+            } else {
+                std::memcpy(reinterpret_cast<double*>(pin) + i * n, h.samples.data(), n * sizeof(double));
+            }
+            if (fs_out) fs_out[i] = h.fs;
+            if (t0_out) t0_out[i] = h.t0;
+        });
+        const cudaStream_t st = (cudaStream_t)stream;
+        skg::check(cudaMemcpy2DAsync(d_out, out_stride * es, pin, n * es, n * es, count, cudaMemcpyHostToDevice, st),
+                   "H2D");
+        skg::check(cudaStreamSynchronize(st), "sync");
+    });
+}
+
+sk_status skg_spectra_write_csv(const char* const* paths, size_t count, int precision, const void* d_bins,
+                                size_t bins_stride, size_t nbins, const double* f_start_hz, double f_step_hz,
+                                int threads, void* stream) {
+    if (!paths || !d_bins) return bad_arg("skg_spectra_write_csv: null argument");
+    if (bins_stride < nbins) return bad_arg("skg_spectra_write_csv: row stride shorter than the spectrum");
+    for (size_t i = 0; i < count; ++i)
+        if (!paths[i]) return bad_arg("skg_spectra_write_csv: null path");
+    return guarded([&] {
+        if (count == 0 || nbins == 0) return;
+        skg::require_device();
+        std::lock_guard<std::mutex> lk(g_io_mu);
+        const bool f32 = precision == SKG_F32;
+        const size_t cs = f32 ? 2 * sizeof(float) : 2 * sizeof(double);
+        unsigned char* pin = static_cast<unsigned char*>(io_pinned(count * nbins * cs));
+        const cudaStream_t st = (cudaStream_t)stream;
+        skg::check(cudaMemcpy2DAsync(pin, nbins * cs, d_bins, bins_stride * cs, nbins * cs, count,
+                                     cudaMemcpyDeviceToHost, st),
+                   "D2H");
+        skg::check(cudaStreamSynchronize(st), "sync");
+        skg::parallel_for(count, threads, [&](size_t i) {
+            const double f0 = f_start_hz ? f_start_hz[i] : 0.0;
+            if (f32) {   // the reference's writer prints doubles: promote
+                std::vector<double> b(2 * nbins);
+                const float* src = reinterpret_cast<const float*>(pin) + 2 * i * nbins;
+                for (size_t k = 0; k < 2 * nbins; ++k) b[k] = src[k];
+                skg::write_spectrum_csv_file(b.data(), nbins, f0, f_step_hz, paths[i]);
+            } else {
+                skg::write_spectrum_csv_file(reinterpret_cast<const double*>(pin) + 2 * i * nbins, nbins, f0,
+                                             f_step_hz, paths[i]);
+            }
+        });
+    });
+}
 
 // ---- spectra -----------------------------------------------------------------------------------
 sk_status sk_fft_spectrum(const sk_trace* t, size_t transform_len, sk_spectrum** out) {

@@ -1,0 +1,210 @@
+// io.cpp — trace ingest / spectrum serialisation restated from the reference (signals.cpp:100-189,
+// spectra.cpp:63-78) for the batched path: whole-file reads, std::from_chars parsing (the
+// reference's own parser), std::to_chars(general, 17) formatting (specified as printf's %.17g, the
+// reference's snprintf format, so the bytes are identical), files processed in parallel.
+#include "io.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <charconv>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <string_view>
+#include <thread>
+
+namespace skg {
+
+namespace {
+
+bool parse_double(std::string_view field, double& out) {   // signals.cpp:102-112
+    while (!field.empty() && (field.front() == ' ' || field.front() == '\t')) field.remove_prefix(1);
+    while (!field.empty() && (field.back() == ' ' || field.back() == '\t')) field.remove_suffix(1);
+    if (field.empty()) return false;
+    const char* last = field.data() + field.size();
+    auto [ptr, ec] = std::from_chars(field.data(), last, out);
+    return ec == std::errc{} && ptr == last;
+}
+
+bool parse_row(std::string_view line, double& t, double& x) {   // signals.cpp:114-120
+    const size_t comma = line.find(',');
+    if (comma == std::string_view::npos) return false;
+    if (line.find(',', comma + 1) != std::string_view::npos) return false;
+    return parse_double(line.substr(0, comma), t) && parse_double(line.substr(comma + 1), x);
+}
+
+std::string slurp(FILE* f) {
+    std::string s;
+    char buf[1 << 16];
+    size_t r;
+    while ((r = fread(buf, 1, sizeof buf, f)) > 0) s.append(buf, r);
+    return s;
+}
+
+// %.17g into p (returns the end)
+char* put_g17(char* p, char* end, double v) {
+    auto r = std::to_chars(p, end, v, std::chars_format::general, 17);
+    return r.ptr;
+}
+
+double magnitude_db(double re, double im) {   // types.cpp:13-18 (std::abs of std::complex = hypot)
+    const double mag = std::hypot(re, im);
+    return mag > 1e-15 ? 20.0 * std::log10(mag) : -300.0;
+}
+
+FILE* open_out(const std::string& path, const char* what) {
+    if (path == "-") return stdout;
+    FILE* f = fopen(path.c_str(), "wb");
+    if (!f) throw IoError(std::string("cannot open ") + what + " file for writing: " + path);
+    return f;
+}
+
+void finish_out(FILE* f, bool ok, const char* what) {
+    if (f != stdout) ok = (fclose(f) == 0) && ok;
+    else ok = (fflush(f) == 0) && ok;
+    if (!ok) throw IoError(std::string(what) + " csv: write failed");
+}
+
+}  // namespace
+
+HostTrace parse_trace_csv(const char* data, size_t len, const std::string& origin) {
+    std::vector<double> times, values;
+    size_t line_no = 0;
+    bool first_content = true;
+    size_t pos = 0;
+    while (pos < len) {   // std::getline: every '\n'-terminated line, plus a non-empty tail
+        const char* nl = static_cast<const char*>(memchr(data + pos, '\n', len - pos));
+        const size_t end = nl ? (size_t)(nl - data) : len;
+        std::string_view line(data + pos, end - pos);
+        pos = end + 1;
+        ++line_no;
+        if (!line.empty() && line.back() == '\r') line.remove_suffix(1);
+        if (line.find_first_not_of(" \t") == std::string_view::npos) continue;
+        double t = 0.0, x = 0.0;
+        if (!parse_row(line, t, x)) {
+            if (first_content) {   // optional header
+                first_content = false;
+                continue;
+            }
+            throw ParseError(origin + ": malformed row at line " + std::to_string(line_no), line_no);
+        }
+        first_content = false;
+        times.push_back(t);
+        values.push_back(x);
+    }
+    if (times.size() < 2) throw FormatError(origin + ": need at least 2 samples to infer the sample rate");
+    std::vector<double> steps(times.size() - 1);
+    for (size_t i = 0; i + 1 < times.size(); ++i) steps[i] = times[i + 1] - times[i];
+    std::vector<double> sorted = steps;
+    std::nth_element(sorted.begin(), sorted.begin() + sorted.size() / 2, sorted.end());
+    const double median = sorted[sorted.size() / 2];
+    if (!(median > 0.0)) throw FormatError(origin + ": time column is not strictly increasing");
+    for (size_t i = 0; i < steps.size(); ++i)
+        if (std::abs(steps[i] - median) > 1e-6 * median)
+            throw FormatError(origin + ": non-uniform time step between rows " + std::to_string(i + 1) + " and " +
+                              std::to_string(i + 2) + " (got " + std::to_string(steps[i]) + " s, expected " +
+                              std::to_string(median) + " s)");
+    HostTrace tr;
+    tr.samples = std::move(values);
+    tr.fs = 1.0 / median;
+    tr.t0 = times.front();
+    // validate_trace (types.cpp:20-27)
+    if (!(tr.fs > 0.0) || !std::isfinite(tr.fs))
+        throw std::invalid_argument("trace: sample rate must be positive and finite");
+    for (double v : tr.samples)
+        if (!std::isfinite(v)) throw std::invalid_argument("trace: non-finite sample");
+    if (!std::isfinite(tr.t0)) throw std::invalid_argument("trace: non-finite start time");
+    return tr;
+}
+
+HostTrace read_trace_csv_file(const std::string& path) {
+    if (path == "-") {
+        const std::string s = slurp(stdin);
+        return parse_trace_csv(s.data(), s.size(), "stdin");
+    }
+    FILE* f = fopen(path.c_str(), "rb");
+    if (!f) throw IoError("cannot open trace file: " + path);
+    const std::string s = slurp(f);
+    fclose(f);
+    return parse_trace_csv(s.data(), s.size(), path);
+}
+
+void write_trace_csv_file(const double* samples, size_t n, double fs, double t0, const std::string& path) {
+    FILE* f = open_out(path, "trace");
+    // validate_trace runs inside write_trace_csv, after the file was opened (signals.cpp:178-195)
+    auto invalid = [&](const char* msg) {
+        if (f != stdout) fclose(f);
+        throw std::invalid_argument(msg);
+    };
+    if (n == 0) invalid("trace: no samples");
+    if (!(fs > 0.0) || !std::isfinite(fs)) invalid("trace: sample rate must be positive and finite");
+    for (size_t i = 0; i < n; ++i)
+        if (!std::isfinite(samples[i])) invalid("trace: non-finite sample");
+    if (!std::isfinite(t0)) invalid("trace: non-finite start time");
+    std::string out = "time_s,amplitude\n";
+    out.reserve(out.size() + n * 50);
+    const double dt = 1.0 / fs;
+    char buf[96];
+    for (size_t i = 0; i < n; ++i) {
+        char* p = put_g17(buf, buf + sizeof buf, t0 + static_cast<double>(i) * dt);
+        *p++ = ',';
+        p = put_g17(p, buf + sizeof buf, samples[i]);
+        *p++ = '\n';
+        out.append(buf, p - buf);
+    }
+    const bool ok = fwrite(out.data(), 1, out.size(), f) == out.size();
+    finish_out(f, ok, "trace");
+}
+
+std::string format_spectrum_csv(const double* b, size_t n, double f_start, double f_step) {
+    std::string out = "frequency_hz,re,im,magnitude_db\n";
+    out.reserve(out.size() + n * 100);
+    char buf[160];
+    for (size_t k = 0; k < n; ++k) {
+        const double re = b[2 * k], im = b[2 * k + 1];
+        char* e = buf + sizeof buf;
+        char* p = put_g17(buf, e, f_start + static_cast<double>(k) * f_step);   // Spectrum::frequency
+        *p++ = ',';
+        p = put_g17(p, e, re);
+        *p++ = ',';
+        p = put_g17(p, e, im);
+        *p++ = ',';
+        p = put_g17(p, e, magnitude_db(re, im));
+        *p++ = '\n';
+        out.append(buf, p - buf);
+    }
+    return out;
+}
+
+void write_spectrum_csv_file(const double* b, size_t n, double f_start, double f_step, const std::string& path) {
+    FILE* f = open_out(path, "spectrum");
+    const std::string out = format_spectrum_csv(b, n, f_start, f_step);
+    const bool ok = fwrite(out.data(), 1, out.size(), f) == out.size();
+    finish_out(f, ok, "spectrum");
+}
+
+void parallel_for(size_t count, int threads, const std::function<void(size_t)>& fn) {
+    if (count == 0) return;
+    size_t nt = threads > 0 ? (size_t)threads : std::max(1u, std::thread::hardware_concurrency());
+    nt = std::min(nt, count);
+    std::vector<std::exception_ptr> err(count);
+    std::atomic<size_t> next{0};
+    auto work = [&] {
+        for (size_t i; (i = next.fetch_add(1)) < count;) {
+            try {
+                fn(i);
+            } catch (...) {
+                err[i] = std::current_exception();
+            }
+        }
+    };
+    std::vector<std::thread> pool;
+    for (size_t t = 1; t < nt; ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+    for (auto& e : err)
+        if (e) std::rethrow_exception(e);
+}
+
+}  // namespace skg

@@ -93,6 +93,69 @@ def ref_band(samples, fs, length, lo, hi):
     return re + 1j * im, db, f0, df
 
 
+CSV_CASES = {
+    # name: file body (bytes) — read through sk_trace_read_csv (signals.cpp:125-170)
+    "crlf_blank_ws": b"\r\n  0.0 ,\t1.5\r\n\r\n1e-13, -2.25 \r\n 2e-13,3\r\n   \r\n3e-13,4.5e-3\r\n",
+    "header_notrail": b"time_s,amplitude\n0,1\n0.5,2\n1.0,3\n1.5,4",
+    "jitter_ok": b"0,1\n1.0000001,2\n2,3\n3.0000002,4\n4,5\n",
+    "malformed": b"t,x\n0,1\n1,2\n\n1.5;2\n2,3\n",
+    "three_cols": b"t,x\n0,1,2\n",
+    "bad_number": b"0,1\n1,2x\n",
+    "nonuniform": b"0,1\n1,2\n2,3\n3.5,4\n4.5,5\n",
+    "decreasing": b"3,1\n2,2\n1,3\n",
+    "one_sample": b"time_s,amplitude\n0,1\n",
+    "header_only": b"time_s,amplitude\n",
+    "empty": b"",
+    "nan_sample": b"0,1\n1,nan\n2,3\n",
+    "plus_sign": b"0,+1\n1,2\n",
+    "two_headers": b"a,b\nc,d\n0,1\n",
+}
+
+
+def ref_trace_read_csv(path):
+    R.sk_trace_read_csv.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+    R.sk_trace_size.restype = C.c_size_t
+    R.sk_trace_size.argtypes = [C.c_void_p]
+    R.sk_trace_sample_rate.restype = C.c_double
+    R.sk_trace_sample_rate.argtypes = [C.c_void_p]
+    R.sk_trace_t0.restype = C.c_double
+    R.sk_trace_t0.argtypes = [C.c_void_p]
+    R.sk_trace_samples.restype = C.POINTER(C.c_double)
+    R.sk_trace_samples.argtypes = [C.c_void_p]
+    t = C.c_void_p()
+    rc = R.sk_trace_read_csv(path.encode(), C.byref(t))
+    if rc != 0:
+        return rc, R.sk_last_error().decode(), None, 0.0, 0.0
+    n = R.sk_trace_size(t)
+    x = np.array([R.sk_trace_samples(t)[i] for i in range(n)])
+    fs, t0 = R.sk_trace_sample_rate(t), R.sk_trace_t0(t)
+    R.sk_trace_free(t)
+    return 0, "", x, fs, t0
+
+
+def ref_write_csv(kind, path, data, a, b):
+    """sk_trace_write_csv (kind 'trace': data samples, a fs, b t0) or sk_spectrum_write_csv
+    (kind 'spectrum': data complex bins, a f_start, b f_step); returns the file bytes"""
+    if kind == "trace":
+        s = np.ascontiguousarray(data, np.float64)
+        h = C.c_void_p()
+        assert R.sk_trace_create(P(s), s.size, a, b, C.byref(h)) == 0
+        R.sk_trace_write_csv.argtypes = [C.c_void_p, C.c_char_p]
+        assert R.sk_trace_write_csv(h, path.encode()) == 0
+        R.sk_trace_free(h)
+    else:
+        re, im = np.ascontiguousarray(data.real), np.ascontiguousarray(data.imag)
+        h = C.c_void_p()
+        R.sk_spectrum_create.argtypes = [oracle.dp, oracle.dp, C.c_size_t, C.c_double, C.c_double,
+                                         C.POINTER(C.c_void_p)]
+        assert R.sk_spectrum_create(P(re), P(im), re.size, a, b, C.byref(h)) == 0
+        R.sk_spectrum_write_csv.argtypes = [C.c_void_p, C.c_char_p]
+        assert R.sk_spectrum_write_csv(h, path.encode()) == 0
+        R.sk_spectrum_free(h)
+    with open(path, "rb") as f:
+        return f.read()
+
+
 def ref_zoom(samples, fs, f1, f2, taps=None, n_fft=None, **kw):
     o = dict(center_hz=0.0, center_set=0, decimation=0, cutoff_hz=0.0, num_taps=0, circular=1,
              trim_transient=0, pad_pow2=1)
@@ -181,6 +244,37 @@ def main():
     bd["p500_X"], bd["p500_db"], bd["p500_f0"], bd["p500_df"] = ref_band(pulse, 10e12, 500, 0.5e12, 2.0e12)
     bd["zeros_X"], bd["zeros_db"], _, _ = ref_band(np.zeros(64), W.FS, 64, 0.0, 5e12)
     np.savez_compressed(os.path.join(OUT, "band.npz"), **bd)
+
+    # --- CSV ingest / writers: reference parse results and file bytes --------
+    import tempfile
+    cv = {}
+    with tempfile.TemporaryDirectory() as td:
+        for name, body in CSV_CASES.items():
+            path = os.path.join(td, name + ".csv")
+            with open(path, "wb") as f:
+                f.write(body)
+            rc, msg, x, fs, t0 = ref_trace_read_csv(path)
+            cv[f"in_{name}"] = np.frombuffer(body, np.uint8)
+            cv[f"rc_{name}"] = rc
+            cv[f"msg_{name}"] = msg.replace(path, "<PATH>")
+            if rc == 0:
+                cv[f"x_{name}"], cv[f"fs_{name}"], cv[f"t0_{name}"] = x, fs, t0
+        rc, msg, _, _, _ = ref_trace_read_csv(os.path.join(td, "missing.csv"))
+        cv["rc_missing"], cv["msg_missing"] = rc, msg.replace(td, "<DIR>")
+        tr = sample[:300]
+        cv["w_trace_x"] = tr
+        cv["w_trace"] = np.frombuffer(ref_write_csv("trace", os.path.join(td, "t.csv"), tr, W.FS, 1.25e-12), np.uint8)
+        cv["w_spec_X"], cv["w_spec_f0"], cv["w_spec_df"] = bd["thz_X"], bd["thz_f0"], bd["thz_df"]
+        cv["w_spec"] = np.frombuffer(ref_write_csv("spectrum", os.path.join(td, "s.csv"), bd["thz_X"], bd["thz_f0"],
+                                                   bd["thz_df"]), np.uint8)
+        odd = np.array([0.0, -0.0 + 1e-300j, 1e-16, -1.0 - 0.0j, 3.14159e200 + 1e-320j, 2.5e-8 - 7e8j, 0.1 + 0.2j])
+        cv["w_odd_X"] = odd
+        cv["w_odd"] = np.frombuffer(ref_write_csv("spectrum", os.path.join(td, "o.csv"), odd, -5.0, 1.0 / 3.0),
+                                    np.uint8)
+        rt_path = os.path.join(td, "t.csv")   # the written trace read back by the reference
+        rc, _, x, fs, t0 = ref_trace_read_csv(rt_path)
+        cv["rt_x"], cv["rt_fs"], cv["rt_t0"] = x, fs, t0
+    np.savez_compressed(os.path.join(OUT, "csv.npz"), **cv)
 
     # --- zoom: cfg3 reference sizing (65 taps, n_fft 512), the 2048 variant, 500-sample plans ----
     zm = {}
