@@ -400,6 +400,10 @@ def bench_extras(args, sk, W, dev, world, pk):
                               "hbm_gbs": hc["bytes"] * cube.shape[0] / ks / 1e9,
                               "hbm_frac": hc["bytes"] * cube.shape[0] / ks / 1e9 / pk["hbm_gbs"]}
     del cd, mag, ph
+    # SURVEY §8f rows 1-2, files -> files: 1024 cfg2 traces (N=1024 fp64) as reference-format CSV
+    # (written once, untimed); a step = batched ingest -> fused band FFT 4096 (0.1-3 THz) -> batched
+    # reference-format CSV writer. Host wall clock (file I/O and parsing are the work here).
+    res["csv_pipeline_f64"] = bench_csv_pipeline(args, sk, W, dev)
     # cfg1 latency: one pair, fp64, FFT 4096 + H (device-resident) and through the C ABI (host)
     r1, s1 = W.cfg1_pair()
     tp1 = sk.TransferPlanGPU(r1, 4096, sk.SKG_F64)
@@ -415,6 +419,61 @@ def bench_extras(args, sk, W, dev, world, pk):
     res["cfg1_pair_f64"] = {"device_us_per_pair_H": float(np.median(per)) * 1e6,
                             "c_abi_us_per_fft_spectrum": float(np.median(calls)) * 1e6,
                             "c_abi_us_per_fft_spectrum_max": float(np.max(calls)) * 1e6}
+    return res
+
+
+def bench_csv_pipeline(args, sk, W, dev, nfiles=1024):
+    import tempfile
+
+    import torch
+    x = W.cfg2_batch(nfiles // 2, 1024)
+    with tempfile.TemporaryDirectory() as td:
+        ins = [os.path.join(td, f"t{i:05d}.csv") for i in range(nfiles)]
+        outs = [os.path.join(td, f"s{i:05d}.csv") for i in range(nfiles)]
+        for p, r in zip(ins, x):
+            sk.trace_write_csv(r, W.FS, 0.0, p)
+
+        def step():
+            d, fs, _ = sk.traces_read_csv(ins, 1024, device=dev)
+            bins, _, f0, df = sk.fft_spectrum_band_batch(d, fs[0], 0.1e12, 3.0e12, 4096, db=False)
+            sk.spectra_write_csv(outs, bins, f0, df)
+            return bins.shape[1]
+
+        nb = step()
+        ts = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            step()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        out_bytes = sum(os.path.getsize(p) for p in outs)
+        in_bytes = sum(os.path.getsize(p) for p in ins)
+        res = {"files_per_s": nfiles / float(np.median(ts)), "ms_per_step": float(np.median(ts)) * 1e3,
+               "bins_per_file": nb, "csv_in_mb": in_bytes / 1e6, "csv_out_mb": out_bytes / 1e6,
+               "host_threads": os.cpu_count()}
+        if not args.no_cpu:
+            try:
+                import oracle as O
+                from concurrent.futures import ThreadPoolExecutor
+                if O.ref() is not None:
+                    refo = [p + ".ref" for p in outs]
+                    with ThreadPoolExecutor(os.cpu_count()) as ex:
+                        t0 = time.perf_counter()
+                        list(ex.map(lambda i: O.ref_csv_chain(ins[i], refo[i], 4096, 0.1e12, 3.0e12), range(nfiles)))
+                        tr = time.perf_counter() - t0
+                    worst = 0.0
+                    for a, b in zip(outs[:16], refo[:16]):   # parsed back: bins of the GPU path vs the reference
+                        ga, gb = np.loadtxt(a, delimiter=",", skiprows=1), np.loadtxt(b, delimiter=",", skiprows=1)
+                        za, zb = ga[:, 1] + 1j * ga[:, 2], gb[:, 1] + 1j * gb[:, 2]
+                        worst = max(worst, float(np.max(np.abs(za - zb)) / np.max(np.abs(zb))))
+                        assert np.array_equal(ga[:, 0], gb[:, 0])
+                    res["reference_files_per_s"] = nfiles / tr
+                    res["reference_kind"] = ("compiled reference: sk_trace_read_csv -> sk_fft_spectrum -> "
+                                             f"sk_spectrum_slice_band -> sk_spectrum_write_csv, {os.cpu_count()} threads")
+                    res["parity_max_rel_vs_reference"] = worst
+            except Exception as e:   # the reference arm is a report, not a gate
+                res["reference_error"] = str(e)[:200]
     return res
 
 

@@ -144,6 +144,28 @@ def ref():
     return _ref
 
 
+def ref_csv_chain(in_path, out_path, transform_len, f_lo, f_hi):
+    """The reference's own file-to-file chain for one trace (the CLI `transform` path,
+    spectral_kit.cpp:109-186): sk_trace_read_csv -> sk_fft_spectrum -> sk_spectrum_slice_band ->
+    sk_spectrum_write_csv. Test / cpu_baseline infrastructure only."""
+    R = ref()
+    if not getattr(R, "_csv_sigs", False):
+        R.sk_trace_read_csv.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        R.sk_spectrum_slice_band.argtypes = [C.c_void_p, C.c_double, C.c_double, C.POINTER(C.c_void_p)]
+        R.sk_spectrum_write_csv.argtypes = [C.c_void_p, C.c_char_p]
+        R._csv_sigs = True
+    t, s, b = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    rc = R.sk_trace_read_csv(os.fsencode(in_path), C.byref(t))
+    rc = rc or R.sk_fft_spectrum(t, transform_len, C.byref(s))
+    rc = rc or R.sk_spectrum_slice_band(s, f_lo, f_hi, C.byref(b))
+    rc = rc or R.sk_spectrum_write_csv(b, os.fsencode(out_path))
+    for h, fr in ((b, R.sk_spectrum_free), (s, R.sk_spectrum_free), (t, R.sk_trace_free)):
+        if h.value:
+            fr(h)
+    if rc:
+        raise OracleError(R.sk_last_error().decode())
+
+
 class OracleError(ValueError):
     pass
 

@@ -14,11 +14,11 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 
-def _write_traces(tmp_path, x, fs=W.FS):
+def _write_traces(tmp_path, x, fs=W.FS, t0_step=1e-12):
     paths = []
     for i, r in enumerate(x):
         p = str(tmp_path / f"trace_{i:04d}.csv")
-        sk.trace_write_csv(r, fs, 1e-12 * i, p)
+        sk.trace_write_csv(r, fs, t0_step * i, p)
         paths.append(p)
     return paths
 
@@ -56,8 +56,11 @@ def test_pipeline_files_to_files(tmp_path):
     drop-in chain (sk_trace_read_csv, sk_fft_spectrum, sk_spectrum_slice_band, sk_spectrum_write_csv):
     byte-identical output files."""
     x = W.sample_traces(16, 1024)
-    paths = _write_traces(tmp_path, x)
+    # one time axis for the batch: the parsed rate is 1 / median step of the %.17g-printed times, so
+    # files with different t0 can differ in the last bit of fs (and of the frequency column)
+    paths = _write_traces(tmp_path, x, t0_step=0.0)
     dev, fs, _ = sk.traces_read_csv(paths, 1024)
+    assert np.all(fs == fs[0])
     bins, _, f0, df = sk.fft_spectrum_band_batch(dev, fs[0], 0.1e12, 3.0e12, 4096, db=False)
     outs = [str(tmp_path / f"spec_{i:04d}.csv") for i in range(16)]
     sk.spectra_write_csv(outs, bins, f0, df, threads=3)
