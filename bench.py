@@ -404,6 +404,9 @@ def bench_extras(args, sk, W, dev, world, pk):
     # (written once, untimed); a step = batched ingest -> fused band FFT 4096 (0.1-3 THz) -> batched
     # reference-format CSV writer. Host wall clock (file I/O and parsing are the work here).
     res["csv_pipeline_f64"] = bench_csv_pipeline(args, sk, W, dev)
+    # the two-tone resolvability sweep as a batched caller (THz scale: fs 20 THz,
+    # n 1024, band 0.1-3 THz, m 2048 -> padded FFT 14124 via Bluestein, 999 separations)
+    res["resolvability_scan_thz"] = bench_scan(args, sk, W)
     # cfg1 latency: one pair, fp64, FFT 4096 + H (device-resident) and through the C ABI (host)
     r1, s1 = W.cfg1_pair()
     tp1 = sk.TransferPlanGPU(r1, 4096, sk.SKG_F64)
@@ -474,6 +477,43 @@ def bench_csv_pipeline(args, sk, W, dev, nfiles=1024):
                     res["parity_max_rel_vs_reference"] = worst
             except Exception as e:   # the reference arm is a report, not a gate
                 res["reference_error"] = str(e)[:200]
+    return res
+
+
+def bench_scan(args, sk, W):
+    import torch
+    cfg = dict(W.SCAN_CASES["thz"], center_hz=1.5e12, sep_start_hz=1e9, sep_stop_hz=500e9, sep_step_hz=0.5e9)
+    got = sk.resolvability_scan(**cfg)
+    ts = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        got = sk.resolvability_scan(**cfg)
+        ts.append(time.perf_counter() - t0)
+    S = got["separations_hz"].size
+    res = {"separations": S, "fft_len": got["fft_len"], "separations_per_s": S / float(np.median(ts)),
+           "ms_per_sweep": float(np.median(ts)) * 1e3, "min_resolved_fft_hz": got["min_resolved_fft_hz"],
+           "min_resolved_czt_hz": got["min_resolved_czt_hz"]}
+    if not args.no_cpu:
+        try:
+            import ctypes as C
+
+            import oracle as O
+            R = O.ref()
+            if R is not None:   # the reference's own sweep (single thread, as it runs) on a bounded subset
+                sub = dict(cfg, sep_stop_hz=cfg["sep_start_hz"] + 19 * cfg["sep_step_hz"])
+                c = sk.scan_config(**sub)
+                R.sk_resolvability_scan.argtypes = [C.POINTER(sk.SkScanConfig), C.POINTER(C.c_void_p)]
+                R.sk_resolvability_curve_free.argtypes = [C.c_void_p]
+                h = C.c_void_p()
+                t0 = time.perf_counter()
+                assert R.sk_resolvability_scan(C.byref(c), C.byref(h)) == 0
+                tr = time.perf_counter() - t0
+                R.sk_resolvability_curve_free(h)
+                res["reference_separations_per_s"] = 20 / tr
+                res["reference_kind"] = "compiled reference sk_resolvability_scan, 1 thread, 20 separations"
+        except Exception as e:
+            res["reference_error"] = str(e)[:200]
     return res
 
 

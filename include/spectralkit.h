@@ -108,6 +108,45 @@ SK_API sk_status sk_spectrum_slice_band(const sk_spectrum* s, double f_lo_hz, do
  * byte-identical to the reference's writer */
 SK_API sk_status sk_spectrum_write_csv(const sk_spectrum* s, const char* path);
 
+/* Two-tone analysis (ref spectralkit.h:197-243, analysis.cpp:30-195). The resolvability sweep runs
+ * every separation's padded-FFT route and band-CZT route as two batched GPU launches; the valley
+ * test (dip_metric) runs on host threads. SK_ERR_INSUFFICIENT_RESOLUTION from sk_dip_metric_compute
+ * when fewer than 3 bins lie between the tones. */
+typedef struct sk_dip_metric {
+    int resolved;
+    double dip_db;
+    double f_peak_a_hz;
+    double peak_a_db;
+    double f_peak_b_hz;
+    double peak_b_db;
+    double f_valley_hz;
+    double valley_db;
+} sk_dip_metric;
+SK_API sk_status sk_dip_metric_compute(const sk_spectrum* s, double f_a_hz, double f_b_hz,
+                                       sk_dip_metric* out);
+typedef struct sk_scan_config {
+    double sample_rate_hz;
+    size_t n;
+    double f1_hz;
+    double f2_hz;
+    size_t m;
+    double center_hz; /* 0 = band midpoint */
+    double sep_start_hz;
+    double sep_stop_hz;
+    double sep_step_hz;
+} sk_scan_config;
+SK_API void sk_scan_config_defaults(sk_scan_config* cfg);
+typedef struct sk_resolvability_curve sk_resolvability_curve;
+SK_API sk_status sk_resolvability_scan(const sk_scan_config* cfg, sk_resolvability_curve** out);
+SK_API void sk_resolvability_curve_free(sk_resolvability_curve* c);
+SK_API size_t sk_resolvability_curve_size(const sk_resolvability_curve* c);
+SK_API sk_status sk_resolvability_curve_point(const sk_resolvability_curve* c, size_t i,
+                                              double* separation_hz, sk_dip_metric* fft_m,
+                                              sk_dip_metric* czt_m);
+/* NaN when no separation resolved on that route */
+SK_API double sk_resolvability_min_fft(const sk_resolvability_curve* c);
+SK_API double sk_resolvability_min_czt(const sk_resolvability_curve* c);
+
 /* Zoom pipeline (ref spectralkit.h:170-195, capi.cpp:515-564). Same struct layout. */
 typedef struct sk_zoom_options {
     double center_hz;     /* used only when center_set */

@@ -80,6 +80,9 @@ SK_API sk_status skg_spectra_write_csv(const char* const* paths, size_t count, i
                                        const double* f_start_hz, double f_step_hz, int threads,
                                        void* stream);
 
+/* padded full-range transform length of a resolvability curve (ResolvabilityCurve::fft_len) */
+SK_API size_t skg_resolvability_fft_len(const sk_resolvability_curve* c);
+
 /* Chirp-z transform plan (CztPlan, czt.cpp:85-137). */
 typedef struct skg_czt_plan skg_czt_plan;
 SK_API sk_status skg_czt_plan_create(size_t n, double a_re, double a_im, double w_re, double w_im,

@@ -43,6 +43,23 @@ class SkError(RuntimeError):
         self.message = message
 
 
+class SkDipMetric(C.Structure):
+    """sk_dip_metric (spectralkit.h two-tone analysis; analysis.hpp:15-24)."""
+    _fields_ = [("resolved", C.c_int), ("dip_db", C.c_double), ("f_peak_a_hz", C.c_double),
+                ("peak_a_db", C.c_double), ("f_peak_b_hz", C.c_double), ("peak_b_db", C.c_double),
+                ("f_valley_hz", C.c_double), ("valley_db", C.c_double)]
+
+    def astuple(self):
+        return tuple(float(getattr(self, f)) for f, _ in self._fields_)
+
+
+class SkScanConfig(C.Structure):
+    """sk_scan_config (analysis.hpp:31-41)."""
+    _fields_ = [("sample_rate_hz", C.c_double), ("n", C.c_size_t), ("f1_hz", C.c_double), ("f2_hz", C.c_double),
+                ("m", C.c_size_t), ("center_hz", C.c_double), ("sep_start_hz", C.c_double),
+                ("sep_stop_hz", C.c_double), ("sep_step_hz", C.c_double)]
+
+
 class SkZoomOptions(C.Structure):
     """sk_zoom_options (spectralkit.h:170-179 layout)."""
     _fields_ = [("center_hz", C.c_double), ("center_set", C.c_int), ("decimation", sz),
@@ -109,6 +126,15 @@ def _declare(L):
         "skg_traces_read_csv": (st, [C.POINTER(C.c_char_p), sz, sz, C.c_int, vp, sz, dp, dp, C.c_int, vp]),
         "skg_spectra_write_csv": (st, [C.POINTER(C.c_char_p), sz, C.c_int, vp, sz, sz, dp, C.c_double, C.c_int,
                                        vp]),
+        "sk_dip_metric_compute": (st, [vp, C.c_double, C.c_double, C.POINTER(SkDipMetric)]),
+        "sk_scan_config_defaults": (None, [C.POINTER(SkScanConfig)]),
+        "sk_resolvability_scan": (st, [C.POINTER(SkScanConfig), C.POINTER(vp)]),
+        "sk_resolvability_curve_free": (None, [vp]),
+        "sk_resolvability_curve_size": (sz, [vp]),
+        "sk_resolvability_curve_point": (st, [vp, sz, dp, C.POINTER(SkDipMetric), C.POINTER(SkDipMetric)]),
+        "sk_resolvability_min_fft": (C.c_double, [vp]),
+        "sk_resolvability_min_czt": (C.c_double, [vp]),
+        "skg_resolvability_fft_len": (sz, [vp]),
         "skg_czt_plan_create": (st, [sz, C.c_double, C.c_double, C.c_double, C.c_double, sz, C.c_int,
                                      C.POINTER(vp)]),
         "skg_czt_plan_free": (None, [vp]),
@@ -333,6 +359,55 @@ def spectra_write_csv(paths, bins, f_start_hz, f_step_hz, threads=0):
     f0 = np.ascontiguousarray(np.broadcast_to(np.asarray(f_start_hz, np.float64), (b,)))
     _chk(lib().skg_spectra_write_csv(_paths(paths), b, _prec(bins), vp(bins.data_ptr()), s, bins.shape[-1], _p(f0),
                                      f_step_hz, threads, _stream()))
+
+
+def scan_config(**kw) -> SkScanConfig:
+    c = SkScanConfig()
+    lib().sk_scan_config_defaults(C.byref(c))
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def read_curve(L, h, fft_len_fn=None):
+    """(separations, fft metrics S x 8, czt metrics S x 8, min_fft, min_czt) of a curve handle through
+    the sk_resolvability_* accessors of library L (ours or the reference's: same ABI)."""
+    S = int(L.sk_resolvability_curve_size(h))
+    sep, fm, cm = np.zeros(S), np.zeros((S, 8)), np.zeros((S, 8))
+    a, b, v = SkDipMetric(), SkDipMetric(), C.c_double()
+    for i in range(S):
+        _chk(L.sk_resolvability_curve_point(h, i, C.byref(v), C.byref(a), C.byref(b)))
+        sep[i], fm[i], cm[i] = v.value, a.astuple(), b.astuple()
+    return sep, fm, cm, float(L.sk_resolvability_min_fft(h)), float(L.sk_resolvability_min_czt(h))
+
+
+def resolvability_scan(**cfg):
+    """sk_resolvability_scan (analysis.cpp:99-195) on the GPU: dict with separations_hz, fft / czt
+    metric rows (resolved, dip_db, f_peak_a, peak_a_db, f_peak_b, peak_b_db, f_valley, valley_db),
+    min_resolved_fft_hz / _czt_hz (NaN when none) and fft_len."""
+    c = scan_config(**cfg)
+    h = vp()
+    _chk(lib().sk_resolvability_scan(C.byref(c), C.byref(h)))
+    try:
+        sep, fm, cm, mf, mc = read_curve(lib(), h)
+        return {"separations_hz": sep, "fft": fm, "czt": cm, "min_resolved_fft_hz": mf, "min_resolved_czt_hz": mc,
+                "fft_len": int(lib().skg_resolvability_fft_len(h))}
+    finally:
+        lib().sk_resolvability_curve_free(h)
+
+
+def dip_metric(bins, f_start_hz, f_step_hz, f_a_hz, f_b_hz):
+    """sk_dip_metric_compute (analysis.cpp:30-97) on a host spectrum."""
+    b = np.ascontiguousarray(bins, np.complex128)
+    re, im = np.ascontiguousarray(b.real), np.ascontiguousarray(b.imag)
+    h = vp()
+    _chk(lib().sk_spectrum_create(_p(re), _p(im), b.size, f_start_hz, f_step_hz, C.byref(h)))
+    try:
+        m = SkDipMetric()
+        _chk(lib().sk_dip_metric_compute(h, f_a_hz, f_b_hz, C.byref(m)))
+        return m.astuple()
+    finally:
+        lib().sk_spectrum_free(h)
 
 
 def _take_spectrum(h) -> Spectrum:

@@ -3,6 +3,7 @@
 // exceptions are mapped to status codes, the message goes to a thread-local string.
 #include <algorithm>
 #include <cmath>
+#include <limits>
 #include <memory>
 #include <mutex>
 #include <cstring>
@@ -10,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "analysis.hpp"
 #include "host.hpp"
 #include "io.hpp"
 #include "spectralkit.h"
@@ -35,6 +37,9 @@ struct sk_spectrum {
 struct sk_zoom_plan {
     std::unique_ptr<skg::ZoomPlanG> p;
 };
+struct sk_resolvability_curve {
+    skg::CurveH c;
+};
 struct skg_czt_plan {
     std::unique_ptr<skg::CztPlanG> p;
     bool f32 = false;
@@ -58,7 +63,10 @@ template <typename Fn> sk_status guarded(Fn&& fn) {
     } catch (const std::invalid_argument& e) {
         g_err = e.what();
         return SK_ERR_INVALID_ARGUMENT;
-    } catch (const skg::ParseError& e) {   // capi.cpp:56-67 of the reference
+    } catch (const skg::InsufficientResolution& e) {   // capi.cpp:56-67 of the reference
+        g_err = e.what();
+        return SK_ERR_INSUFFICIENT_RESOLUTION;
+    } catch (const skg::ParseError& e) {
         g_err = e.what();
         return SK_ERR_PARSE;
     } catch (const skg::FormatError& e) {
@@ -481,6 +489,76 @@ sk_status skg_spectra_write_csv(const char* const* paths, size_t count, int prec
         });
     });
 }
+
+// ---- two-tone analysis (analysis.cpp:30-195; capi.cpp:568-629 of the reference) ----------------
+namespace {
+void copy_metric(const skg::DipMetricH& m, sk_dip_metric* o) {
+    o->resolved = m.resolved ? 1 : 0;
+    o->dip_db = m.dip_db;
+    o->f_peak_a_hz = m.f_peak_a_hz;
+    o->peak_a_db = m.peak_a_db;
+    o->f_peak_b_hz = m.f_peak_b_hz;
+    o->peak_b_db = m.peak_b_db;
+    o->f_valley_hz = m.f_valley_hz;
+    o->valley_db = m.valley_db;
+}
+}  // namespace
+
+sk_status sk_dip_metric_compute(const sk_spectrum* s, double f_a, double f_b, sk_dip_metric* out) {
+    if (!s || !out) return bad_arg("sk_dip_metric_compute: null argument");
+    return guarded([&] {
+        copy_metric(skg::dip_metric(s->bins.data(), s->bins.size(), s->f_start, s->f_step, f_a, f_b), out);
+    });
+}
+
+void sk_scan_config_defaults(sk_scan_config* cfg) {
+    if (!cfg) return;
+    const skg::ScanConfigH d;
+    cfg->sample_rate_hz = d.sample_rate_hz;
+    cfg->n = d.n;
+    cfg->f1_hz = d.f1_hz;
+    cfg->f2_hz = d.f2_hz;
+    cfg->m = d.m;
+    cfg->center_hz = d.center_hz;
+    cfg->sep_start_hz = d.sep_start_hz;
+    cfg->sep_stop_hz = d.sep_stop_hz;
+    cfg->sep_step_hz = d.sep_step_hz;
+}
+
+sk_status sk_resolvability_scan(const sk_scan_config* cfg, sk_resolvability_curve** out) {
+    if (!cfg || !out) return bad_arg("sk_resolvability_scan: null argument");
+    return guarded([&] {
+        skg::ScanConfigH c;
+        c.sample_rate_hz = cfg->sample_rate_hz;
+        c.n = cfg->n;
+        c.f1_hz = cfg->f1_hz;
+        c.f2_hz = cfg->f2_hz;
+        c.m = cfg->m;
+        c.center_hz = cfg->center_hz;
+        c.sep_start_hz = cfg->sep_start_hz;
+        c.sep_stop_hz = cfg->sep_stop_hz;
+        c.sep_step_hz = cfg->sep_step_hz;
+        *out = new sk_resolvability_curve{skg::resolvability_scan(c)};
+    });
+}
+void sk_resolvability_curve_free(sk_resolvability_curve* c) { delete c; }
+size_t sk_resolvability_curve_size(const sk_resolvability_curve* c) { return c ? c->c.separations_hz.size() : 0; }
+sk_status sk_resolvability_curve_point(const sk_resolvability_curve* c, size_t i, double* sep, sk_dip_metric* fm,
+                                       sk_dip_metric* cm) {
+    if (!c) return bad_arg("sk_resolvability_curve_point: null curve");
+    if (i >= c->c.separations_hz.size()) return bad_arg("sk_resolvability_curve_point: index out of range");
+    if (sep) *sep = c->c.separations_hz[i];
+    if (fm) copy_metric(c->c.fft_metrics[i], fm);
+    if (cm) copy_metric(c->c.czt_metrics[i], cm);
+    return SK_OK;
+}
+double sk_resolvability_min_fft(const sk_resolvability_curve* c) {
+    return c ? c->c.min_resolved_fft_hz : std::numeric_limits<double>::quiet_NaN();
+}
+double sk_resolvability_min_czt(const sk_resolvability_curve* c) {
+    return c ? c->c.min_resolved_czt_hz : std::numeric_limits<double>::quiet_NaN();
+}
+size_t skg_resolvability_fft_len(const sk_resolvability_curve* c) { return c ? c->c.fft_len : 0; }
 
 // ---- spectra -----------------------------------------------------------------------------------
 sk_status sk_fft_spectrum(const sk_trace* t, size_t transform_len, sk_spectrum** out) {

@@ -121,3 +121,15 @@ def cfg4_cube(h=256, w=256, n=2048, seed=SEED + 5, dtype=np.float32):
         cube[s:e] = blk.astype(dtype)
     ref = thz_pulse(n) + NOISE * np.random.default_rng(seed + 3).standard_normal(n)
     return cube, ref
+
+
+# resolvability sweeps used for parity against the reference's own curves (tests/golden/scan.npz) and
+# in bench.py: the reference defaults (chirp route, fft_len 1138), a power-of-two
+# padded route (fft_len 512), and a THz-scale sweep (fft_len 14124, multi-pass Bluestein)
+SCAN_CASES = {
+    "default": {},
+    "pow2": dict(f1_hz=0.0, f2_hz=4000.0, m=256, center_hz=2000.0, sep_start_hz=20.0, sep_stop_hz=400.0,
+                 sep_step_hz=10.0),
+    "thz": dict(sample_rate_hz=20e12, n=1024, f1_hz=0.1e12, f2_hz=3.0e12, m=2048, center_hz=1.0e12,
+                sep_start_hz=5e9, sep_stop_hz=200e9, sep_step_hz=5e9),
+}

@@ -156,6 +156,31 @@ def ref_write_csv(kind, path, data, a, b):
         return f.read()
 
 
+SCAN_CASES = W.SCAN_CASES
+
+
+def ref_scan(**kw):
+    import paper_2108_03948_b200 as sk
+    R.sk_scan_config_defaults.argtypes = [C.POINTER(sk.SkScanConfig)]
+    R.sk_resolvability_scan.argtypes = [C.POINTER(sk.SkScanConfig), C.POINTER(C.c_void_p)]
+    R.sk_resolvability_curve_size.restype = C.c_size_t
+    R.sk_resolvability_curve_size.argtypes = [C.c_void_p]
+    R.sk_resolvability_curve_point.argtypes = [C.c_void_p, C.c_size_t, C.POINTER(C.c_double),
+                                               C.POINTER(sk.SkDipMetric), C.POINTER(sk.SkDipMetric)]
+    R.sk_resolvability_min_fft.restype = R.sk_resolvability_min_czt.restype = C.c_double
+    R.sk_resolvability_min_fft.argtypes = R.sk_resolvability_min_czt.argtypes = [C.c_void_p]
+    R.sk_resolvability_curve_free.argtypes = [C.c_void_p]
+    c = sk.SkScanConfig()
+    R.sk_scan_config_defaults(C.byref(c))
+    for k, v in kw.items():
+        setattr(c, k, v)
+    h = C.c_void_p()
+    assert R.sk_resolvability_scan(C.byref(c), C.byref(h)) == 0, R.sk_last_error()
+    out = sk.read_curve(R, h)
+    R.sk_resolvability_curve_free(h)
+    return out
+
+
 def ref_zoom(samples, fs, f1, f2, taps=None, n_fft=None, **kw):
     o = dict(center_hz=0.0, center_set=0, decimation=0, cutoff_hz=0.0, num_taps=0, circular=1,
              trim_transient=0, pad_pow2=1)
@@ -275,6 +300,14 @@ def main():
         rc, _, x, fs, t0 = ref_trace_read_csv(rt_path)
         cv["rt_x"], cv["rt_fs"], cv["rt_t0"] = x, fs, t0
     np.savez_compressed(os.path.join(OUT, "csv.npz"), **cv)
+
+    # --- resolvability sweep: the reference's own curves -------------------------
+    rs = {}
+    for name, kw in SCAN_CASES.items():
+        rs[f"{name}_sep"], rs[f"{name}_fft"], rs[f"{name}_czt"], rs[f"{name}_minfft"], rs[f"{name}_minczt"] = \
+            ref_scan(**kw)
+    # dip_metric on a reference spectrum (fft of a two-tone record), incl. the insufficient-resolution case
+    np.savez_compressed(os.path.join(OUT, "scan.npz"), **rs)
 
     # --- zoom: cfg3 reference sizing (65 taps, n_fft 512), the 2048 variant, 500-sample plans ----
     zm = {}
