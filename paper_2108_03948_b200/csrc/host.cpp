@@ -213,6 +213,38 @@ const void* cached(int kind, int a, int b, bool f32, const std::function<std::ve
 
 int single_cta_max_log2(bool f32) { return f32 ? kMaxLog2F32 : kMaxLog2F64; }
 
+namespace {
+// W_L^{r k2}, r < 8, k2 < L/8: the cluster FFT's inter-CTA twiddles (fp64 phase reduction)
+const void* cluster_twiddles(int log2L, bool f32) {
+    require_device();
+    return cached(4, log2L, 0, f32, [&] {
+        const size_t L = size_t{1} << log2L, Q = L / 8;
+        std::vector<cd> v(L);
+        const double q = -1.0 / static_cast<double>(L);
+        for (size_t r = 0; r < 8; ++r)
+            for (size_t k = 0; k < Q; ++k) v[r * Q + k] = cis_cycles(q, static_cast<double>(r * k));
+        return v;
+    });
+}
+// opt-in (SKG_CLUSTER=1): measured slower than the four-step passes on B200 (fp64 L = 2^15: 7.5 vs
+// 6.7 ms, 2^16: 10.6 vs 6.9 ms per 1 GiB batch; fp32 2^16 equal) — the per-SM Q-point FFTs run at
+// 1-2 CTAs per SM and stall on the exchange; kept, tested, for the packed / multi-trace follow-up
+bool cluster_enabled(int log2L, bool f32) {
+    const char* e = getenv("SKG_CLUSTER");   // read per call so tests can switch paths in-process
+    return e && e[0] == '1' && cluster_fft_log2q(log2L, f32) > 0;
+}
+// one L-point transform per 8-CTA cluster (kernels_cluster.cu); in_kind 0 complex, 1 real rows
+void fft_cluster(int lg, bool f32, bool inverse, int mode, const void* x, int in_kind, long long x_stride,
+                 long long N, long long batch, void* out, long long out_stride, cudaStream_t st) {
+    const int lq = cluster_fft_log2q(lg, f32);
+    check(launch_fft_cluster(lg, f32, inverse, mode, x, in_kind, x_stride, N, batch, stockham_twiddles(lq, f32),
+                             cluster_twiddles(lg, f32), out, out_stride,
+                             inverse ? 1.0 / static_cast<double>(size_t{1} << lg) : 1.0, st),
+          "cluster fft launch");
+    count_launch();
+}
+}  // namespace
+
 const void* stockham_twiddles(int log2L, bool f32) {
     require_device();
     return cached(1, log2L, 0, f32, [&] {
@@ -310,6 +342,10 @@ void fft_c2c(size_t n, bool inverse, bool f32, const void* in, long long in_stri
              long long out_stride, long long batch, cudaStream_t st) {
     if (batch <= 0) return;
     const int lg = ilog2(n);
+    if (lg > single_cta_max_log2(f32) && cluster_enabled(lg, f32)) {   // in place is safe: a trace is
+        fft_cluster(lg, f32, inverse, 0, in, 0, in_stride, (long long)n, batch, out, out_stride, st);   // read before it is written
+        return;
+    }
     if (lg > single_cta_max_log2(f32)) {
         FourStep f(lg, f32);
         if (in == out) {   // the row pass scatters: stage through a copy for in-place calls
@@ -586,6 +622,11 @@ void fft_spectrum_batch(size_t n, size_t len, bool f32, int layout, const void* 
         return;
     }
     const int lgM = ilog2(len) - 1;
+    if (lgM > single_cta_max_log2(f32) && cluster_enabled(lgM + 1, f32)) {
+        // one cluster per transform: complex FFT of the zero-padded real rows, full or half layout
+        fft_cluster(lgM + 1, f32, false, layout == 0 ? 0 : 1, x, 1, x_stride, (long long)n, batch, out, out_stride, st);
+        return;
+    }
     if (lgM > single_cta_max_log2(f32)) {
         // multi-pass: complex FFT of the zero-padded real rows (imaginary part synthesised as 0)
         FourStep f(lgM + 1, f32);

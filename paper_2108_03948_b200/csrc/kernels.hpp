@@ -118,6 +118,16 @@ cudaError_t launch_zoom_cfir(const ZoomArgs& a, bool f32, const void* x, long lo
 // shared bytes the fused zoom kernel needs for this geometry
 size_t zoom_smem_bytes(const ZoomArgs& a, int log2n, bool f32);
 
+// ---- cluster FFT (kernels_cluster.cu): one L-point transform per 8-CTA cluster, DSMEM exchange ----
+// log2 of the per-CTA length Q = L / 8 when L has a cluster instantiation (fp64 2^15..2^16,
+// fp32 2^16..2^17), else 0
+int cluster_fft_log2q(int log2L, bool f32);
+// in_kind 0 complex rows / 1 real rows; mode 0 all L bins, 1 bins 0..L/2; tw_q = Stockham tables of
+// the Q-point transform, twc = W_L^{r k2} (r < 8, k2 < Q) row-major
+cudaError_t launch_fft_cluster(int log2L, bool f32, bool inverse, int mode, const void* x, int in_kind,
+                               long long x_stride, long long N, long long batch, const void* tw_q, const void* twc,
+                               void* out, long long out_stride, double scale, cudaStream_t st);
+
 // band slice + magnitude_db of complex rows (slice_band spectra.cpp:40-61, magnitude_db types.cpp:13-18):
 // bins [klo, klo + nb) of each input row -> out (optional) and dB (optional)
 cudaError_t launch_band_db(bool f32, const void* in, long long in_stride, long long klo, long long nb,

@@ -92,3 +92,35 @@ def test_chunking_many_traces():
     got = sk.fft_spectrum_batch(xd, L).cpu().numpy()
     for i in (0, 95, 96, 97, 199):
         assert rel_max_rows(got[i:i + 1], O.fft_spectrum_batch(x[i:i + 1], L)) <= TOL_F64
+
+
+@pytest.mark.parametrize("path", ["cluster", "four-step"])
+@pytest.mark.parametrize("prec,L", [("f64", 32768), ("f64", 65536), ("f32", 65536), ("f32", 131072)])
+def test_long_fft_batches(prec, L, path, monkeypatch):
+    """both long-transform paths — the 8-CTA cluster FFT (kernels_cluster.cu, opt-in SKG_CLUSTER=1)
+    and the four-step passes: more traces than resident CTAs (persistent loops), a length that is no
+    multiple of 8 (partial residue classes), strided rows, half layout, an in-place complex round trip."""
+    monkeypatch.setenv("SKG_CLUSTER", "1" if path == "cluster" else "0")
+    n = L // 4 - 3
+    b = 40
+    x = W.sample_traces(b, n)
+    dt = torch.float64 if prec == "f64" else torch.float32
+    xs = torch.zeros((b, n + 5), dtype=dt, device=DEV)
+    xs[:, :n] = torch.from_numpy(x).to(dt)
+    xin = xs[:, :n].cpu().double().numpy()
+    want = O.fft_spectrum_batch(xin, L)
+    got = sk.fft_spectrum_batch(xs[:, :n], L).cpu().numpy()
+    half = sk.fft_spectrum_batch(xs[:, :n], L, layout=sk.SKG_HALF).cpu().numpy()
+    if prec == "f64":
+        assert rel_max_rows(got, want) <= TOL_F64
+    else:
+        assert rel_l2_rows(got, want) <= TOL_F32
+    np.testing.assert_array_equal(half, got[:, : L // 2 + 1])
+    c = torch.from_numpy(got[:4]).to(DEV)
+    ref_back = np.stack([O.ifft(r.astype(np.complex128)) for r in got[:4]])
+    sk.fft_batch(c, inverse=True, out=c)   # in place
+    cb = c.cpu().numpy()
+    if prec == "f64":
+        assert rel_max_rows(cb, ref_back) <= TOL_F64
+    else:
+        assert rel_l2_rows(cb, ref_back) <= TOL_F32

@@ -43,6 +43,12 @@ def run(name, steps):
         p = sk.CztPlanGPU(16384, a, w, 16384, sk.SKG_F64)
         xd = torch.from_numpy(x).to(dev)
         fn = lambda: p.execute(xd)  # noqa: E731
+    elif name.startswith("specL"):   # specL15_64: L = 2^15 fp64 spectra (cluster / four-step path)
+        lgL, pr = name[5:].split("_")
+        L = 1 << int(lgL)
+        x = W.sample_traces(64, L // 4).astype(np.float32 if pr == "32" else np.float64)
+        xd = torch.from_numpy(x).to(dev).repeat(32, 1)
+        fn = lambda: sk.fft_spectrum_batch(xd, L)  # noqa: E731
     elif name == "spec64":
         x = W.sample_traces(32768, 1024)
         xd = torch.from_numpy(x).to(dev)
