@@ -103,10 +103,12 @@ __device__ __forceinline__ float abs_t(float x, float y) {
     const float h = fmaf(x, x, y * y);
     return h > 0.0f ? h * rsqrtf(h) : 0.0f;
 }
-// magnitude_db (types.cpp:13-18): 20 log10 |v|, -300 dB at |v| <= 1e-15 (|v| = hypot, like std::abs)
+// magnitude_db (types.cpp:13-18): 20 log10 |v|, -300 dB at |v| <= 1e-15
 __device__ __forceinline__ double magnitude_db_t(double x, double y) {
-    const double m = hypot(x, y);
-    return m > 1e-15 ? 20.0 * log10(m) : -300.0;
+    // 20 log10 hypot = 10 log10 |v|^2 (a few ulp of the argument: ~1e-15 dB), without hypot's
+    // scaling work; |v|^2 <= 1e-30 <=> |v| <= 1e-15 (an |v|^2 that underflows is below the floor too)
+    const double h = fma(x, x, y * y);
+    return h > 1e-30 ? 10.0 * log10(h) : -300.0;
 }
 __device__ __forceinline__ float magnitude_db_t(float x, float y) {
     // 20 log10 sqrt(h) = 10 log10 h; the floor test on h = |v|^2 (1e-30 is a normal float)

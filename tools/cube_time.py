@@ -13,17 +13,20 @@ import paper_2108_03948_b200 as sk  # noqa: E402
 from paper_2108_03948_b200 import workloads as W  # noqa: E402
 
 
-def timeit(fn, reps):
+def timeit(fn, reps, inner=10):
+    """per-call device time: `inner` back-to-back calls between two events, so the host-side cost of
+    a call (ctypes, tensor allocation) overlaps the previous call's kernel instead of idling the GPU"""
     fn()
     torch.cuda.synchronize()
     ts = []
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        fn()
+        for _ in range(inner):
+            fn()
         e1.record()
         torch.cuda.synchronize()
-        ts.append(e0.elapsed_time(e1))
+        ts.append(e0.elapsed_time(e1) / inner)
     return float(np.median(ts)), float(min(ts))
 
 
