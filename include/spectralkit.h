@@ -66,6 +66,13 @@ SK_API sk_status sk_czt_params_for_band(double f1_hz, double f2_hz, double sampl
 
 /* ref spectralkit.h:70: smallest power of two >= max(n, 1) */
 SK_API size_t sk_next_pow2(size_t n);
+/* sizing helpers (ref spectralkit.h:71-78, resolution.cpp:18-63) */
+SK_API sk_status sk_fft_resolution(double sample_rate_hz, size_t n, double* out_hz);
+SK_API sk_status sk_record_len_for_step(double sample_rate_hz, double target_step_hz, size_t* out_len);
+SK_API sk_status sk_zeros_for_resolution(double sample_rate_hz, size_t n, double target_step_hz,
+                                         size_t* out_zeros);
+SK_API sk_status sk_czt_len_for_matched_resolution(double f1_hz, double f2_hz, double sample_rate_hz,
+                                                   size_t n_fft, size_t* out_m);
 
 /* Traces (ref spectralkit.h:82-90, capi.cpp:264-297). */
 typedef struct sk_trace sk_trace;
@@ -107,6 +114,9 @@ SK_API sk_status sk_spectrum_slice_band(const sk_spectrum* s, double f_lo_hz, do
 /* CSV "frequency_hz,re,im,magnitude_db", %.17g rows (ref spectralkit.h:163-165, spectra.cpp:63-78);
  * byte-identical to the reference's writer */
 SK_API sk_status sk_spectrum_write_csv(const sk_spectrum* s, const char* path);
+/* ref spectralkit.h:164, spectra.cpp:94-156: four fields per row, optional header, uniform axis
+ * (1e-6 step tolerance); SK_ERR_PARSE / SK_ERR_FORMAT / SK_ERR_IO as the reference */
+SK_API sk_status sk_spectrum_read_csv(const char* path, sk_spectrum** out);
 
 /* Two-tone analysis (ref spectralkit.h:197-243, analysis.cpp:30-195). The resolvability sweep runs
  * every separation's padded-FFT route and band-CZT route as two batched GPU launches; the valley
@@ -146,6 +156,8 @@ SK_API sk_status sk_resolvability_curve_point(const sk_resolvability_curve* c, s
 /* NaN when no separation resolved on that route */
 SK_API double sk_resolvability_min_fft(const sk_resolvability_curve* c);
 SK_API double sk_resolvability_min_czt(const sk_resolvability_curve* c);
+/* ref spectralkit.h:239, serialize.cpp:141-154: byte-identical CSV of the curve */
+SK_API sk_status sk_resolvability_write_csv(const sk_resolvability_curve* c, const char* path);
 
 /* Zoom pipeline (ref spectralkit.h:170-195, capi.cpp:515-564). Same struct layout. */
 typedef struct sk_zoom_options {

@@ -126,6 +126,12 @@ def _declare(L):
         "skg_traces_read_csv": (st, [C.POINTER(C.c_char_p), sz, sz, C.c_int, vp, sz, dp, dp, C.c_int, vp]),
         "skg_spectra_write_csv": (st, [C.POINTER(C.c_char_p), sz, C.c_int, vp, sz, sz, dp, C.c_double, C.c_int,
                                        vp]),
+        "sk_spectrum_read_csv": (st, [C.c_char_p, C.POINTER(vp)]),
+        "sk_resolvability_write_csv": (st, [vp, C.c_char_p]),
+        "sk_fft_resolution": (st, [C.c_double, sz, dp]),
+        "sk_record_len_for_step": (st, [C.c_double, C.c_double, C.POINTER(sz)]),
+        "sk_zeros_for_resolution": (st, [C.c_double, sz, C.c_double, C.POINTER(sz)]),
+        "sk_czt_len_for_matched_resolution": (st, [C.c_double, C.c_double, C.c_double, sz, C.POINTER(sz)]),
         "sk_dip_metric_compute": (st, [vp, C.c_double, C.c_double, C.POINTER(SkDipMetric)]),
         "sk_scan_config_defaults": (None, [C.POINTER(SkScanConfig)]),
         "sk_resolvability_scan": (st, [C.POINTER(SkScanConfig), C.POINTER(vp)]),
@@ -381,14 +387,48 @@ def read_curve(L, h, fft_len_fn=None):
     return sep, fm, cm, float(L.sk_resolvability_min_fft(h)), float(L.sk_resolvability_min_czt(h))
 
 
-def resolvability_scan(**cfg):
+def spectrum_read_csv(path) -> "Spectrum":
+    """sk_spectrum_read_csv (spectra.cpp:94-156)."""
+    h = vp()
+    _chk(lib().sk_spectrum_read_csv(os.fsencode(path), C.byref(h)))
+    return _take_spectrum(h)
+
+
+def fft_resolution(fs, n):
+    v = C.c_double()
+    _chk(lib().sk_fft_resolution(fs, n, C.byref(v)))
+    return v.value
+
+
+def record_len_for_step(fs, step):
+    v = sz()
+    _chk(lib().sk_record_len_for_step(fs, step, C.byref(v)))
+    return v.value
+
+
+def zeros_for_resolution(fs, n, step):
+    v = sz()
+    _chk(lib().sk_zeros_for_resolution(fs, n, step, C.byref(v)))
+    return v.value
+
+
+def czt_len_for_matched_resolution(f1, f2, fs, n_fft):
+    v = sz()
+    _chk(lib().sk_czt_len_for_matched_resolution(f1, f2, fs, n_fft, C.byref(v)))
+    return v.value
+
+
+def resolvability_scan(csv_path=None, **cfg):
     """sk_resolvability_scan (analysis.cpp:99-195) on the GPU: dict with separations_hz, fft / czt
     metric rows (resolved, dip_db, f_peak_a, peak_a_db, f_peak_b, peak_b_db, f_valley, valley_db),
-    min_resolved_fft_hz / _czt_hz (NaN when none) and fft_len."""
+    min_resolved_fft_hz / _czt_hz (NaN when none) and fft_len; csv_path: also write the curve
+    (sk_resolvability_write_csv)."""
     c = scan_config(**cfg)
     h = vp()
     _chk(lib().sk_resolvability_scan(C.byref(c), C.byref(h)))
     try:
+        if csv_path is not None:
+            _chk(lib().sk_resolvability_write_csv(h, os.fsencode(csv_path)))
         sep, fm, cm, mf, mc = read_curve(lib(), h)
         return {"separations_hz": sep, "fft": fm, "czt": cm, "min_resolved_fft_hz": mf, "min_resolved_czt_hz": mc,
                 "fft_len": int(lib().skg_resolvability_fft_len(h))}

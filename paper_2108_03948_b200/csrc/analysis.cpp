@@ -42,6 +42,44 @@ size_t record_len_for_step(double fs, double step) {
     return static_cast<size_t>(std::ceil(q));
 }
 
+double fft_resolution(double fs, size_t n) {
+    check_rate(fs);
+    if (n == 0) throw std::invalid_argument("fft_resolution: n must be >= 1");
+    return fs / static_cast<double>(n);
+}
+
+size_t czt_len_for_matched_resolution(double f1, double f2, double fs, size_t n_fft) {
+    check_rate(fs);
+    if (n_fft == 0) throw std::invalid_argument("czt_len_for_matched_resolution: n_fft must be >= 1");
+    if (!(f1 >= 0.0) || !(f1 < f2)) throw std::invalid_argument("czt_len_for_matched_resolution: need 0 <= f1 < f2");
+    if (f2 > fs / 2.0 * (1.0 + 1e-12))
+        throw std::invalid_argument("czt_len_for_matched_resolution: band edge exceeds the usable half rate");
+    const double m = std::round((f2 - f1) / fs * static_cast<double>(n_fft));
+    return m < 1.0 ? 1 : static_cast<size_t>(m);
+}
+
+std::string format_resolvability_csv(const CurveH& c) {
+    std::string out = "separation_hz,method,resolved,dip_db,f_peak_a_hz,peak_a_db,f_peak_b_hz,peak_b_db,"
+                      "f_valley_hz,valley_db\n";
+    auto fields = [&](const DipMetricH& m) {
+        out += m.resolved ? "1" : "0";
+        for (double v : {m.dip_db, m.f_peak_a_hz, m.peak_a_db, m.f_peak_b_hz, m.peak_b_db, m.f_valley_hz, m.valley_db}) {
+            out += ',';
+            append_g17(out, v);
+        }
+    };
+    for (size_t i = 0; i < c.separations_hz.size(); ++i) {
+        std::string sep;
+        append_g17(sep, c.separations_hz[i]);
+        out += sep + ",fft,";
+        fields(c.fft_metrics[i]);
+        out += "\n" + sep + ",czt,";
+        fields(c.czt_metrics[i]);
+        out += '\n';
+    }
+    return out;
+}
+
 size_t zeros_for_resolution(double fs, size_t n, double step) {
     check_rate(fs);
     if (n == 0) throw std::invalid_argument("zeros_for_resolution: n must be >= 1");

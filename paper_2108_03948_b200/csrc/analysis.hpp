@@ -39,6 +39,11 @@ struct CurveH {   // analysis.hpp:46-54
 };
 CurveH resolvability_scan(const ScanConfigH& cfg, int threads = 0);
 
+// write_resolvability_csv (serialize.cpp:39-45, 141-154): two rows per separation, %.17g fields
+std::string format_resolvability_csv(const CurveH& c);
+
+double fft_resolution(double fs, size_t n);                   // resolution.cpp:28-32
+size_t czt_len_for_matched_resolution(double f1, double f2, double fs, size_t n_fft);   // resolution.cpp:49-63
 size_t record_len_for_step(double fs, double step);           // resolution.cpp:18-26
 size_t zeros_for_resolution(double fs, size_t n, double step);   // resolution.cpp:34-47
 

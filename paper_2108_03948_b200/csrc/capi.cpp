@@ -396,6 +396,20 @@ sk_status sk_trace_write_csv(const sk_trace* t, const char* path) {
     return guarded([&] { skg::write_trace_csv_file(t->samples.data(), t->samples.size(), t->fs, t->t0, path); });
 }
 
+sk_status sk_spectrum_read_csv(const char* path, sk_spectrum** out) {
+    if (!path || !out) return bad_arg("sk_spectrum_read_csv: null argument");
+    return guarded([&] {
+        skg::HostSpectrum h = skg::read_spectrum_csv_file(path);
+        auto* s = new sk_spectrum;
+        s->bins.resize(h.bins.size() / 2);
+        for (size_t k = 0; k < s->bins.size(); ++k) s->bins[k] = cd(h.bins[2 * k], h.bins[2 * k + 1]);
+        s->f_start = h.f_start;
+        s->f_step = h.f_step;
+        s->source_n = h.source_n;
+        *out = s;
+    });
+}
+
 sk_status sk_spectrum_write_csv(const sk_spectrum* s, const char* path) {
     if (!s || !path) return bad_arg("sk_spectrum_write_csv: null argument");
     return guarded([&] {
@@ -559,6 +573,30 @@ double sk_resolvability_min_czt(const sk_resolvability_curve* c) {
     return c ? c->c.min_resolved_czt_hz : std::numeric_limits<double>::quiet_NaN();
 }
 size_t skg_resolvability_fft_len(const sk_resolvability_curve* c) { return c ? c->c.fft_len : 0; }
+sk_status sk_resolvability_write_csv(const sk_resolvability_curve* c, const char* path) {
+    if (!c || !path) return bad_arg("sk_resolvability_write_csv: null argument");
+    return guarded([&] {
+        skg::write_text_file(skg::format_resolvability_csv(c->c), path, "cannot open for writing: ", "resolvability");
+    });
+}
+
+// sizing helpers (resolution.cpp:18-63; capi.cpp:237-265 of the reference)
+sk_status sk_fft_resolution(double fs, size_t n, double* out) {
+    if (!out) return bad_arg("sk_fft_resolution: null output");
+    return guarded([&] { *out = skg::fft_resolution(fs, n); });
+}
+sk_status sk_record_len_for_step(double fs, double step, size_t* out) {
+    if (!out) return bad_arg("sk_record_len_for_step: null output");
+    return guarded([&] { *out = skg::record_len_for_step(fs, step); });
+}
+sk_status sk_zeros_for_resolution(double fs, size_t n, double step, size_t* out) {
+    if (!out) return bad_arg("sk_zeros_for_resolution: null output");
+    return guarded([&] { *out = skg::zeros_for_resolution(fs, n, step); });
+}
+sk_status sk_czt_len_for_matched_resolution(double f1, double f2, double fs, size_t n_fft, size_t* out) {
+    if (!out) return bad_arg("sk_czt_len_for_matched_resolution: null output");
+    return guarded([&] { *out = skg::czt_len_for_matched_resolution(f1, f2, fs, n_fft); });
+}
 
 // ---- spectra -----------------------------------------------------------------------------------
 sk_status sk_fft_spectrum(const sk_trace* t, size_t transform_len, sk_spectrum** out) {

@@ -118,6 +118,95 @@ HostTrace parse_trace_csv(const char* data, size_t len, const std::string& origi
     return tr;
 }
 
+HostSpectrum parse_spectrum_csv(const char* data, size_t len, const std::string& origin) {
+    std::vector<double> freqs, bins;
+    size_t line_no = 0, pos = 0;
+    bool first_content = true;
+    while (pos < len) {
+        const char* nl = static_cast<const char*>(memchr(data + pos, '\n', len - pos));
+        const size_t end = nl ? (size_t)(nl - data) : len;
+        std::string_view line(data + pos, end - pos);
+        pos = end + 1;
+        ++line_no;
+        if (!line.empty() && line.back() == '\r') line.remove_suffix(1);
+        if (line.find_first_not_of(" \t") == std::string_view::npos) continue;
+        double vals[4];
+        std::string_view rest = line;
+        bool ok = true;
+        for (int c = 0; c < 4 && ok; ++c) {   // spectra.cpp:106-121: exactly four fields
+            const size_t comma = rest.find(',');
+            std::string_view field = c < 3 ? rest.substr(0, comma) : rest;
+            if (c < 3) {
+                if (comma == std::string_view::npos) {
+                    ok = false;
+                    break;
+                }
+                rest = rest.substr(comma + 1);
+            } else if (comma != std::string_view::npos) {
+                ok = false;
+                break;
+            }
+            ok = parse_double(field, vals[c]);
+        }
+        if (!ok) {
+            if (first_content) {
+                first_content = false;
+                continue;
+            }
+            throw ParseError(origin + ": malformed row at line " + std::to_string(line_no), line_no);
+        }
+        first_content = false;
+        freqs.push_back(vals[0]);
+        bins.push_back(vals[1]);
+        bins.push_back(vals[2]);
+    }
+    if (bins.empty()) throw FormatError(origin + ": no spectrum rows");
+    HostSpectrum s;
+    s.f_start = freqs.front();
+    const size_t n = freqs.size();
+    if (n == 1) {
+        s.f_step = 0.0;
+    } else {
+        const double step = (freqs.back() - freqs.front()) / static_cast<double>(n - 1);
+        if (!(step > 0.0)) throw FormatError(origin + ": frequency axis is not increasing");
+        for (size_t k = 0; k + 1 < n; ++k)
+            if (std::abs(freqs[k + 1] - freqs[k] - step) > 1e-6 * step)
+                throw FormatError(origin + ": non-uniform frequency step near row " + std::to_string(k + 1));
+        s.f_step = step;
+    }
+    s.bins = std::move(bins);
+    s.source_n = n;
+    return s;
+}
+
+HostSpectrum read_spectrum_csv_file(const std::string& path) {
+    if (path == "-") {
+        const std::string s = slurp(stdin);
+        return parse_spectrum_csv(s.data(), s.size(), "stdin");
+    }
+    FILE* f = fopen(path.c_str(), "rb");
+    if (!f) throw IoError("cannot open spectrum file: " + path);
+    const std::string s = slurp(f);
+    fclose(f);
+    return parse_spectrum_csv(s.data(), s.size(), path);
+}
+
+void append_g17(std::string& out, double v) {
+    char buf[64];
+    char* p = put_g17(buf, buf + sizeof buf, v);
+    out.append(buf, p - buf);
+}
+
+void write_text_file(const std::string& body, const std::string& path, const char* open_msg, const char* what) {
+    FILE* f = stdout;
+    if (path != "-") {
+        f = fopen(path.c_str(), "wb");
+        if (!f) throw IoError(std::string(open_msg) + path);
+    }
+    const bool ok = fwrite(body.data(), 1, body.size(), f) == body.size();
+    finish_out(f, ok, what);
+}
+
 HostTrace read_trace_csv_file(const std::string& path) {
     if (path == "-") {
         const std::string s = slurp(stdin);

@@ -32,6 +32,15 @@ struct HostTrace {
 HostTrace parse_trace_csv(const char* data, size_t len, const std::string& origin);
 // read_trace_csv_file (signals.cpp:172-176); "-" reads stdin (capi.cpp:98, 394)
 HostTrace read_trace_csv_file(const std::string& path);
+struct HostSpectrum {
+    std::vector<double> bins;   // interleaved re, im
+    double f_start = 0.0, f_step = 0.0;
+    size_t source_n = 0;
+};
+// read_spectrum_csv (spectra.cpp:94-150): "frequency_hz,re,im,magnitude_db" rows, optional header,
+// uniform axis check; read_spectrum_csv_file (spectra.cpp:152-156), "-" = stdin
+HostSpectrum parse_spectrum_csv(const char* data, size_t len, const std::string& origin);
+HostSpectrum read_spectrum_csv_file(const std::string& path);
 // write_trace_csv (signals.cpp:178-189) to a file ("-" = stdout); validates like the reference
 void write_trace_csv_file(const double* samples, size_t n, double fs, double t0, const std::string& path);
 // write_spectrum_csv (spectra.cpp:63-72): "frequency_hz,re,im,magnitude_db" + %.17g rows
@@ -39,6 +48,11 @@ void write_spectrum_csv_file(const double* bins_interleaved, size_t n, double f_
                              const std::string& path);
 // the CSV body as a string (the same bytes the file gets)
 std::string format_spectrum_csv(const double* bins_interleaved, size_t n, double f_start, double f_step);
+
+// open a reference-format output file (serialize.cpp:22-26 message; "-" = stdout), write, close
+void write_text_file(const std::string& body, const std::string& path, const char* open_msg, const char* what);
+// %.17g of v appended to out (std::to_chars, the printf format the reference uses)
+void append_g17(std::string& out, double v);
 
 // run fn(i) for i < count on up to `threads` host threads (0 = all cores); the lowest-index
 // exception is rethrown after every task finished

@@ -25,10 +25,15 @@ template <typename T> struct Tile {
 enum : int { IN_CPLX = 0, IN_REAL = 1, IN_REAL_CHIRP = 2, IN_CPLX_CHIRP = 3, IN_WORK = 4 };
 enum : int { OUT_WORK_TW = 0, OUT_CHIRP = 1, OUT_SCALE = 2 };
 
-template <typename T, int LOG2R, bool INV>
+#ifndef SKG_4STEP_COL_THREADS
+#define SKG_4STEP_COL_THREADS 512   // resident threads per SM the column pass's register cap targets
+#endif
+// NZ: leading nonzero rows n1 of the column transforms (zero padding: x[C n1 + n2] = 0 for
+// C n1 + n2 >= N), which prunes the first radix-16 pass; the forward pass only.
+template <typename T, int LOG2R, bool INV, int NZ = 16>
 __global__ void __launch_bounds__(FftGeom<LOG2R>::NT * Tile<T>::W,
-                                  (FftGeom<LOG2R>::NT * Tile<T>::W) >= 512 ? 1
-                                  : 512 / ((FftGeom<LOG2R>::NT * Tile<T>::W) < 32 ? 32 : (FftGeom<LOG2R>::NT * Tile<T>::W)))
+                                  (FftGeom<LOG2R>::NT * Tile<T>::W) >= SKG_4STEP_COL_THREADS ? 1
+                                  : SKG_4STEP_COL_THREADS / ((FftGeom<LOG2R>::NT * Tile<T>::W) < 32 ? 32 : (FftGeom<LOG2R>::NT * Tile<T>::W)))
 k4_col(const void* __restrict__ xin, int in_kind, int conj_in, long long x_stride, long long N,
        const cx_t<T>* __restrict__ cin, cx_t<T>* __restrict__ Y, int log2C, long long batch,
        const cx_t<T>* __restrict__ tw, const cx_t<T>* __restrict__ twL, int out_kind, void* __restrict__ out,
@@ -69,13 +74,21 @@ k4_col(const void* __restrict__ xin, int in_kind, int conj_in, long long x_strid
         const long long b = u / tiles;
         const long long n2 = (u % tiles) * TC + g;
         prefetch(u + gridDim.x);
+        if (out_kind == OUT_WORK_TW && g == 0) {
+            // the store's W_L twiddles: one 128-byte line per (row, 8/16-column tile) into L1 now, so
+            // the twiddle loads after the transform hit L1 instead of waiting on L2
+#pragma unroll
+            for (int q = 0; q < G::EPT; ++q) prefetch_l1(twL + (tid + (long long)G::NT * q) * Cn + n2);
+        }
         C v[G::EPT];
 #pragma unroll
         for (int q = 0; q < G::EPT; ++q) {
             const long long n1 = tid + (long long)G::NT * q;
             const long long n = n1 * Cn + n2;
             C val = czero<C>();
-            if (in_kind == IN_WORK) {
+            if (q >= NZ && in_kind != IN_WORK) {
+                // rows past the data: zero (the caller guarantees C n1 >= N here)
+            } else if (in_kind == IN_WORK) {
                 val = Y[b * L + n];   // Y[k1][n2] with k1 = n1
             } else if (n < N) {
                 if (in_kind == IN_REAL || in_kind == IN_REAL_CHIRP)
@@ -87,7 +100,7 @@ k4_col(const void* __restrict__ xin, int in_kind, int conj_in, long long x_strid
             }
             v[q] = val;
         }
-        block_fft<INV, LOG2R>(v, sm, tws, tid);
+        block_fft<INV, LOG2R, NZ>(v, sm, tws, tid);
 #pragma unroll
         for (int q = 0; q < G::EPT; ++q) {
             const long long k1 = tid + (long long)G::NT * q;
@@ -208,7 +221,12 @@ cudaError_t launch_4step_col_impl(int log2R, bool inverse, int in_kind, int conj
                 out_kind, out, out_stride, M, (const C*)cout, scale, conj_out);
             return cudaGetLastError();
         };
-        return inverse ? launch(k4_col<T, LG, true>) : launch(k4_col<T, LG, false>);
+        if (inverse || in_kind == IN_WORK) return inverse ? launch(k4_col<T, LG, true>) : launch(k4_col<T, LG, false>);
+        // rows n1 holding data: C n1 < N  ->  n1 < ceil(N / C)
+        const int nz = LG >= 8 ? nz_class((N + (1LL << log2C) - 1) >> log2C, G::NT) : 16;
+        if (nz == 4) return launch(k4_col<T, LG, false, 4>);
+        if (nz == 8) return launch(k4_col<T, LG, false, 8>);
+        return launch(k4_col<T, LG, false>);
     });
 }
 

@@ -133,6 +133,34 @@ def ref_trace_read_csv(path):
     return 0, "", x, fs, t0
 
 
+SPEC_CSV_CASES = {
+    "three_fields": b"frequency_hz,re,im,magnitude_db\n0,1,2,3\n1,1,2\n",
+    "five_fields": b"0,1,2,3\n1,1,2,3,4\n",
+    "nonuniform": b"0,1,0,0\n1,1,0,0\n2.5,1,0,0\n3.5,1,0,0\n",
+    "decreasing": b"2,1,0,0\n1,1,0,0\n",
+    "single": b"frequency_hz,re,im,magnitude_db\n5e12,1.5,-2,4\n",
+    "header_only": b"frequency_hz,re,im,magnitude_db\n",
+    "crlf_ws": b"\r\n 0 , 1 ,\t2, 0\r\n1e9,3,4,0\r\n\r\n2e9,5,6,0",
+    "jitter": b"0,1,0,0\n1.0000000001,2,0,0\n2,3,0,0\n",
+}
+
+
+def ref_spectrum_read_csv(path):
+    R.sk_spectrum_read_csv.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+    R.sk_spectrum_source_n.restype = C.c_size_t
+    R.sk_spectrum_source_n.argtypes = [C.c_void_p]
+    h = C.c_void_p()
+    rc = R.sk_spectrum_read_csv(path.encode(), C.byref(h))
+    if rc != 0:
+        return rc, R.sk_last_error().decode(), None, 0.0, 0.0, 0
+    n = R.sk_spectrum_size(h)
+    re, im = np.zeros(n), np.zeros(n)
+    R.sk_spectrum_copy_data(h, P(re), P(im))
+    out = (0, "", re + 1j * im, R.sk_spectrum_f_start(h), R.sk_spectrum_f_step(h), R.sk_spectrum_source_n(h))
+    R.sk_spectrum_free(h)
+    return out
+
+
 def ref_write_csv(kind, path, data, a, b):
     """sk_trace_write_csv (kind 'trace': data samples, a fs, b t0) or sk_spectrum_write_csv
     (kind 'spectrum': data complex bins, a f_start, b f_step); returns the file bytes"""
@@ -296,6 +324,15 @@ def main():
         cv["w_odd_X"] = odd
         cv["w_odd"] = np.frombuffer(ref_write_csv("spectrum", os.path.join(td, "o.csv"), odd, -5.0, 1.0 / 3.0),
                                     np.uint8)
+        for name, body in dict(SPEC_CSV_CASES, written=bytes(cv["w_spec"])).items():
+            path = os.path.join(td, "sp_" + name + ".csv")
+            with open(path, "wb") as f:
+                f.write(body)
+            rc, msg, X, f0, df, sn = ref_spectrum_read_csv(path)
+            cv[f"sin_{name}"] = np.frombuffer(body, np.uint8)
+            cv[f"src_{name}"], cv[f"smsg_{name}"] = rc, msg.replace(path, "<PATH>")
+            if rc == 0:
+                cv[f"sX_{name}"], cv[f"sf0_{name}"], cv[f"sdf_{name}"], cv[f"sn_{name}"] = X, f0, df, sn
         rt_path = os.path.join(td, "t.csv")   # the written trace read back by the reference
         rc, _, x, fs, t0 = ref_trace_read_csv(rt_path)
         cv["rt_x"], cv["rt_fs"], cv["rt_t0"] = x, fs, t0

@@ -73,3 +73,41 @@ def test_invalid_trace_write(tmp_path):
     with pytest.raises(sk.SkError) as e:
         sk.trace_write_csv(np.array([1.0, 2.0]), 1.0, 0.0, str(tmp_path / "no" / "dir.csv"))
     assert e.value.status == 2 and "cannot open trace file for writing" in e.value.message
+
+
+SPEC_CASES = ["three_fields", "five_fields", "nonuniform", "decreasing", "single", "header_only", "crlf_ws",
+              "jitter", "written"]
+
+
+@pytest.mark.parametrize("name", SPEC_CASES)
+def test_spectrum_read_matches_reference(golden, tmp_path, name):
+    """sk_spectrum_read_csv (spectra.cpp:94-156) against the reference on the same file bytes."""
+    g = golden("csv")
+    path = tmp_path / f"sp_{name}.csv"
+    path.write_bytes(bytes(g[f"sin_{name}"]))
+    rc = int(g[f"src_{name}"])
+    if rc == 0:
+        s = sk.spectrum_read_csv(str(path))
+        assert np.array_equal(s.bins, g[f"sX_{name}"])
+        assert s.f_start_hz == g[f"sf0_{name}"] and s.f_step_hz == g[f"sdf_{name}"]
+        assert s.source_n == int(g[f"sn_{name}"])
+    else:
+        with pytest.raises(sk.SkError) as e:
+            sk.spectrum_read_csv(str(path))
+        assert e.value.status == rc
+        assert e.value.message == str(g[f"smsg_{name}"]).replace("<PATH>", str(path))
+
+
+def test_sizing_helpers():
+    """resolution.cpp:18-63 (the reference's sizing arithmetic, restated) incl. its errors."""
+    assert sk.record_len_for_step(10e12, 20e9) == 500 and sk.record_len_for_step(10e12, 6e9) == 1667
+    assert sk.fft_resolution(20e12, 4096) == 20e12 / 4096
+    assert sk.zeros_for_resolution(20e12, 1024, 2.9e12 / 2048) == 14125 - 1024   # ceil(14124.1)
+    assert sk.zeros_for_resolution(8000.0, 128, 62.5) == 0
+    assert sk.czt_len_for_matched_resolution(0.5e12, 2.0e12, 10e12, 1667) == 250
+    with pytest.raises(sk.SkError, match="coarser than the unpadded spacing"):
+        sk.zeros_for_resolution(8000.0, 128, 100.0)
+    with pytest.raises(sk.SkError, match="band edge exceeds"):
+        sk.czt_len_for_matched_resolution(0.0, 6e12, 10e12, 100)
+    with pytest.raises(sk.SkError, match="positive and finite"):
+        sk.fft_resolution(0.0, 10)

@@ -47,3 +47,19 @@ def test_scan_matches_reference(golden, name):
                                                                  np.isnan(g[f"{name}_minfft"]))
     assert got["min_resolved_czt_hz"] == g[f"{name}_minczt"] or (np.isnan(got["min_resolved_czt_hz"]) and
                                                                  np.isnan(g[f"{name}_minczt"]))
+
+
+def test_curve_csv(tmp_path):
+    """sk_resolvability_write_csv (serialize.cpp:39-45, 141-154): the header, two rows per separation,
+    %.17g fields — checked against Python's printf formatting of the same curve values."""
+    p = tmp_path / "curve.csv"
+    got = sk.resolvability_scan(csv_path=str(p), **SCAN_CASES["default"])
+    lines = p.read_text().splitlines()
+    assert lines[0] == ("separation_hz,method,resolved,dip_db,f_peak_a_hz,peak_a_db,f_peak_b_hz,peak_b_db,"
+                        "f_valley_hz,valley_db")
+    assert len(lines) == 1 + 2 * got["separations_hz"].size
+    for i, sep in enumerate(got["separations_hz"]):
+        for j, route in enumerate(("fft", "czt")):
+            m = got[route][i]
+            want = ",".join(["%.17g" % sep, route, "%d" % int(m[0])] + ["%.17g" % v for v in m[1:]])
+            assert lines[1 + 2 * i + j] == want

@@ -34,3 +34,23 @@ for prec, dt, s in (("f64", torch.float64, 8), ("f32", torch.float32, 4)):
               f"({byts / t / 1e6 / 6540:.2f} of HBM)")
         del x, out
         torch.cuda.empty_cache()
+
+for prec, dt, s in (("f64", torch.float64, 8), ("f32", torch.float32, 4)):
+    for n, m in ((16384, 16384), (4096, 16384)):
+        batch = 8192 if prec == "f64" else 16384
+        x = torch.from_numpy(W.sample_traces(64, n)).to(dt).cuda().repeat(batch // 64, 1)
+        a, w = W.cfg2_czt_params(m)
+        p = sk.CztPlanGPU(n, a, w, m, sk.SKG_F64 if prec == "f64" else sk.SKG_F32)
+        out = p.execute(x)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            p.execute(x, out=out)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        print(f"[{tag}] CZT {prec} N={n} M={m} L={p.conv_size} batch={batch}: {float(np.median(ts)):.3f} ms")
+        del x, out
+        torch.cuda.empty_cache()
