@@ -17,6 +17,21 @@
 
 namespace skg {
 
+// W^{e0 + d q}, q < 16, from two table entries a = W^{e0}, s = W^{d}: products of depth <= 6
+// (s^2, s^4, then a s^{4j} s^i), so no per-element table load waits on L2 after the transform
+template <typename C, typename F> __device__ __forceinline__ void twiddle_series(C a, C s, F&& use) {
+    const C s2 = cmul(s, s), s3 = cmul(s2, s), s4 = cmul(s2, s2);
+    C b = a;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        use(4 * j, b);
+        use(4 * j + 1, cmul(b, s));
+        use(4 * j + 2, cmul(b, s2));
+        use(4 * j + 3, cmul(b, s3));
+        if (j < 3) b = cmul(b, s4);
+    }
+}
+
 template <typename T> struct Tile {
     static constexpr int W = 128 / (int)sizeof(cx_t<T>);   // columns per CTA: 8 (fp64) / 16 (fp32)
 };
@@ -74,11 +89,12 @@ k4_col(const void* __restrict__ xin, int in_kind, int conj_in, long long x_strid
         const long long b = u / tiles;
         const long long n2 = (u % tiles) * TC + g;
         prefetch(u + gridDim.x);
-        if (out_kind == OUT_WORK_TW && g == 0) {
-            // the store's W_L twiddles: one 128-byte line per (row, 8/16-column tile) into L1 now, so
-            // the twiddle loads after the transform hit L1 instead of waiting on L2
-#pragma unroll
-            for (int q = 0; q < G::EPT; ++q) prefetch_l1(twL + (tid + (long long)G::NT * q) * Cn + n2);
+        // the store's W_L^{n2 k1}, k1 = tid + NT q: two table entries loaded now (in flight during the
+        // transform), the sixteen twiddles formed from them after it
+        C tw_a = czero<C>(), tw_s = czero<C>();
+        if (out_kind == OUT_WORK_TW) {
+            tw_a = __ldg(twL + (long long)tid * Cn + n2);
+            tw_s = __ldg(twL + (long long)G::NT * Cn + n2);
         }
         C v[G::EPT];
 #pragma unroll
@@ -101,12 +117,24 @@ k4_col(const void* __restrict__ xin, int in_kind, int conj_in, long long x_strid
             v[q] = val;
         }
         block_fft<INV, LOG2R, NZ>(v, sm, tws, tid);
+        if (out_kind == OUT_WORK_TW) {
+            // Y[k1][n2] = v * W_L^{n2 k1} (forward twiddle of the four-step split)
+            if constexpr (G::EPT == 16) {
+                twiddle_series(tw_a, tw_s, [&](int q, C w) {
+                    Y[b * L + (tid + (long long)G::NT * q) * Cn + n2] = cmul(v[q], w);
+                });
+            } else {
+#pragma unroll
+                for (int q = 0; q < G::EPT; ++q) {
+                    const long long k1 = tid + (long long)G::NT * q;
+                    Y[b * L + k1 * Cn + n2] = cmul(v[q], __ldg(twL + k1 * Cn + n2));
+                }
+            }
+        }
 #pragma unroll
         for (int q = 0; q < G::EPT; ++q) {
             const long long k1 = tid + (long long)G::NT * q;
             if (out_kind == OUT_WORK_TW) {
-                // Y[k1][n2] = v * W_L^{n2 k1} (forward twiddle of the four-step split)
-                Y[b * L + k1 * Cn + n2] = cmul(v[q], __ldg(twL + k1 * Cn + n2));
             } else {
                 const long long n = k1 * Cn + n2;   // output sample index C n1 + n2
                 if (out_kind == OUT_CHIRP) {
@@ -179,13 +207,11 @@ k4_row(cx_t<T>* __restrict__ Y, int log2R, long long batch, const cx_t<T>* __res
             const C* kp = khat_p + k1 * Cn;
 #pragma unroll
             for (int q = 0; q < G::EPT; ++q) v[q] = cmul(v[q], __ldg(kp + tid + G::NT * q));
-            block_fft<true, LOG2C>(v, sm, tws, tid);
             const C* t = twL + k1 * Cn;
-#pragma unroll
-            for (int q = 0; q < G::EPT; ++q) {
-                const int n2 = tid + G::NT * q;
-                row[n2] = cmulc(v[q], __ldg(t + n2));   // x conj(W_L^{n2 k1})
-            }
+            const C tw_a = __ldg(t + tid), tw_s = __ldg(t + G::NT);   // in flight during the inverse FFT
+            block_fft<true, LOG2C>(v, sm, tws, tid);
+            // x conj(W_L^{n2 k1}), n2 = tid + NT q, the twiddles formed from two table entries
+            twiddle_series(tw_a, tw_s, [&](int q, C w) { row[tid + G::NT * q] = cmulc(v[q], w); });
         }
     }
 }
