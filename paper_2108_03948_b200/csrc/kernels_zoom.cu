@@ -995,7 +995,7 @@ k_zoom_pfir(const T* __restrict__ x, long long x_stride, long long batch, ZoomAr
 }
 
 // LH instantiated for these phase-row lengths (a row's taps are zero padded up to the next one)
-constexpr int kPfirLH[] = {1, 2, 3, 4, 5, 6, 8, 10, 12, 16};
+constexpr int kPfirLH[] = {1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 12, 16};
 
 template <typename T, int D, int LH>
 static cudaError_t run_pfir(const ZoomArgs& a, const T* x, long long xs, long long batch, const void* gph,
@@ -1026,7 +1026,9 @@ static cudaError_t pfir_lh(int lh, const ZoomArgs& a, const T* x, long long xs, 
         case 4: return run_pfir<T, D, 4>(a, x, xs, batch, gph, gnat, S, zb, z_stride, st);
         case 5: return run_pfir<T, D, 5>(a, x, xs, batch, gph, gnat, S, zb, z_stride, st);
         case 6: return run_pfir<T, D, 6>(a, x, xs, batch, gph, gnat, S, zb, z_stride, st);
+        case 7: return run_pfir<T, D, 7>(a, x, xs, batch, gph, gnat, S, zb, z_stride, st);
         case 8: return run_pfir<T, D, 8>(a, x, xs, batch, gph, gnat, S, zb, z_stride, st);
+        case 9: return run_pfir<T, D, 9>(a, x, xs, batch, gph, gnat, S, zb, z_stride, st);
         case 10: return run_pfir<T, D, 10>(a, x, xs, batch, gph, gnat, S, zb, z_stride, st);
         case 12: return run_pfir<T, D, 12>(a, x, xs, batch, gph, gnat, S, zb, z_stride, st);
         case 16: return run_pfir<T, D, 16>(a, x, xs, batch, gph, gnat, S, zb, z_stride, st);
@@ -1040,8 +1042,9 @@ int zoom_pfir_lh(const ZoomArgs& a) {
     if (D < 1 || D > 16 || (D & (D - 1))) return 0;
     const int need = (a.T + D - 1) / D;   // longest phase row
     if (D == 1) return need == 1 ? 1 : 0;
+    static const bool no_odd = std::getenv("SKG_PFIR_NO_ODD") != nullptr;   // A/B: pad rows to the even sizes
     for (int v : kPfirLH)
-        if (v >= need && v > 1) return v;
+        if (v >= need && v > 1 && !(no_odd && (v == 7 || v == 9))) return v;
     return 0;
 }
 
