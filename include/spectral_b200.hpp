@@ -11,6 +11,9 @@
 
 #include <complex>
 #include <cstddef>
+#include <iosfwd>
+#include <stdexcept>
+#include <string>
 #include <memory>
 #include <optional>
 #include <span>
@@ -135,6 +138,73 @@ ComplexBuffer filter_decimate_circular(std::span<const cplx> x, std::span<const 
 ZoomFftPlan make_zoom_plan(std::size_t input_len, double f1_hz, double f2_hz, double sample_rate_hz,
                            const ZoomOptions& opts = {});
 Spectrum zoom_fft(const ZoomFftPlan& plan, const Trace& t);
+
+
+// ---- errors.hpp:9-30 ---------------------------------------------------------------------------
+struct IoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ParseError : std::runtime_error {
+    ParseError(const std::string& msg, std::size_t line_no) : std::runtime_error(msg), line(line_no) {}
+    std::size_t line = 0;
+};
+struct FormatError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct InsufficientResolutionError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+// ---- trace / spectrum CSV (signals.hpp, spectra.hpp; byte-identical formats) -------------------
+Trace read_trace_csv(std::istream& in, const std::string& origin);      // signals.cpp:125-170
+Trace read_trace_csv_file(const std::string& path);
+void write_trace_csv(const Trace& t, std::ostream& out);                // signals.cpp:178-189
+void write_trace_csv_file(const Trace& t, const std::string& path);
+Spectrum read_spectrum_csv(std::istream& in, const std::string& origin);    // spectra.cpp:94-150
+Spectrum read_spectrum_csv_file(const std::string& path);
+void write_spectrum_csv(const Spectrum& s, std::ostream& out);              // spectra.cpp:63-72
+void write_spectrum_csv_file(const Spectrum& s, const std::string& path);
+
+// ---- resolution.hpp sizing helpers --------------------------------------------------------------
+std::size_t record_len_for_step(double sample_rate_hz, double target_step_hz);
+double fft_resolution(double sample_rate_hz, std::size_t n);
+std::size_t zeros_for_resolution(double sample_rate_hz, std::size_t n, double target_step_hz);
+std::size_t czt_len_for_matched_resolution(double f1_hz, double f2_hz, double sample_rate_hz, std::size_t n_fft);
+
+// ---- analysis.hpp: two-tone valley test and the resolvability sweep (both routes batched on the GPU)
+struct DipMetric {
+    bool resolved = false;
+    double dip_db = 0.0;
+    double f_peak_a_hz = 0.0;
+    double peak_a_db = 0.0;
+    double f_peak_b_hz = 0.0;
+    double peak_b_db = 0.0;
+    double f_valley_hz = 0.0;
+    double valley_db = 0.0;
+};
+DipMetric dip_metric(const Spectrum& s, double f_a_hz, double f_b_hz);
+struct ScanConfig {
+    double sample_rate_hz = 8000.0;
+    std::size_t n = 128;
+    double f1_hz = 100.0;
+    double f2_hz = 1000.0;
+    std::size_t m = 128;
+    double center_hz = 0.0;
+    double sep_start_hz = 10.0;
+    double sep_stop_hz = 200.0;
+    double sep_step_hz = 5.0;
+};
+struct ResolvabilityCurve {
+    ScanConfig config;
+    std::vector<double> separations_hz;
+    std::vector<DipMetric> fft_metrics;
+    std::vector<DipMetric> czt_metrics;
+    double min_resolved_fft_hz = 0.0;
+    double min_resolved_czt_hz = 0.0;
+    std::size_t fft_len = 0;
+};
+ResolvabilityCurve resolvability_scan(const ScanConfig& cfg);
+void write_resolvability_csv(const ResolvabilityCurve& c, std::ostream& out);   // serialize.cpp:141-154
 
 }  // namespace spectral
 

@@ -8,7 +8,13 @@
 #include <stdexcept>
 #include <string>
 
+#include <istream>
+#include <iterator>
+#include <ostream>
+
+#include "analysis.hpp"
 #include "host.hpp"
+#include "io.hpp"
 
 namespace skg {
 cudaError_t launch_dft_naive(const void* x, long long n, const void* tw, void* out, cudaStream_t st);
@@ -390,6 +396,154 @@ Spectrum zoom_fft(const ZoomFftPlan& plan, const Trace& t) {   // zoomfft.cpp:18
     s.f_step_hz = z.f_step_hz();
     s.source_n = z.n_fft;
     return s;
+}
+
+// ---- file formats and analysis (io.cpp / analysis.cpp), the runtime's errors mapped to the
+// reference's exception classes ------------------------------------------------------------------
+namespace {
+template <typename F> auto mapped(F&& f) -> decltype(f()) {
+    try {
+        return f();
+    } catch (const skg::ParseError& e) {
+        throw ParseError(e.what(), e.line);
+    } catch (const skg::FormatError& e) {
+        throw FormatError(e.what());
+    } catch (const skg::IoError& e) {
+        throw IoError(e.what());
+    } catch (const skg::InsufficientResolution& e) {
+        throw InsufficientResolutionError(e.what());
+    }
+}
+std::string slurp(std::istream& in) { return std::string(std::istreambuf_iterator<char>(in), {}); }
+Trace to_trace(skg::HostTrace&& h) {
+    Trace t;
+    t.samples = std::move(h.samples);
+    t.sample_rate_hz = h.fs;
+    t.t0_s = h.t0;
+    return t;
+}
+Spectrum to_spectrum(const skg::HostSpectrum& h) {
+    Spectrum s;
+    s.bins.resize(h.bins.size() / 2);
+    for (std::size_t k = 0; k < s.bins.size(); ++k) s.bins[k] = cplx(h.bins[2 * k], h.bins[2 * k + 1]);
+    s.f_start_hz = h.f_start;
+    s.f_step_hz = h.f_step;
+    s.source_n = h.source_n;
+    return s;
+}
+std::string trace_csv(const Trace& t) {
+    validate_trace(t);
+    std::string out = "time_s,amplitude\n";
+    const double dt = 1.0 / t.sample_rate_hz;
+    for (std::size_t i = 0; i < t.samples.size(); ++i) {
+        skg::append_g17(out, t.t0_s + static_cast<double>(i) * dt);
+        out += ',';
+        skg::append_g17(out, t.samples[i]);
+        out += '\n';
+    }
+    return out;
+}
+skg::DipMetricH to_h(const DipMetric& m) {
+    skg::DipMetricH h;
+    h.resolved = m.resolved;
+    h.dip_db = m.dip_db;
+    h.f_peak_a_hz = m.f_peak_a_hz;
+    h.peak_a_db = m.peak_a_db;
+    h.f_peak_b_hz = m.f_peak_b_hz;
+    h.peak_b_db = m.peak_b_db;
+    h.f_valley_hz = m.f_valley_hz;
+    h.valley_db = m.valley_db;
+    return h;
+}
+DipMetric from_h(const skg::DipMetricH& h) {
+    DipMetric m;
+    m.resolved = h.resolved;
+    m.dip_db = h.dip_db;
+    m.f_peak_a_hz = h.f_peak_a_hz;
+    m.peak_a_db = h.peak_a_db;
+    m.f_peak_b_hz = h.f_peak_b_hz;
+    m.peak_b_db = h.peak_b_db;
+    m.f_valley_hz = h.f_valley_hz;
+    m.valley_db = h.valley_db;
+    return m;
+}
+}  // namespace
+
+Trace read_trace_csv(std::istream& in, const std::string& origin) {
+    const std::string s = slurp(in);
+    return mapped([&] { return to_trace(skg::parse_trace_csv(s.data(), s.size(), origin)); });
+}
+Trace read_trace_csv_file(const std::string& path) {
+    return mapped([&] { return to_trace(skg::read_trace_csv_file(path)); });
+}
+void write_trace_csv(const Trace& t, std::ostream& out) {
+    out << trace_csv(t);
+    if (!out) throw IoError("trace csv: write failed");
+}
+void write_trace_csv_file(const Trace& t, const std::string& path) {
+    mapped([&] { skg::write_trace_csv_file(t.samples.data(), t.samples.size(), t.sample_rate_hz, t.t0_s, path); });
+}
+Spectrum read_spectrum_csv(std::istream& in, const std::string& origin) {
+    const std::string s = slurp(in);
+    return mapped([&] { return to_spectrum(skg::parse_spectrum_csv(s.data(), s.size(), origin)); });
+}
+Spectrum read_spectrum_csv_file(const std::string& path) {
+    return mapped([&] { return to_spectrum(skg::read_spectrum_csv_file(path)); });
+}
+void write_spectrum_csv(const Spectrum& s, std::ostream& out) {
+    out << skg::format_spectrum_csv(reinterpret_cast<const double*>(s.bins.data()), s.bins.size(), s.f_start_hz,
+                                    s.f_step_hz);
+    if (!out) throw IoError("spectrum csv: write failed");
+}
+void write_spectrum_csv_file(const Spectrum& s, const std::string& path) {
+    mapped([&] {
+        skg::write_spectrum_csv_file(reinterpret_cast<const double*>(s.bins.data()), s.bins.size(), s.f_start_hz,
+                                     s.f_step_hz, path);
+    });
+}
+
+std::size_t record_len_for_step(double fs, double step) { return skg::record_len_for_step(fs, step); }
+double fft_resolution(double fs, std::size_t n) { return skg::fft_resolution(fs, n); }
+std::size_t zeros_for_resolution(double fs, std::size_t n, double step) { return skg::zeros_for_resolution(fs, n, step); }
+std::size_t czt_len_for_matched_resolution(double f1, double f2, double fs, std::size_t n_fft) {
+    return skg::czt_len_for_matched_resolution(f1, f2, fs, n_fft);
+}
+
+DipMetric dip_metric(const Spectrum& s, double f_a, double f_b) {
+    return mapped([&] { return from_h(skg::dip_metric(s.bins.data(), s.bins.size(), s.f_start_hz, s.f_step_hz, f_a, f_b)); });
+}
+
+ResolvabilityCurve resolvability_scan(const ScanConfig& cfg) {
+    skg::ScanConfigH c;
+    c.sample_rate_hz = cfg.sample_rate_hz;
+    c.n = cfg.n;
+    c.f1_hz = cfg.f1_hz;
+    c.f2_hz = cfg.f2_hz;
+    c.m = cfg.m;
+    c.center_hz = cfg.center_hz;
+    c.sep_start_hz = cfg.sep_start_hz;
+    c.sep_stop_hz = cfg.sep_stop_hz;
+    c.sep_step_hz = cfg.sep_step_hz;
+    const skg::CurveH h = mapped([&] { return skg::resolvability_scan(c); });
+    ResolvabilityCurve r;
+    r.config = cfg;
+    r.config.center_hz = h.config.center_hz;
+    r.separations_hz = h.separations_hz;
+    for (const auto& m : h.fft_metrics) r.fft_metrics.push_back(from_h(m));
+    for (const auto& m : h.czt_metrics) r.czt_metrics.push_back(from_h(m));
+    r.min_resolved_fft_hz = h.min_resolved_fft_hz;
+    r.min_resolved_czt_hz = h.min_resolved_czt_hz;
+    r.fft_len = h.fft_len;
+    return r;
+}
+
+void write_resolvability_csv(const ResolvabilityCurve& c, std::ostream& out) {
+    skg::CurveH h;
+    h.separations_hz = c.separations_hz;
+    for (const auto& m : c.fft_metrics) h.fft_metrics.push_back(to_h(m));
+    for (const auto& m : c.czt_metrics) h.czt_metrics.push_back(to_h(m));
+    out << skg::format_resolvability_csv(h);
+    if (!out) throw IoError("resolvability csv: write failed");
 }
 
 }  // namespace spectral

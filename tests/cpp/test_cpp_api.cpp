@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdio>
 #include <random>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 
@@ -149,6 +150,56 @@ int main() {
     Trace wrong = pulse;
     wrong.samples.resize(400);
     CHECK(throws_invalid([&] { zoom_fft(zp, wrong); }));
+    // CSV formats (signals.cpp:125-189, spectra.cpp:63-150): stream round trips and the error classes
+    std::stringstream ts;
+    write_trace_csv(pulse, ts);
+    const Trace back = read_trace_csv(ts, "mem");
+    CHECK(back.samples == pulse.samples && back.size() == 500 && std::abs(back.sample_rate_hz - 10e12) < 1e-9 * 10e12);
+    std::stringstream bad_trace("t,x\n0,1\n1;2\n");
+    try {
+        read_trace_csv(bad_trace, "mem");
+        CHECK(false);
+    } catch (const ParseError& e) {
+        CHECK(e.line == 3 && std::string(e.what()) == "mem: malformed row at line 3");
+    }
+    std::stringstream one("0,1\n");
+    bool fmt = false;
+    try {
+        read_trace_csv(one, "mem");
+    } catch (const FormatError&) {
+        fmt = true;
+    }
+    CHECK(fmt);
+    std::stringstream ss;
+    write_spectrum_csv(s512, ss);
+    const Spectrum sback = read_spectrum_csv(ss, "mem");
+    CHECK(sback.size() == 512 && sback.bins == s512.bins && sback.f_start_hz == 0.0);
+    CHECK(std::abs(sback.f_step_hz - s512.f_step_hz) < 1e-6 * s512.f_step_hz);
+    bool io = false;
+    try {
+        read_trace_csv_file("/nonexistent/dir/trace.csv");
+    } catch (const IoError& e) {
+        io = std::string(e.what()) == "cannot open trace file: /nonexistent/dir/trace.csv";
+    }
+    CHECK(io);
+    // sizing helpers and the resolvability sweep (resolution.cpp, analysis.cpp:99-195): the reference's
+    // default sweep resolves both routes first at 45 Hz (tests/golden/scan.npz)
+    CHECK(record_len_for_step(10e12, 20e9) == 500 && zeros_for_resolution(8000.0, 128, 62.5) == 0);
+    const ResolvabilityCurve rc = resolvability_scan(ScanConfig{});
+    CHECK(rc.separations_hz.size() == 39 && rc.fft_len == 1138);
+    CHECK(rc.min_resolved_fft_hz == 45.0 && rc.min_resolved_czt_hz == 45.0);
+    std::stringstream cs2;
+    write_resolvability_csv(rc, cs2);
+    std::string first;
+    std::getline(cs2, first);
+    CHECK(first == "separation_hz,method,resolved,dip_db,f_peak_a_hz,peak_a_db,f_peak_b_hz,peak_b_db,f_valley_hz,valley_db");
+    bool ins = false;
+    try {
+        dip_metric(s512, 1e9, 2e9);
+    } catch (const InsufficientResolutionError&) {
+        ins = true;
+    }
+    CHECK(ins);
     std::printf("%s: %d failures\n", failures ? "FAILED" : "ok", failures);
     return failures ? 1 : 0;
 }
