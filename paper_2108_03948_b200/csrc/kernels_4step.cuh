@@ -13,6 +13,7 @@
 // Both passes are persistent (grid = resident CTAs) and pull the next tile into L2 while transforming.
 #pragma once
 
+#include "bulk_copy.cuh"
 #include "kernels_impl.cuh"
 
 namespace skg {
@@ -151,6 +152,16 @@ k4_col(const void* __restrict__ xin, int in_kind, int conj_in, long long x_strid
 
 // mode 0: rows lane-interleaved (TR = Tile::W rows per CTA), natural-order scatter store.
 // mode 1: rows contiguous per group, Bluestein middle in place.
+// Rows are staged one unit ahead by TMA bulk copies when the staging buffer fits beside the exchange
+// buffers (everything but mode 0 at C = 1024).
+template <typename T, int LOG2C, int MODE> struct RowCfg {
+    using G = FftGeom<LOG2C>;
+    static constexpr int ROWS = MODE == 0 ? Tile<T>::W : KCfg<T, LOG2C>::GROUPS;
+    static constexpr size_t BASE = ((size_t)ROWS * (G::SMEM + 1) + G::TW_ALLOC) * sizeof(cx_t<T>);
+    static constexpr size_t STAGE = 16 + (size_t)ROWS * (G::L + 16 / sizeof(cx_t<T>)) * sizeof(cx_t<T>);
+    static constexpr bool STG = BASE + STAGE <= 200 * 1024;
+    static constexpr size_t SMEM = BASE + (STG ? STAGE : 0);
+};
 template <typename T, int LOG2C, int MODE>
 __global__ void __launch_bounds__(MODE == 0 ? FftGeom<LOG2C>::NT * Tile<T>::W : KCfg<T, LOG2C>::BLOCK)
 k4_row(cx_t<T>* __restrict__ Y, int log2R, long long batch, const cx_t<T>* __restrict__ tw,
@@ -159,6 +170,7 @@ k4_row(cx_t<T>* __restrict__ Y, int log2R, long long batch, const cx_t<T>* __res
     using C = cx_t<T>;
     using G = FftGeom<LOG2C>;
     extern __shared__ __align__(16) unsigned char smraw[];
+    __shared__ __align__(8) uint64_t stg_bar;
     const long long R = 1LL << log2R;
     const long long Cn = G::L;
     const long long L = R * Cn;
@@ -174,25 +186,52 @@ k4_row(cx_t<T>* __restrict__ Y, int log2R, long long batch, const cx_t<T>* __res
     }
     C* sm = reinterpret_cast<C*>(smraw) + g * (G::SMEM + 1);
     C* tws = reinterpret_cast<C*>(smraw) + rows_per_cta * (G::SMEM + 1);
+    // staging for the NEXT unit's rows (one TMA bulk copy per row, rows padded by 16 bytes so the
+    // strided register loads below are conflict free), 16-byte aligned after the twiddle tables
+    constexpr int RS = (int)G::L + 16 / (int)sizeof(C);
+    C* stg = reinterpret_cast<C*>(
+        (reinterpret_cast<uintptr_t>(tws + G::TW_ALLOC) + 15) & ~static_cast<uintptr_t>(15));
     load_twiddles<LOG2C>(tws, tw);
+    if (threadIdx.x == 0) {
+        mbar_init(&stg_bar, 1);
+        mbar_fence_init();
+    }
     __syncthreads();
     const long long tiles = R / rows_per_cta;
     const long long units = tiles * batch;
-    for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+    // the unit's rows k1 = k1_0 .. k1_0 + rows - 1 are consecutive rows of Y: rows copies of Cn complex
+    auto issue = [&](long long un) {
+        if (threadIdx.x != 0 || un >= units) return;
+        fence_proxy_async_smem();   // earlier generic reads of stg before the async-proxy writes
+        const uint32_t row_bytes = (uint32_t)(Cn * sizeof(C));
+        mbar_arrive_expect_tx(&stg_bar, row_bytes * (uint32_t)rows_per_cta);
+        const C* src = Y + (un / tiles) * L + ((un % tiles) * rows_per_cta) * Cn;
+        for (int r = 0; r < rows_per_cta; ++r) bulk_g2s(stg + r * RS, src + r * Cn, row_bytes, &stg_bar);
+    };
+    constexpr bool STG = RowCfg<T, LOG2C, MODE>::STG;
+    if constexpr (STG) issue(blockIdx.x);
+    uint32_t parity = 0;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x, parity ^= 1u) {
         const long long b = u / tiles;
         const long long k1 = (u % tiles) * rows_per_cta + g;
         C* row = Y + b * L + k1 * Cn;
-        {   // the next unit's rows into L2 (one 128-byte line per lane and step)
-            const long long un = u + gridDim.x;
+        C v[G::EPT];
+        if constexpr (STG) {
+            mbar_wait(&stg_bar, parity);
+#pragma unroll
+            for (int q = 0; q < G::EPT; ++q) v[q] = stg[g * RS + tid + G::NT * q];
+            __syncthreads();            // every row read out of the staging buffer
+            issue(u + gridDim.x);       // the next unit streams in while this one is transformed
+        } else {
+            const long long un = u + gridDim.x;   // the next unit's rows into L2
             if (un < units) {
                 const C* rn = Y + (un / tiles) * L + ((un % tiles) * rows_per_cta + g) * Cn;
                 constexpr int per_line = 128 / (int)sizeof(C);
                 for (int i = tid * per_line; i < G::L; i += G::NT * per_line) prefetch_l2(rn + i);
             }
-        }
-        C v[G::EPT];
 #pragma unroll
-        for (int q = 0; q < G::EPT; ++q) v[q] = row[tid + G::NT * q];
+            for (int q = 0; q < G::EPT; ++q) v[q] = row[tid + G::NT * q];
+        }
         block_fft<false, LOG2C>(v, sm, tws, tid);
         if constexpr (MODE == 0) {
             C* o = out + b * out_stride;
@@ -267,7 +306,7 @@ cudaError_t launch_4step_row_impl(int log2C, int mode, void* Y, int log2R, long 
         const long long R = 1LL << log2R;
         if (mode == 0) {
             constexpr int TR = Tile<T>::W;
-            const size_t smem = ((size_t)TR * (G::SMEM + 1) + G::TW_ALLOC) * sizeof(C);
+            const size_t smem = RowCfg<T, LG, 0>::SMEM;
             auto kern = k4_row<T, LG, 0>;
             cudaError_t e = prep_smem(kern, smem);
             if (e != cudaSuccess) return e;
@@ -276,7 +315,7 @@ cudaError_t launch_4step_row_impl(int log2C, int mode, void* Y, int log2R, long 
                                                                        out_stride, scale, conj_out);
         } else {
             using K = KCfg<T, LG>;
-            const size_t smem = ((size_t)K::GROUPS * (G::SMEM + 1) + G::TW_ALLOC) * sizeof(C);
+            const size_t smem = RowCfg<T, LG, 1>::SMEM;
             auto kern = k4_row<T, LG, 1>;
             cudaError_t e = prep_smem(kern, smem);
             if (e != cudaSuccess) return e;
