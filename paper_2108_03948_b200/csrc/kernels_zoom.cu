@@ -862,8 +862,11 @@ namespace skg {
 // with <= 10-tap phase rows, cfg3: 0.102 -> 0.097 ms per call — else 3
 #define SKG_PFIR_MINB64(D, LH) ((D) <= 8 && (LH) <= 10 ? 4 : 3)
 #endif
+#ifndef SKG_PFIR_MINB32
+#define SKG_PFIR_MINB32 4
+#endif
 template <typename T, int D, int LH>
-__global__ void __launch_bounds__(128, sizeof(T) == 8 ? SKG_PFIR_MINB64(D, LH) : 4)
+__global__ void __launch_bounds__(128, sizeof(T) == 8 ? SKG_PFIR_MINB64(D, LH) : SKG_PFIR_MINB32)
 k_zoom_pfir(const T* __restrict__ x, long long x_stride, long long batch, ZoomArgs a, int gchunk, int tasks_per_rec,
             const cx_t<T>* __restrict__ gph, const cx_t<T>* __restrict__ gnat, const cx_t<T>* __restrict__ S,
             cx_t<T>* __restrict__ zb, long long z_stride) {
