@@ -156,3 +156,26 @@ def test_fft_spectrum_random_sizes_guarded(prec, case):
         assert rel_max_rows(got, want) <= TOL_F64, (n, L)
     else:
         assert rel_l2_rows(got, want) <= TOL_F32, (n, L)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("n,L", [(1024, 4096), (3000, 16384), (16384, 65536), (700, 1000)])
+def test_band_db_guards(prec, n, L):
+    """skg_fft_spectrum_band_batch (fused band + dB store, and the chirp / multi-pass fallback through
+    skg_band_db_batch) on poisoned strided input rows into canaried strided bins and dB rows."""
+    import ctypes as C
+    x = torch.from_numpy(W.sample_traces(23, n)).cuda()
+    x = x if prec == "f64" else x.float()
+    ref_bins, ref_db, _, _ = sk.fft_spectrum_band_batch(x, W.FS, 0.1e12, 3.0e12, L)
+    k_lo, cnt, _ = sk.band_bins(L, 0.0, W.FS / L, 0.1e12, 3.0e12)
+    bbuf, bins, boff, _ = _strided_out(23, cnt, ref_bins.dtype)
+    dbuf, db, doff, _ = _strided_out(23, cnt, ref_db.dtype)
+    xs = _strided_in(x)
+    P = sk.SKG_F64 if prec == "f64" else sk.SKG_F32
+    rc = sk.lib().skg_fft_spectrum_band_batch(n, L, P, k_lo, cnt, C.c_void_p(xs.data_ptr()), xs.stride(0), 23,
+                                              C.c_void_p(bins.data_ptr()), bins.stride(0),
+                                              C.c_void_p(db.data_ptr()), db.stride(0), sk._stream())
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert _same(bins, ref_bins) and _same(db, ref_db)
+    assert _canaries_ok(bbuf, boff, cnt) and _canaries_ok(dbuf, doff, cnt)
