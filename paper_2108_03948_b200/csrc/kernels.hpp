@@ -109,6 +109,12 @@ int zoom_pfir_lh(const ZoomArgs& a);
 cudaError_t launch_zoom_pfir(const ZoomArgs& a, bool f32, const void* x, long long xs, long long batch,
                              const void* gph, const void* gnat, const void* S, void* zb, long long z_stride,
                              cudaStream_t st);
+// the phase-lane FIR and the short FFT + band gather in one kernel (kernels_zoom_fused.cu); returns
+// cudaErrorNotSupported outside its instantiated geometry (the caller then runs the split route)
+cudaError_t launch_zoom_pfir_fft(const ZoomArgs& a, int lh, int log2n, bool f32, const void* x, long long xs,
+                                 long long batch, const void* gph, const void* gnat, const void* S, const void* tw,
+                                 int k_lo, int nbins, const void* band, void* out, long long out_stride,
+                                 cudaStream_t st);
 // constant-bank FIR specialised on (D, T) (kernels_zoom_cfir.cu); gph_host = the plan's phase-row
 // taps as interleaved fp64 complex (D x lh)
 bool zoom_cfir_available(const ZoomArgs& a);

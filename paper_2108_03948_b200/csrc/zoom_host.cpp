@@ -202,6 +202,18 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
     const bool pfir = !no_pfir && zoom_pfir_lh(a) > 0;
     static const bool no_cfir = getenv("SKG_ZOOM_NO_CFIR") != nullptr;
     const bool cfir = !no_cfir && zoom_cfir_available(a);
+    static const bool split_only = getenv("SKG_ZOOM_SPLIT") != nullptr;   // A/B: the two-kernel route
+    if (single && pfir && !force && !split_only) {
+        // FIR and short FFT in one kernel where instantiated (configs[2] geometry)
+        const cudaError_t e = launch_zoom_pfir_fft(a, zoom_pfir_lh(a), lg, f32, x, x_stride, batch, d.g.p, d.gn.p,
+                                                   d.sdec.p, stockham_twiddles(lg, f32), (int)k_lo, (int)bins(),
+                                                   d.band.p, out, out_stride, st);
+        if (e != cudaErrorNotSupported) {
+            check(e, "zoom fir+fft");
+            count_launch();
+            return;
+        }
+    }
     if (single && (wfir || pfir || cfir) && !force) {
         // warp-chunk FIR -> work rows (L2-resident chunk of records) -> FFT + band gather
         const size_t cs = f32 ? 8 : 16, es = f32 ? 4 : 8;

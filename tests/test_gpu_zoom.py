@@ -176,9 +176,11 @@ np.savez({out!r}, *outs)
 """
 
 
-@pytest.mark.parametrize("env", [{}, {"SKG_ZOOM_NO_PFIR": "1"}, {"SKG_ZOOM_NO_PFIR": "1", "SKG_ZOOM_NO_CFIR": "1"},
+@pytest.mark.parametrize("env", [{}, {"SKG_ZOOM_SPLIT": "1"}, {"SKG_ZOOM_NO_PFIR": "1"},
+                                 {"SKG_ZOOM_NO_PFIR": "1", "SKG_ZOOM_NO_CFIR": "1"},
                                  {"SKG_ZOOM_PATH": "fused"}, {"SKG_ZOOM_PATH": "unfused"}],
-                         ids=["split-pfir", "split-cfir", "split-wfir", "fused", "unfused"])
+                         ids=["default(pfir+fft one kernel where instantiated)", "split-pfir", "split-cfir", "split-wfir",
+                              "fused", "unfused"])
 def test_zoom_routes_match_oracle(env, tmp_path):
     """Every zoom route (phase-lane FIR, constant-bank FIR, warp-window FIR, fused single kernel,
     unfused FIR + FFT + gather) on linear/circular, power-of-two and odd decimations, against the oracle."""
