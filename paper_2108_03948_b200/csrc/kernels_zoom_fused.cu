@@ -3,6 +3,8 @@
 // record slot instead of the L2 work rows, and the CTA — whose four warps cover whole records —
 // then runs the n_fft-point Stockham transform on those slots and stores the signed band window
 // (x D x group-delay phase). One launch, no work-row round trip; the FIR is the same code.
+#include <cstdlib>
+
 #include "fft_device.cuh"
 #include "kernels.hpp"
 #include "kernels_impl.cuh"
@@ -13,11 +15,27 @@
 #ifndef SKG_PFIR_MINB32
 #define SKG_PFIR_MINB32 4
 #endif
+#ifndef SKG_ZF_MINB64
+#define SKG_ZF_MINB64 4
+#endif
 
 namespace skg {
 
+// a tap load the compiler may not hoist out of the task loop (volatile asm): keeps the taps' live
+// range inside the FIR phase, so the FFT phase gets their registers
+__device__ __forceinline__ double2 ld_tap(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float2 ld_tap(const float2* p) {
+    float2 v;
+    asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+    return v;
+}
+
 template <typename T, int D, int LH, int LOG2N>
-__global__ void __launch_bounds__(128, sizeof(T) == 8 ? 3 : SKG_PFIR_MINB32)
+__global__ void __launch_bounds__(128, sizeof(T) == 8 ? SKG_ZF_MINB64 : SKG_PFIR_MINB32)
 k_zoom_pfir_fft(const T* __restrict__ x, long long x_stride, long long batch, ZoomArgs a, int gchunk, int tasks_per_rec,
             const cx_t<T>* __restrict__ gph, const cx_t<T>* __restrict__ gnat, const cx_t<T>* __restrict__ S,
             const cx_t<T>* __restrict__ tw, int k_lo, int nbins, const cx_t<T>* __restrict__ band,
@@ -45,15 +63,19 @@ k_zoom_pfir_fft(const T* __restrict__ x, long long x_stride, long long batch, Zo
     auto ridx = [&](int m) { return FG::L >= 16 ? pad16(m) : m; };
     const int nout = a.nout, trim = a.trim, mwrap = a.mwrap;
     // this phase row's taps (rows are zero padded to a.lh >= LH entries... or shorter: guard)
-    C tp[LH];
-#pragma unroll
-    for (int l = 0; l < LH; ++l) tp[l] = l < a.lh ? __ldg(gph + ph * a.lh + l) : czero<C>();
     const long long ntasks = batch * tasks_per_rec;
     const long long tstride = (long long)gridDim.x * (blockDim.x >> 5);
     for (long long tbase = (long long)blockIdx.x * (blockDim.x >> 5); tbase < ntasks; tbase += tstride) {
       const long long task = tbase + warp;
       const bool has_task = task < ntasks;
       if (has_task) {
+        // this phase row's taps, re-read (L1) every task so they are not live across the FFT phase
+        C tp[LH];
+#pragma unroll
+        for (int l = 0; l < LH; ++l) {
+            tp[l] = czero<C>();
+            if (l < a.lh) tp[l] = ld_tap(gph + ph * a.lh + l);
+        }
         const long long b = task / tasks_per_rec;
         const int tk = (int)(task % tasks_per_rec);
         const T* xr = x + b * x_stride;
@@ -227,19 +249,25 @@ cudaError_t run_pfir_fft(const ZoomArgs& a, const T* x, long long xs, long long 
 }  // namespace
 
 // Measured against the split route (tools/zoom_time.py, cfg3, 4096 records): fp32 n_fft 512 0.065 ->
-// 0.062 ms; fp64 n_fft 512 0.094 -> 0.100 ms (the FFT phase forces the 168-register cap on the FIR),
-// n_fft 2048 slower in both precisions (one 2048-point record at a time per CTA: fp64 0.124 -> 0.207 ms).
-// So it is used for fp32 D = 8 with 9 / 10-tap rows and n_fft 512 only; everything else runs the split
-// route.
+// 0.062 ms; fp64 n_fft 512 0.094 -> 0.100 ms with the taps live across the FFT phase (168-register cap),
+// 0.094 -> 0.096 ms with them re-read per task (128 registers; SKG_ZF_F64=1 enables it), n_fft 2048
+// slower in both precisions (one 2048-point record at a time per CTA: fp64 0.124 -> 0.207 ms). So it is
+// used for fp32 D = 8 with 9 / 10-tap rows and n_fft 512; everything else runs the split route.
 cudaError_t launch_zoom_pfir_fft(const ZoomArgs& a, int lh, int log2n, bool f32, const void* x, long long xs,
                                  long long batch, const void* gph, const void* gnat, const void* S, const void* tw,
                                  int k_lo, int nbins, const void* band, void* out, long long out_stride,
                                  cudaStream_t st) {
-    if (!f32 || a.D != 8 || (lh != 9 && lh != 10) || log2n != 9) return cudaErrorNotSupported;
-    const float* xt = static_cast<const float*>(x);
-    if (lh == 9)
-        return run_pfir_fft<float, 8, 9, 9>(a, xt, xs, batch, gph, gnat, S, tw, k_lo, nbins, band, out, out_stride, st);
-    return run_pfir_fft<float, 8, 10, 9>(a, xt, xs, batch, gph, gnat, S, tw, k_lo, nbins, band, out, out_stride, st);
+    if (a.D != 8 || (lh != 9 && lh != 10) || log2n != 9) return cudaErrorNotSupported;
+    static const bool f64_on = std::getenv("SKG_ZF_F64") != nullptr;
+    if (!f32 && !f64_on) return cudaErrorNotSupported;
+    auto go = [&](auto tag) -> cudaError_t {
+        using T = decltype(tag);
+        const T* xt = static_cast<const T*>(x);
+        if (lh == 9)
+            return run_pfir_fft<T, 8, 9, 9>(a, xt, xs, batch, gph, gnat, S, tw, k_lo, nbins, band, out, out_stride, st);
+        return run_pfir_fft<T, 8, 10, 9>(a, xt, xs, batch, gph, gnat, S, tw, k_lo, nbins, band, out, out_stride, st);
+    };
+    return f32 ? go(float{}) : go(double{});
 }
 
 }  // namespace skg
