@@ -315,7 +315,7 @@ def bench_ours(args):
     ok_e2e = bool(torch.allclose(oh[:4].to(dev), out[:4]))
 
     extra = {}
-    if not args.quick:
+    if not args.quick and world == 1:   # single-GPU characterisation (the scaled metric is the headline)
         extra = bench_extras(args, sk, W, dev, world, pk)
 
     line = {
