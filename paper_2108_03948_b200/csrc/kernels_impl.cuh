@@ -90,9 +90,14 @@ k_fft_c2c(const cx_t<T>* in, long long in_stride, cx_t<T>* out, long long out_st
 #ifndef SKG_R2C_MINB_F32
 #define SKG_R2C_MINB_F32 3   // measured on configs[3]: 2 -> 1.269 ms, 3 -> 1.192 ms, 4 -> 1.215 ms
 #endif
+#ifndef SKG_R2C_MINB_F32_512
+#define SKG_R2C_MINB_F32_512 2   // 64 registers, 2 CTAs per SM: fp32 L = 16384 spectra 2.94 -> 2.69 ms per 256 MiB batch
+#endif
 template <typename T, int LOG2M> struct R2cCfg {
     // fp32 256-thread transforms: CTAs per SM the register cap targets (2 = 128 registers)
-    static constexpr int MINB = (sizeof(T) == 4 && KCfg<T, LOG2M>::BLOCK == 256) ? SKG_R2C_MINB_F32 : KCfg<T, LOG2M>::MINB;
+    static constexpr int MINB = (sizeof(T) == 4 && KCfg<T, LOG2M>::BLOCK == 256) ? SKG_R2C_MINB_F32
+                                : (sizeof(T) == 4 && KCfg<T, LOG2M>::BLOCK == 512) ? SKG_R2C_MINB_F32_512
+                                                                                   : KCfg<T, LOG2M>::MINB;
 };
 template <typename T, int LOG2M, int NZ, int MODE>
 __global__ void __launch_bounds__(KCfg<T, LOG2M>::BLOCK, R2cCfg<T, LOG2M>::MINB)
