@@ -211,8 +211,16 @@ k_fft_r2c(const T* __restrict__ x, long long x_stride, long long N, int vec, lon
 
 // ---------------------------------------------------------------------------------------
 // fused Bluestein CZT (CztPlan::execute, czt.cpp:116-130)
+#ifndef SKG_CZT_MINB_F32_512
+#define SKG_CZT_MINB_F32_512 1
+#endif
+template <typename T, int LOG2L> struct CztCfg {
+    // fp32 512-thread transforms (L = 8192): CTAs per SM the register cap targets
+    static constexpr int MINB = (sizeof(T) == 4 && KCfg<T, LOG2L>::BLOCK == 512) ? SKG_CZT_MINB_F32_512
+                                                                                 : KCfg<T, LOG2L>::MINB;
+};
 template <typename T, int LOG2L, int NZ, int NO>
-__global__ void __launch_bounds__(KCfg<T, LOG2L>::BLOCK, KCfg<T, LOG2L>::MINB)
+__global__ void __launch_bounds__(KCfg<T, LOG2L>::BLOCK, CztCfg<T, LOG2L>::MINB)
 k_czt(const void* __restrict__ xin, int complex_in, long long x_stride, long long N, long long M, long long batch,
       int nseg, long long seg_len, long long cin_stride, cx_t<T>* __restrict__ out, long long out_stride, const cx_t<T>* __restrict__ tw,
       const cx_t<T>* __restrict__ cin, const cx_t<T>* __restrict__ khat, const cx_t<T>* __restrict__ cout) {
