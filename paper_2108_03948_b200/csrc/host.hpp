@@ -184,10 +184,12 @@ class ZoomPlanG {                     // ZoomFftPlan + make_zoom_plan, zoomfft.h
     ZoomPlanG() = default;
     struct Dev {
         DevMem g, gn, sdec, wrap, band;
+        DevMem shift, hf;     // frequency-domain route: e^{-i2pi fc n/fs} (n < U), DFT_U of the taps
         std::vector<cd> gh;   // host copy of g (phase rows, fp64) for the constant-bank FIR
     };
     const Dev& dev(bool f32) const;
     void compute_band();
+    bool spectral_route_ok() const;
     mutable std::once_flag once_[2];
     mutable Dev dev_[2];
     std::unique_ptr<CztPlanG> bluestein_;   // n_fft not a power of two (dft_any route)

@@ -115,6 +115,11 @@ cudaError_t launch_zoom_pfir_fft(const ZoomArgs& a, int lh, int log2n, bool f32,
                                  long long batch, const void* gph, const void* gnat, const void* S, const void* tw,
                                  int k_lo, int nbins, const void* band, void* out, long long out_stride,
                                  cudaStream_t st);
+// circular zoom with n_fft = U / D in the frequency domain (kernels_zoom_spec.cu): one U-point FFT of
+// the shifted trace, x DFT_U(h), D-term alias sum per band bin; U = 2^log2u (2^8 .. single-CTA max)
+cudaError_t launch_zoom_spec(int log2u, bool f32, const void* x, long long xs, long long batch, const void* tw,
+                             const void* shift, const void* hf, int nf, int D, int k_lo, int nbins, const void* band,
+                             void* out, long long os, cudaStream_t st);
 // constant-bank FIR specialised on (D, T) (kernels_zoom_cfir.cu); gph_host = the plan's phase-row
 // taps as interleaved fp64 complex (D x lh)
 bool zoom_cfir_available(const ZoomArgs& a);

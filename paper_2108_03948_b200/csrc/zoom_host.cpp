@@ -99,6 +99,13 @@ std::unique_ptr<ZoomPlanG> ZoomPlanG::from_fields(const ZoomFields& f) {
     return p;
 }
 
+// the frequency-domain route's conditions: circular, no trim, the whole record used, a power-of-two
+// record, and the short FFT exactly the decimated length (no zero padding of u)
+bool ZoomPlanG::spectral_route_ok() const {
+    return circular && trim_samples == 0 && usable_len == input_len && is_pow2(usable_len) && decimation >= 1 &&
+           is_pow2(n_fft) && n_fft * decimation == usable_len;
+}
+
 double ZoomPlanG::f_step_hz() const {   // zoomfft.cpp:11-13
     return sample_rate_hz / (static_cast<double>(decimation) * static_cast<double>(n_fft));
 }
@@ -180,6 +187,22 @@ const ZoomPlanG::Dev& ZoomPlanG::dev(bool f32) const {
         for (long k = k_lo; k <= k_hi; ++k)
             band[static_cast<size_t>(k - k_lo)] = static_cast<double>(decimation) * cis_cycles(q, static_cast<double>(k));
         d.band = to_device(band.empty() ? std::vector<cd>{cd(0, 0)} : band, f32);
+        // frequency-domain route tables (circular, untrimmed, n_fft = U / D, U a power of two)
+        if (spectral_route_ok()) {
+            const size_t U = usable_len;
+            std::vector<cd> sh(U), hf(U, cd(0.0, 0.0));
+            for (size_t n = 0; n < U; ++n) sh[n] = cis_cycles(qc, static_cast<double>(n));   // zoomfft.cpp:174-177
+            // H[k] = sum_t h[t] e^{-i 2pi t k / U}, the exponent reduced exactly mod U
+            for (size_t k = 0; k < U; ++k) {
+                cd acc(0.0, 0.0);
+                for (int t = 0; t < T; ++t)
+                    acc += filter_taps[t] * cis_cycles(-1.0 / static_cast<double>(U),
+                                                       static_cast<double>((static_cast<size_t>(t) * k) % U));
+                hf[k] = acc;
+            }
+            d.shift = to_device(sh, f32);
+            d.hf = to_device(hf, f32);
+        }
     });
     return dev_[f32 ? 1 : 0];
 }
@@ -203,6 +226,22 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
     static const bool no_cfir = getenv("SKG_ZOOM_NO_CFIR") != nullptr;
     const bool cfir = !no_cfir && zoom_cfir_available(a);
     static const bool split_only = getenv("SKG_ZOOM_SPLIT") != nullptr;   // A/B: the two-kernel route
+    static const bool no_spec = getenv("SKG_ZOOM_NO_SPEC") != nullptr;
+    // circular, n_fft = U / D, long phase rows: FIR + decimation + short FFT as ONE U-point transform
+    // (an exact rewrite, kernels_zoom_spec.cu). Measured against the FIR routes: 2x faster at 101 taps,
+    // D = 4 (26 taps per phase row: fp64 0.40 -> 0.19-0.22 ms, fp32 0.50 -> 0.21-0.31 ms per 256 MiB),
+    // slower with short rows (cfg3, 9 taps per row: 0.095 -> 0.119 ms; D = 16, 7 per row: 0.14 -> 0.23
+    // ms), so it takes over above 12 taps per phase row (SKG_ZOOM_NO_SPEC=1: never)
+    const size_t taps_per_row = (filter_taps.size() + decimation - 1) / decimation;
+    if (!force && !split_only && !no_pfir && !no_cfir && !no_spec && spectral_route_ok() && taps_per_row > 12 &&
+        ilog2(usable_len) <= single_cta_max_log2(f32) && ilog2(usable_len) >= 8) {
+        check(launch_zoom_spec(ilog2(usable_len), f32, x, x_stride, batch, stockham_twiddles(ilog2(usable_len), f32),
+                               d.shift.p, d.hf.p, (int)n_fft, (int)decimation, (int)k_lo, (int)bins(), d.band.p, out,
+                               out_stride, st),
+              "zoom spectral");
+        count_launch();
+        return;
+    }
     if (single && pfir && !force && !split_only) {
         // FIR and short FFT in one kernel where instantiated (configs[2] geometry)
         const cudaError_t e = launch_zoom_pfir_fft(a, zoom_pfir_lh(a), lg, f32, x, x_stride, batch, d.g.p, d.gn.p,
