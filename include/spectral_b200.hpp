@@ -164,6 +164,8 @@ Spectrum read_spectrum_csv(std::istream& in, const std::string& origin);    // s
 Spectrum read_spectrum_csv_file(const std::string& path);
 void write_spectrum_csv(const Spectrum& s, std::ostream& out);              // spectra.cpp:63-72
 void write_spectrum_csv_file(const Spectrum& s, const std::string& path);
+void write_spectrum_json(const Spectrum& s, std::ostream& out);             // spectra.cpp:161-176
+void write_spectrum_json_file(const Spectrum& s, const std::string& path);
 
 // ---- resolution.hpp sizing helpers --------------------------------------------------------------
 std::size_t record_len_for_step(double sample_rate_hz, double target_step_hz);

@@ -114,6 +114,10 @@ SK_API sk_status sk_spectrum_slice_band(const sk_spectrum* s, double f_lo_hz, do
 /* CSV "frequency_hz,re,im,magnitude_db", %.17g rows (ref spectralkit.h:163-165, spectra.cpp:63-78);
  * byte-identical to the reference's writer */
 SK_API sk_status sk_spectrum_write_csv(const sk_spectrum* s, const char* path);
+/* ref spectralkit.h:166, spectra.cpp:161-183: {f_start_hz, f_step_hz, im[], magnitude_db[], re[],
+ * source_n}, two-space indentation, numbers in the reference JSON library's shortest form (Grisu2);
+ * byte-identical to the reference's writer */
+SK_API sk_status sk_spectrum_write_json(const sk_spectrum* s, const char* path);
 /* ref spectralkit.h:164, spectra.cpp:94-156: four fields per row, optional header, uniform axis
  * (1e-6 step tolerance); SK_ERR_PARSE / SK_ERR_FORMAT / SK_ERR_IO as the reference */
 SK_API sk_status sk_spectrum_read_csv(const char* path, sk_spectrum** out);

@@ -127,6 +127,7 @@ def _declare(L):
         "skg_spectra_write_csv": (st, [C.POINTER(C.c_char_p), sz, C.c_int, vp, sz, sz, dp, C.c_double, C.c_int,
                                        vp]),
         "sk_spectrum_read_csv": (st, [C.c_char_p, C.POINTER(vp)]),
+        "sk_spectrum_write_json": (st, [vp, C.c_char_p]),
         "sk_resolvability_write_csv": (st, [vp, C.c_char_p]),
         "sk_fft_resolution": (st, [C.c_double, sz, dp]),
         "sk_record_len_for_step": (st, [C.c_double, C.c_double, C.POINTER(sz)]),
@@ -336,6 +337,18 @@ def spectrum_write_csv(bins, f_start_hz, f_step_hz, path):
     _chk(lib().sk_spectrum_create(_p(re), _p(im), b.size, f_start_hz, f_step_hz, C.byref(h)))
     try:
         _chk(lib().sk_spectrum_write_csv(h, os.fsencode(path)))
+    finally:
+        lib().sk_spectrum_free(h)
+
+
+def spectrum_write_json(bins, f_start_hz, f_step_hz, path):
+    """sk_spectrum_write_json (spectra.cpp:161-183): the reference's JSON, byte for byte."""
+    b = np.ascontiguousarray(bins, np.complex128)
+    re, im = np.ascontiguousarray(b.real), np.ascontiguousarray(b.imag)
+    h = vp()
+    _chk(lib().sk_spectrum_create(_p(re), _p(im), b.size, f_start_hz, f_step_hz, C.byref(h)))
+    try:
+        _chk(lib().sk_spectrum_write_json(h, os.fsencode(path)))
     finally:
         lib().sk_spectrum_free(h)
 

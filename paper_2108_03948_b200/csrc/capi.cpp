@@ -396,6 +396,14 @@ sk_status sk_trace_write_csv(const sk_trace* t, const char* path) {
     return guarded([&] { skg::write_trace_csv_file(t->samples.data(), t->samples.size(), t->fs, t->t0, path); });
 }
 
+sk_status sk_spectrum_write_json(const sk_spectrum* s, const char* path) {
+    if (!s || !path) return bad_arg("sk_spectrum_write_json: null argument");
+    return guarded([&] {
+        skg::write_spectrum_json_file(reinterpret_cast<const double*>(s->bins.data()), s->bins.size(), s->f_start,
+                                      s->f_step, s->source_n, path);
+    });
+}
+
 sk_status sk_spectrum_read_csv(const char* path, sk_spectrum** out) {
     if (!path || !out) return bad_arg("sk_spectrum_read_csv: null argument");
     return guarded([&] {
@@ -576,7 +584,7 @@ size_t skg_resolvability_fft_len(const sk_resolvability_curve* c) { return c ? c
 sk_status sk_resolvability_write_csv(const sk_resolvability_curve* c, const char* path) {
     if (!c || !path) return bad_arg("sk_resolvability_write_csv: null argument");
     return guarded([&] {
-        skg::write_text_file(skg::format_resolvability_csv(c->c), path, "cannot open for writing: ", "resolvability");
+        skg::write_text_file(skg::format_resolvability_csv(c->c), path, "cannot open for writing: ", "resolvability csv");
     });
 }
 

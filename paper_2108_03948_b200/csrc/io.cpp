@@ -14,6 +14,8 @@
 #include <string_view>
 #include <thread>
 
+#include "grisu_powers.hpp"
+
 namespace skg {
 
 namespace {
@@ -63,10 +65,205 @@ FILE* open_out(const std::string& path, const char* what) {
 void finish_out(FILE* f, bool ok, const char* what) {
     if (f != stdout) ok = (fclose(f) == 0) && ok;
     else ok = (fflush(f) == 0) && ok;
-    if (!ok) throw IoError(std::string(what) + " csv: write failed");
+    if (!ok) throw IoError(std::string(what) + ": write failed");
+}
+
+// ---- JSON numbers: Grisu2 (Loitsch, "Printing floating-point numbers quickly and accurately with
+// integers", PLDI 2010) with the conservative boundaries, then the decimal layout the reference's JSON
+// library prints (plain notation for decimal exponents in (-4, 15], else d.ddde+XX; integral values
+// keep ".0"). The reference's spectrum JSON (spectra.cpp:161-176) formats every double this way.
+namespace grisu {
+struct Fp {
+    uint64_t f;
+    int e;
+};
+Fp mul(Fp x, Fp y) {   // the upper 64 bits of the 128-bit product, rounded half up
+    const unsigned __int128 p = (unsigned __int128)x.f * y.f;
+    const uint64_t h = (uint64_t)(p >> 64), l = (uint64_t)p;
+    return {h + (l >> 63), x.e + y.e + 64};
+}
+Fp normalize(Fp x) {
+    while ((x.f >> 63) == 0) {
+        x.f <<= 1;
+        x.e--;
+    }
+    return x;
+}
+Fp normalize_to(Fp x, int e) { return {x.f << (x.e - e), e}; }
+
+void boundaries(double value, Fp& w, Fp& lo, Fp& hi) {
+    uint64_t bits;
+    std::memcpy(&bits, &value, sizeof bits);
+    const uint64_t E = bits >> 52, F = bits & ((uint64_t{1} << 52) - 1);
+    constexpr int kBias = 1075, kMinExp = 1 - kBias;
+    const Fp v = E == 0 ? Fp{F, kMinExp} : Fp{F + (uint64_t{1} << 52), (int)E - kBias};
+    const bool lower_closer = F == 0 && E > 1;   // the gap below a power of two is half the gap above
+    const Fp m_plus{2 * v.f + 1, v.e - 1};
+    const Fp m_minus = lower_closer ? Fp{4 * v.f - 1, v.e - 2} : Fp{2 * v.f - 1, v.e - 1};
+    hi = normalize(m_plus);
+    lo = normalize_to(m_minus, hi.e);
+    w = normalize(v);
+}
+
+int largest_pow10(uint32_t n, uint32_t& p) {
+    static const uint32_t t[] = {1u, 10u, 100u, 1000u, 10000u, 100000u, 1000000u, 10000000u, 100000000u, 1000000000u};
+    int k = 10;
+    while (k > 1 && n < t[k - 1]) --k;
+    p = t[k - 1];
+    return k;
+}
+
+void round_weed(char* buf, int len, uint64_t dist, uint64_t delta, uint64_t rest, uint64_t ten_k) {
+    while (rest < dist && delta - rest >= ten_k && (rest + ten_k < dist || dist - rest > rest + ten_k - dist)) {
+        buf[len - 1]--;
+        rest += ten_k;
+    }
+}
+
+// shortest-in-practice digits of value > 0: buf[0..len) x 10^dexp
+void digits(double value, char* buf, int& len, int& dexp) {
+    Fp w, lo, hi;
+    boundaries(value, w, lo, hi);
+    constexpr int kAlpha = -60;
+    const int f = kAlpha - hi.e - 1;
+    const int k = (f * 78913) / (1 << 18) + (f > 0 ? 1 : 0);
+    const int index = (-kCachedPowersMinDecExp + k + (kCachedPowersDecStep - 1)) / kCachedPowersDecStep;
+    const CachedPow10 c = kCachedPowers[index];
+    const Fp ck{c.f, c.e};
+    const Fp W = mul(w, ck), Wlo = mul(lo, ck), Whi = mul(hi, ck);
+    const Fp Mm{Wlo.f + 1, Wlo.e}, Mp{Whi.f - 1, Whi.e};
+    dexp = -c.k;
+    len = 0;
+    uint64_t delta = Mp.f - Mm.f, dist = Mp.f - W.f;
+    const Fp one{uint64_t{1} << -Mp.e, Mp.e};
+    uint32_t p1 = (uint32_t)(Mp.f >> -one.e);
+    uint64_t p2 = Mp.f & (one.f - 1);
+    uint32_t pow10;
+    int n = largest_pow10(p1, pow10);
+    while (n > 0) {
+        const uint32_t d = p1 / pow10, r = p1 % pow10;
+        buf[len++] = (char)('0' + d);
+        p1 = r;
+        n--;
+        const uint64_t rest = (uint64_t{p1} << -one.e) + p2;
+        if (rest <= delta) {
+            dexp += n;
+            round_weed(buf, len, dist, delta, rest, uint64_t{pow10} << -one.e);
+            return;
+        }
+        pow10 /= 10;
+    }
+    int m = 0;
+    for (;;) {
+        p2 *= 10;
+        const uint64_t d = p2 >> -one.e, r = p2 & (one.f - 1);
+        buf[len++] = (char)('0' + d);
+        p2 = r;
+        m++;
+        delta *= 10;
+        dist *= 10;
+        if (p2 <= delta) break;
+    }
+    dexp -= m;
+    round_weed(buf, len, dist, delta, p2, one.f);
+}
+}  // namespace grisu
+
+// one finite double as the reference's JSON library prints it
+void append_json_number(std::string& out, double v) {
+    if (!std::isfinite(v)) {
+        out += "null";
+        return;
+    }
+    if (std::signbit(v)) {
+        out += '-';
+        v = -v;
+    }
+    if (v == 0.0) {
+        out += "0.0";
+        return;
+    }
+    char d[32];
+    int k = 0, dexp = 0;
+    grisu::digits(v, d, k, dexp);
+    const int n = k + dexp;   // decimal point position relative to the digits
+    constexpr int kMin = -4, kMax = 15;
+    if (k <= n && n <= kMax) {   // digits000.0
+        out.append(d, k);
+        out.append((size_t)(n - k), '0');
+        out += ".0";
+    } else if (0 < n && n <= kMax) {   // dig.its
+        out.append(d, n);
+        out += '.';
+        out.append(d + n, k - n);
+    } else if (kMin < n && n <= 0) {   // 0.000digits
+        out += "0.";
+        out.append((size_t)-n, '0');
+        out.append(d, k);
+    } else {   // d.igitse+XX
+        out += d[0];
+        if (k > 1) {
+            out += '.';
+            out.append(d + 1, k - 1);
+        }
+        int e = n - 1;
+        out += 'e';
+        out += e < 0 ? '-' : '+';
+        if (e < 0) e = -e;
+        char eb[4];
+        int el = 0;
+        if (e < 10) {
+            eb[el++] = '0';
+            eb[el++] = (char)('0' + e);
+        } else if (e < 100) {
+            eb[el++] = (char)('0' + e / 10);
+            eb[el++] = (char)('0' + e % 10);
+        } else {
+            eb[el++] = (char)('0' + e / 100);
+            eb[el++] = (char)('0' + (e / 10) % 10);
+            eb[el++] = (char)('0' + e % 10);
+        }
+        out.append(eb, el);
+    }
 }
 
 }  // namespace
+
+std::string format_spectrum_json(const double* b, size_t n, double f_start, double f_step, size_t source_n) {
+    // spectra.cpp:161-176: an object with keys in sorted order, two-space indentation, one array element
+    // per line, then the writer's newline
+    std::string out = "{\n  \"f_start_hz\": ";
+    append_json_number(out, f_start);
+    out += ",\n  \"f_step_hz\": ";
+    append_json_number(out, f_step);
+    auto array = [&](const char* key, auto&& value) {
+        out += ",\n  \"";
+        out += key;
+        out += "\": ";
+        if (n == 0) {
+            out += "[]";
+            return;
+        }
+        out += "[\n";
+        for (size_t k = 0; k < n; ++k) {
+            out += "    ";
+            append_json_number(out, value(k));
+            out += k + 1 < n ? ",\n" : "\n";
+        }
+        out += "  ]";
+    };
+    array("im", [&](size_t k) { return b[2 * k + 1]; });
+    array("magnitude_db", [&](size_t k) { return magnitude_db(b[2 * k], b[2 * k + 1]); });
+    array("re", [&](size_t k) { return b[2 * k]; });
+    out += ",\n  \"source_n\": " + std::to_string(source_n) + "\n}\n";
+    return out;
+}
+
+void write_spectrum_json_file(const double* b, size_t n, double f_start, double f_step, size_t source_n,
+                              const std::string& path) {
+    write_text_file(format_spectrum_json(b, n, f_start, f_step, source_n), path, "cannot open spectrum file for writing: ",
+                    "spectrum json");
+}
 
 HostTrace parse_trace_csv(const char* data, size_t len, const std::string& origin) {
     std::vector<double> times, values;
@@ -243,7 +440,7 @@ void write_trace_csv_file(const double* samples, size_t n, double fs, double t0,
         out.append(buf, p - buf);
     }
     const bool ok = fwrite(out.data(), 1, out.size(), f) == out.size();
-    finish_out(f, ok, "trace");
+    finish_out(f, ok, "trace csv");
 }
 
 std::string format_spectrum_csv(const double* b, size_t n, double f_start, double f_step) {
@@ -270,7 +467,7 @@ void write_spectrum_csv_file(const double* b, size_t n, double f_start, double f
     FILE* f = open_out(path, "spectrum");
     const std::string out = format_spectrum_csv(b, n, f_start, f_step);
     const bool ok = fwrite(out.data(), 1, out.size(), f) == out.size();
-    finish_out(f, ok, "spectrum");
+    finish_out(f, ok, "spectrum csv");
 }
 
 void parallel_for(size_t count, int threads, const std::function<void(size_t)>& fn) {

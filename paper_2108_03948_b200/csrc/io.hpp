@@ -46,6 +46,12 @@ void write_trace_csv_file(const double* samples, size_t n, double fs, double t0,
 // write_spectrum_csv (spectra.cpp:63-72): "frequency_hz,re,im,magnitude_db" + %.17g rows
 void write_spectrum_csv_file(const double* bins_interleaved, size_t n, double f_start, double f_step,
                              const std::string& path);
+// write_spectrum_json (spectra.cpp:161-183): the reference's JSON object, numbers as its JSON library
+// prints them (Grisu2 shortest digits); byte-identical files
+std::string format_spectrum_json(const double* bins_interleaved, size_t n, double f_start, double f_step,
+                                 size_t source_n);
+void write_spectrum_json_file(const double* bins_interleaved, size_t n, double f_start, double f_step,
+                              size_t source_n, const std::string& path);
 // the CSV body as a string (the same bytes the file gets)
 std::string format_spectrum_csv(const double* bins_interleaved, size_t n, double f_start, double f_step);
 

@@ -502,6 +502,18 @@ void write_spectrum_csv_file(const Spectrum& s, const std::string& path) {
     });
 }
 
+void write_spectrum_json(const Spectrum& s, std::ostream& out) {
+    out << skg::format_spectrum_json(reinterpret_cast<const double*>(s.bins.data()), s.bins.size(), s.f_start_hz,
+                                     s.f_step_hz, s.source_n);
+    if (!out) throw IoError("spectrum json: write failed");
+}
+void write_spectrum_json_file(const Spectrum& s, const std::string& path) {
+    mapped([&] {
+        skg::write_spectrum_json_file(reinterpret_cast<const double*>(s.bins.data()), s.bins.size(), s.f_start_hz,
+                                      s.f_step_hz, s.source_n, path);
+    });
+}
+
 std::size_t record_len_for_step(double fs, double step) { return skg::record_len_for_step(fs, step); }
 double fft_resolution(double fs, std::size_t n) { return skg::fft_resolution(fs, n); }
 std::size_t zeros_for_resolution(double fs, std::size_t n, double step) { return skg::zeros_for_resolution(fs, n, step); }

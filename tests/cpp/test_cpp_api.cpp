@@ -175,6 +175,10 @@ int main() {
     const Spectrum sback = read_spectrum_csv(ss, "mem");
     CHECK(sback.size() == 512 && sback.bins == s512.bins && sback.f_start_hz == 0.0);
     CHECK(std::abs(sback.f_step_hz - s512.f_step_hz) < 1e-6 * s512.f_step_hz);
+    std::stringstream js;
+    write_spectrum_json(s512, js);
+    const std::string jtxt = js.str();
+    CHECK(jtxt.rfind("{\n  \"f_start_hz\": 0.0,\n", 0) == 0 && jtxt.find("\"source_n\": 512\n}\n") != std::string::npos);
     bool io = false;
     try {
         read_trace_csv_file("/nonexistent/dir/trace.csv");

@@ -333,6 +333,27 @@ def main():
             cv[f"src_{name}"], cv[f"smsg_{name}"] = rc, msg.replace(path, "<PATH>")
             if rc == 0:
                 cv[f"sX_{name}"], cv[f"sf0_{name}"], cv[f"sdf_{name}"], cv[f"sn_{name}"] = X, f0, df, sn
+        # spectrum JSON (spectra.cpp:161-183): the band spectrum, the odd values, and random bit patterns
+        R.sk_spectrum_write_json.argtypes = [C.c_void_p, C.c_char_p]
+
+        def ref_json(bins, f0, df):
+            re, im = np.ascontiguousarray(np.real(bins)), np.ascontiguousarray(np.imag(bins))
+            h = C.c_void_p()
+            assert R.sk_spectrum_create(P(re), P(im), re.size, f0, df, C.byref(h)) == 0
+            path = os.path.join(td, "s.json")
+            assert R.sk_spectrum_write_json(h, path.encode()) == 0
+            R.sk_spectrum_free(h)
+            with open(path, "rb") as f:
+                return np.frombuffer(f.read(), np.uint8)
+        cv["j_spec"] = ref_json(bd["thz_X"], float(bd["thz_f0"]), float(bd["thz_df"]))
+        cv["j_odd"] = ref_json(odd, -5.0, 1.0 / 3.0)
+        rj = np.random.default_rng(11)
+        bits = rj.integers(0, 2**63, 3000, dtype=np.uint64) | (rj.integers(0, 2, 3000, dtype=np.uint64) << np.uint64(63))
+        rv = bits.view(np.float64)
+        rv = rv[np.isfinite(rv)]
+        rv = rv[: rv.size // 2 * 2]
+        cv["j_rand_X"] = rv[0::2] + 1j * rv[1::2]
+        cv["j_rand"] = ref_json(cv["j_rand_X"], 0.0, 4882812500.0)
         rt_path = os.path.join(td, "t.csv")   # the written trace read back by the reference
         rc, _, x, fs, t0 = ref_trace_read_csv(rt_path)
         cv["rt_x"], cv["rt_fs"], cv["rt_t0"] = x, fs, t0

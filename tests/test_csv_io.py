@@ -111,3 +111,45 @@ def test_sizing_helpers():
         sk.czt_len_for_matched_resolution(0.0, 6e12, 10e12, 100)
     with pytest.raises(sk.SkError, match="positive and finite"):
         sk.fft_resolution(0.0, 10)
+
+
+def test_spectrum_json_byte_identical(golden, tmp_path):
+    """sk_spectrum_write_json (spectra.cpp:161-183) against the reference's files: the band spectrum,
+    adversarial values (subnormal, huge, negative zero, non-terminating), 1500 random bit patterns."""
+    g = golden("csv")
+    for name, bins, f0, df in (("j_spec", g["w_spec_X"], float(g["w_spec_f0"]), float(g["w_spec_df"])),
+                               ("j_odd", g["w_odd_X"], -5.0, 1.0 / 3.0),
+                               ("j_rand", g["j_rand_X"], 0.0, 4882812500.0)):
+        p = tmp_path / f"{name}.json"
+        sk.spectrum_write_json(bins, f0, df, str(p))
+        assert p.read_bytes() == bytes(g[name]), name
+
+
+def test_spectrum_json_differential_vs_reference(tmp_path):
+    """Number formatting against the compiled reference on 200k random doubles (bit patterns over the
+    whole range, powers of two and their neighbours); runs where oracle/_ref is built."""
+    import ctypes as C
+
+    import oracle as O
+    R = O.ref()
+    if R is None:
+        pytest.skip("oracle/_ref not built here")
+    R.sk_spectrum_create.argtypes = [O.dp, O.dp, C.c_size_t, C.c_double, C.c_double, C.POINTER(C.c_void_p)]
+    R.sk_spectrum_write_json.argtypes = [C.c_void_p, C.c_char_p]
+    R.sk_spectrum_free.argtypes = [C.c_void_p]
+    rng = np.random.default_rng(2024)
+    bits = rng.integers(0, 2**63, 150000, dtype=np.uint64) | (rng.integers(0, 2, 150000, dtype=np.uint64) << np.uint64(63))
+    v = bits.view(np.float64)
+    p2 = np.ldexp(1.0, rng.integers(-1074, 1023, 20000))
+    v = np.concatenate([v[np.isfinite(v)], p2, np.nextafter(p2, np.inf), np.nextafter(p2, 0)])
+    v = v[: v.size // 2 * 2]
+    bins = v[0::2] + 1j * v[1::2]
+    re, im = np.ascontiguousarray(bins.real), np.ascontiguousarray(bins.imag)
+    h = C.c_void_p()
+    assert R.sk_spectrum_create(O._p(re), O._p(im), re.size, 1.5, 0.1, C.byref(h)) == 0
+    ref = tmp_path / "ref.json"
+    assert R.sk_spectrum_write_json(h, str(ref).encode()) == 0
+    R.sk_spectrum_free(h)
+    ours = tmp_path / "ours.json"
+    sk.spectrum_write_json(bins, 1.5, 0.1, str(ours))
+    assert ours.read_bytes() == ref.read_bytes()
