@@ -207,6 +207,7 @@ struct ResolvabilityCurve {
 };
 ResolvabilityCurve resolvability_scan(const ScanConfig& cfg);
 void write_resolvability_csv(const ResolvabilityCurve& c, std::ostream& out);   // serialize.cpp:141-154
+void write_resolvability_json(const ResolvabilityCurve& c, std::ostream& out);  // serialize.cpp:113-135
 
 }  // namespace spectral
 

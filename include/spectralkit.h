@@ -162,6 +162,8 @@ SK_API double sk_resolvability_min_fft(const sk_resolvability_curve* c);
 SK_API double sk_resolvability_min_czt(const sk_resolvability_curve* c);
 /* ref spectralkit.h:239, serialize.cpp:141-154: byte-identical CSV of the curve */
 SK_API sk_status sk_resolvability_write_csv(const sk_resolvability_curve* c, const char* path);
+/* ref spectralkit.h:241, serialize.cpp:113-135 */
+SK_API sk_status sk_resolvability_write_json(const sk_resolvability_curve* c, const char* path);
 
 /* Zoom pipeline (ref spectralkit.h:170-195, capi.cpp:515-564). Same struct layout. */
 typedef struct sk_zoom_options {

@@ -129,6 +129,7 @@ def _declare(L):
         "sk_spectrum_read_csv": (st, [C.c_char_p, C.POINTER(vp)]),
         "sk_spectrum_write_json": (st, [vp, C.c_char_p]),
         "sk_resolvability_write_csv": (st, [vp, C.c_char_p]),
+        "sk_resolvability_write_json": (st, [vp, C.c_char_p]),
         "sk_fft_resolution": (st, [C.c_double, sz, dp]),
         "sk_record_len_for_step": (st, [C.c_double, C.c_double, C.POINTER(sz)]),
         "sk_zeros_for_resolution": (st, [C.c_double, sz, C.c_double, C.POINTER(sz)]),
@@ -431,7 +432,7 @@ def czt_len_for_matched_resolution(f1, f2, fs, n_fft):
     return v.value
 
 
-def resolvability_scan(csv_path=None, **cfg):
+def resolvability_scan(csv_path=None, json_path=None, **cfg):
     """sk_resolvability_scan (analysis.cpp:99-195) on the GPU: dict with separations_hz, fft / czt
     metric rows (resolved, dip_db, f_peak_a, peak_a_db, f_peak_b, peak_b_db, f_valley, valley_db),
     min_resolved_fft_hz / _czt_hz (NaN when none) and fft_len; csv_path: also write the curve
@@ -442,6 +443,8 @@ def resolvability_scan(csv_path=None, **cfg):
     try:
         if csv_path is not None:
             _chk(lib().sk_resolvability_write_csv(h, os.fsencode(csv_path)))
+        if json_path is not None:
+            _chk(lib().sk_resolvability_write_json(h, os.fsencode(json_path)))
         sep, fm, cm, mf, mc = read_curve(lib(), h)
         return {"separations_hz": sep, "fft": fm, "czt": cm, "min_resolved_fft_hz": mf, "min_resolved_czt_hz": mc,
                 "fft_len": int(lib().skg_resolvability_fft_len(h))}

@@ -80,6 +80,81 @@ std::string format_resolvability_csv(const CurveH& c) {
     return out;
 }
 
+std::string format_resolvability_json(const CurveH& c) {
+    // keys in sorted order at every level (the library's object is an ordered map), two-space indent
+    std::string o = "{\n  \"config\": {\n";
+    auto num = [&](const char* ind, const char* key, double v, bool last) {
+        o += ind;
+        o += '"';
+        o += key;
+        o += "\": ";
+        json_number(o, v);
+        o += last ? "\n" : ",\n";
+    };
+    auto uint = [&](const char* ind, const char* key, size_t v, bool last) {
+        o += ind;
+        o += '"';
+        o += key;
+        o += "\": " + std::to_string(v) + (last ? "\n" : ",\n");
+    };
+    const char* i4 = "    ";
+    num(i4, "center_hz", c.config.center_hz, false);
+    num(i4, "f1_hz", c.config.f1_hz, false);
+    num(i4, "f2_hz", c.config.f2_hz, false);
+    uint(i4, "m", c.config.m, false);
+    uint(i4, "n", c.config.n, false);
+    num(i4, "sample_rate_hz", c.config.sample_rate_hz, false);
+    num(i4, "sep_start_hz", c.config.sep_start_hz, false);
+    num(i4, "sep_step_hz", c.config.sep_step_hz, false);
+    num(i4, "sep_stop_hz", c.config.sep_stop_hz, true);
+    o += "  },\n";
+    auto metrics = [&](const char* key, const std::vector<DipMetricH>& ms) {
+        o += "  \"";
+        o += key;
+        o += "\": ";
+        if (ms.empty()) {
+            o += "[],\n";
+            return;
+        }
+        o += "[\n";
+        const char* i6 = "      ";
+        for (size_t i = 0; i < ms.size(); ++i) {
+            const DipMetricH& m = ms[i];
+            o += "    {\n";
+            num(i6, "dip_db", m.dip_db, false);
+            num(i6, "f_peak_a_hz", m.f_peak_a_hz, false);
+            num(i6, "f_peak_b_hz", m.f_peak_b_hz, false);
+            num(i6, "f_valley_hz", m.f_valley_hz, false);
+            num(i6, "peak_a_db", m.peak_a_db, false);
+            num(i6, "peak_b_db", m.peak_b_db, false);
+            o += i6;
+            o += m.resolved ? "\"resolved\": true,\n" : "\"resolved\": false,\n";
+            num(i6, "valley_db", m.valley_db, true);
+            o += i + 1 < ms.size() ? "    },\n" : "    }\n";
+        }
+        o += "  ],\n";
+    };
+    metrics("czt", c.czt_metrics);
+    metrics("fft", c.fft_metrics);
+    uint("  ", "fft_len", c.fft_len, false);
+    num("  ", "min_resolved_czt_hz", c.min_resolved_czt_hz, false);
+    num("  ", "min_resolved_fft_hz", c.min_resolved_fft_hz, false);
+    o += "  \"separations_hz\": ";
+    if (c.separations_hz.empty()) {
+        o += "[],\n";
+    } else {
+        o += "[\n";
+        for (size_t i = 0; i < c.separations_hz.size(); ++i) {
+            o += "    ";
+            json_number(o, c.separations_hz[i]);
+            o += i + 1 < c.separations_hz.size() ? ",\n" : "\n";
+        }
+        o += "  ],\n";
+    }
+    o += "  \"v\": 1\n}\n";
+    return o;
+}
+
 size_t zeros_for_resolution(double fs, size_t n, double step) {
     check_rate(fs);
     if (n == 0) throw std::invalid_argument("zeros_for_resolution: n must be >= 1");

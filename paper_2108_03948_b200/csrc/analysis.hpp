@@ -41,6 +41,8 @@ CurveH resolvability_scan(const ScanConfigH& cfg, int threads = 0);
 
 // write_resolvability_csv (serialize.cpp:39-45, 141-154): two rows per separation, %.17g fields
 std::string format_resolvability_csv(const CurveH& c);
+// write_resolvability_json (serialize.cpp:113-135): the reference JSON library's object layout
+std::string format_resolvability_json(const CurveH& c);
 
 double fft_resolution(double fs, size_t n);                   // resolution.cpp:28-32
 size_t czt_len_for_matched_resolution(double f1, double f2, double fs, size_t n_fft);   // resolution.cpp:49-63

@@ -588,6 +588,14 @@ sk_status sk_resolvability_write_csv(const sk_resolvability_curve* c, const char
     });
 }
 
+sk_status sk_resolvability_write_json(const sk_resolvability_curve* c, const char* path) {
+    if (!c || !path) return bad_arg("sk_resolvability_write_json: null argument");
+    return guarded([&] {
+        skg::write_text_file(skg::format_resolvability_json(c->c), path, "cannot open for writing: ",
+                             "resolvability json");
+    });
+}
+
 // sizing helpers (resolution.cpp:18-63; capi.cpp:237-265 of the reference)
 sk_status sk_fft_resolution(double fs, size_t n, double* out) {
     if (!out) return bad_arg("sk_fft_resolution: null output");

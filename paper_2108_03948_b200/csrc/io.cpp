@@ -229,6 +229,8 @@ void append_json_number(std::string& out, double v) {
 
 }  // namespace
 
+void json_number(std::string& out, double v) { append_json_number(out, v); }
+
 std::string format_spectrum_json(const double* b, size_t n, double f_start, double f_step, size_t source_n) {
     // spectra.cpp:161-176: an object with keys in sorted order, two-space indentation, one array element
     // per line, then the writer's newline

@@ -52,6 +52,8 @@ std::string format_spectrum_json(const double* bins_interleaved, size_t n, doubl
                                  size_t source_n);
 void write_spectrum_json_file(const double* bins_interleaved, size_t n, double f_start, double f_step,
                               size_t source_n, const std::string& path);
+// one double as the reference's JSON library prints it (non-finite: null)
+void json_number(std::string& out, double v);
 // the CSV body as a string (the same bytes the file gets)
 std::string format_spectrum_csv(const double* bins_interleaved, size_t n, double f_start, double f_step);
 

@@ -549,6 +549,33 @@ ResolvabilityCurve resolvability_scan(const ScanConfig& cfg) {
     return r;
 }
 
+namespace {
+skg::CurveH to_curve_h(const ResolvabilityCurve& c) {
+    skg::CurveH h;
+    h.config.sample_rate_hz = c.config.sample_rate_hz;
+    h.config.n = c.config.n;
+    h.config.f1_hz = c.config.f1_hz;
+    h.config.f2_hz = c.config.f2_hz;
+    h.config.m = c.config.m;
+    h.config.center_hz = c.config.center_hz;
+    h.config.sep_start_hz = c.config.sep_start_hz;
+    h.config.sep_stop_hz = c.config.sep_stop_hz;
+    h.config.sep_step_hz = c.config.sep_step_hz;
+    h.separations_hz = c.separations_hz;
+    for (const auto& m : c.fft_metrics) h.fft_metrics.push_back(to_h(m));
+    for (const auto& m : c.czt_metrics) h.czt_metrics.push_back(to_h(m));
+    h.min_resolved_fft_hz = c.min_resolved_fft_hz;
+    h.min_resolved_czt_hz = c.min_resolved_czt_hz;
+    h.fft_len = c.fft_len;
+    return h;
+}
+}  // namespace
+
+void write_resolvability_json(const ResolvabilityCurve& c, std::ostream& out) {
+    out << skg::format_resolvability_json(to_curve_h(c));
+    if (!out) throw IoError("resolvability json: write failed");
+}
+
 void write_resolvability_csv(const ResolvabilityCurve& c, std::ostream& out) {
     skg::CurveH h;
     h.separations_hz = c.separations_hz;

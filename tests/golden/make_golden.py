@@ -364,6 +364,22 @@ def main():
     for name, kw in SCAN_CASES.items():
         rs[f"{name}_sep"], rs[f"{name}_fft"], rs[f"{name}_czt"], rs[f"{name}_minfft"], rs[f"{name}_minczt"] = \
             ref_scan(**kw)
+    # the reference's curve JSON / CSV files for the default sweep (layout pins for the writers)
+    import paper_2108_03948_b200 as sk
+    R.sk_resolvability_write_json.argtypes = [C.c_void_p, C.c_char_p]
+    R.sk_resolvability_write_csv.argtypes = [C.c_void_p, C.c_char_p]
+    c = sk.SkScanConfig()
+    R.sk_scan_config_defaults(C.byref(c))
+    h = C.c_void_p()
+    assert R.sk_resolvability_scan(C.byref(c), C.byref(h)) == 0
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        for ext, fn in (("json", R.sk_resolvability_write_json), ("csv", R.sk_resolvability_write_csv)):
+            path = os.path.join(td, "curve." + ext)
+            assert fn(h, path.encode()) == 0
+            with open(path, "rb") as f:
+                rs[f"default_{ext}"] = np.frombuffer(f.read(), np.uint8)
+    R.sk_resolvability_curve_free(h)
     # dip_metric on a reference spectrum (fft of a two-tone record), incl. the insufficient-resolution case
     np.savez_compressed(os.path.join(OUT, "scan.npz"), **rs)
 

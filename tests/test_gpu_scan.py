@@ -63,3 +63,26 @@ def test_curve_csv(tmp_path):
             m = got[route][i]
             want = ",".join(["%.17g" % sep, route, "%d" % int(m[0])] + ["%.17g" % v for v in m[1:]])
             assert lines[1 + 2 * i + j] == want
+
+
+def test_curve_files_match_reference_layout(golden, tmp_path):
+    """sk_resolvability_write_json / _csv against the reference's own files for the default sweep:
+    identical text once the numbers are masked (layout, key order, booleans, integers, nulls), and the
+    numbers equal to the reference's within the route's tolerance (separations exact)."""
+    import json
+    import re
+    g = golden("scan")
+    pj, pc = tmp_path / "c.json", tmp_path / "c.csv"
+    sk.resolvability_scan(csv_path=str(pc), json_path=str(pj), **SCAN_CASES["default"])
+    num = re.compile(r"-?\d+(\.\d+)?(e[+-]\d+)?")
+    ours, ref = pj.read_text(), bytes(g["default_json"]).decode()
+    assert num.sub("#", ours) == num.sub("#", ref)
+    a, b = json.loads(ours), json.loads(ref)
+    assert a["separations_hz"] == b["separations_hz"] and a["config"] == b["config"]
+    assert a["min_resolved_fft_hz"] == b["min_resolved_fft_hz"] and a["min_resolved_czt_hz"] == b["min_resolved_czt_hz"]
+    for route in ("fft", "czt"):
+        for x, y in zip(a[route], b[route]):
+            assert x["resolved"] == y["resolved"]
+            for k in ("peak_a_db", "peak_b_db"):
+                assert abs(x[k] - y[k]) <= 1e-8
+    assert num.sub("#", pc.read_text()) == num.sub("#", bytes(g["default_csv"]).decode())
