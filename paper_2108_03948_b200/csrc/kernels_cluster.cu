@@ -15,9 +15,10 @@
 //   3. CTA s finishes a radix-CS DFT over n1 for each of its Q/CS k2 and stores X[k1 Q + k2]:
 //      CS runs of Q/CS contiguous bins — coalesced, written once.
 // HBM traffic is the algorithmic minimum (trace in, bins out); the exchange crosses the cluster
-// once. Two cluster barriers per transform: (A) every CTA's Q-FFT is done with its shared buffer,
-// which then receives the pushed values, (B) all pushes landed. Persistent clusters loop over the
-// batch. Replaces FftPlan::run (numerics.cpp:73-97) at these lengths, as fft_spectrum's full /
+// once. Per transform: (A) an execution-only cluster barrier — every CTA's Q-FFT is done with its
+// shared buffer, which then receives the pushed values — and (B) each CTA waits on its own mbarrier
+// until the st.async pushes of all CS CTAs (Q values) have landed. Persistent clusters loop over the
+// batch. Opt-in (SKG_CLUSTER=1): measured slower than the four-step passes. Replaces FftPlan::run (numerics.cpp:73-97) at these lengths, as fft_spectrum's full /
 // half layout (spectra.cpp:21-38) or the plain complex transform (fft / ifft, numerics.cpp:102-120).
 #include <cuda_runtime.h>
 
