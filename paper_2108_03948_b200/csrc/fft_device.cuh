@@ -101,7 +101,13 @@ __device__ __forceinline__ float atan2_t(float y, float x) { return fast_atan2f(
 __device__ __forceinline__ double abs_t(double x, double y) { return hypot(x, y); }
 __device__ __forceinline__ float abs_t(float x, float y) {
     const float h = fmaf(x, x, y * y);
+#ifdef SKG_ABS_RSQRT
     return h > 0.0f ? h * rsqrtf(h) : 0.0f;
+#else
+    float r;   // MUFU.SQRT (max relative error 2^-23; sqrt(0) = 0, so no zero guard)
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(h));
+    return r;
+#endif
 }
 // magnitude_db (types.cpp:13-18): 20 log10 |v|, -300 dB at |v| <= 1e-15
 __device__ __forceinline__ double magnitude_db_t(double x, double y) {
