@@ -780,7 +780,7 @@ cudaError_t launch_zoom_wfir(const ZoomArgs& a, bool f32, const void* x, long lo
 
 // FFT of each work row (first nout entries, zero padded to L) and the signed band gather
 // x D x group-delay phase (zoomfft.cpp:204-234); several records per CTA for short transforms
-template <typename T, int LOG2N>
+template <typename T, int LOG2N, int NZ>
 __global__ void __launch_bounds__(KCfg<T, LOG2N>::BLOCK, KCfg<T, LOG2N>::MINB)
 k_zoom_fftband(const cx_t<T>* __restrict__ zb, long long z_stride, int nout, long long batch, int k_lo, int nbins,
                const cx_t<T>* __restrict__ tw, const cx_t<T>* __restrict__ band, cx_t<T>* __restrict__ out,
@@ -797,7 +797,7 @@ k_zoom_fftband(const cx_t<T>* __restrict__ zb, long long z_stride, int nout, lon
             const int pos = tid + G::NT * q;
             v[q] = (active && pos < nvalid) ? src[pos] : czero<C>();
         }
-        block_fft<false, LOG2N>(v, sm, tws, tid);
+        block_fft<false, LOG2N, NZ>(v, sm, tws, tid);   // NZ: the block is zero padded to n_fft
         if constexpr (G::L >= 16) {
 #pragma unroll
             for (int q = 0; q < G::EPT; ++q) sm[pad16(tid + G::NT * q)] = v[q];
@@ -818,7 +818,7 @@ k_zoom_fftband(const cx_t<T>* __restrict__ zb, long long z_stride, int nout, lon
     }
 }
 
-template <typename T, int LOG2N>
+template <typename T, int LOG2N, int NZ>
 static cudaError_t run_zoom_fftband(const void* zb, long long z_stride, int nout, long long batch, int k_lo,
                                     int nbins, const void* tw, const void* band, void* out, long long out_stride,
                                     cudaStream_t st) {
@@ -826,7 +826,7 @@ static cudaError_t run_zoom_fftband(const void* zb, long long z_stride, int nout
     using C = cx_t<T>;
     // small transforms (L < 16) still need L entries of exchange space
     constexpr size_t smem = K::SMEM_BYTES > 0 ? K::SMEM_BYTES : (size_t)K::GROUPS * 16 * sizeof(C);
-    auto kern = k_zoom_fftband<T, LOG2N>;
+    auto kern = k_zoom_fftband<T, LOG2N, NZ>;
     cudaError_t e = prep_smem(kern, smem);
     if (e != cudaSuccess) return e;
     kern<<<persistent_grid(kern, K::BLOCK, smem, grid_for(batch, K::GROUPS)), K::BLOCK, smem, st>>>(
@@ -841,7 +841,12 @@ cudaError_t launch_zoom_fftband(int log2n, bool f32, const void* zb, long long z
         using T = decltype(tag);
         return dispatch_log2<0, max_log2<T>()>(log2n, [&](auto lg) {
             constexpr int LG = decltype(lg)::value;
-            return run_zoom_fftband<T, LG>(zb, z_stride, nout, batch, k_lo, nbins, tw, band, out, out_stride, st);
+            const int nz = nz_class(nout < (1 << LG) ? nout : (1 << LG), FftGeom<LG>::NT);
+            return dispatch_nz<LG>(nz, [&](auto z) {
+                constexpr int NZ = decltype(z)::value;
+                return run_zoom_fftband<T, LG, NZ>(zb, z_stride, nout, batch, k_lo, nbins, tw, band, out, out_stride,
+                                                   st);
+            });
         });
     };
     return f32 ? go(float{}) : go(double{});
