@@ -29,12 +29,20 @@ METRIC = "traces/sec & achieved HBM GB/s (% of roofline) for batched FFT / CZT /
 UNIT = "traces/s"
 
 
+def _profile_version(path):
+    """(round, version) from a profiles/ file name: r2v3_... -> (2, 3); r1_... -> (1, 0)."""
+    import re
+    m = re.match(r"r(\d+)(?:v(\d+))?", os.path.basename(path))
+    return (int(m.group(1)), int(m.group(2) or 0)) if m else (-1, -1)
+
+
 def ncu_traffic(kernel_prefix):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the named kernel from the newest
-    committed ncu --set full summary in profiles/ (None when absent)."""
+    (highest round, then version) committed ncu --set full summary in profiles/ (None when absent)."""
     import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*.json")), key=_profile_version)
     best = None
-    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_full*.json"))):
+    for f in files:
         try:
             with open(f) as fh:
                 for d in json.load(fh)["launches"]:
@@ -120,17 +128,26 @@ class ClockSampler:
                 "reasons": rs, "samples": len(self.sm), "source": "nvml"}
 
 
-def dist_init():
+def dist_init(args=None, backend="nccl"):
+    """One process per GPU (torchrun env). NCCL logs at INFO into a per-rank file (stdout carries
+    only the JSON line); there is no collective on the data path, only barrier + max-over-ranks."""
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args is not None and args.gpus > 1 and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    elif torch.cuda.is_available():
+        if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_FILE", f"/tmp/skg_nccl.rank{rank}.%p.log")
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    elif backend == "nccl" and torch.cuda.is_available():
         torch.cuda.set_device(0)
     return rank, world, local
 
@@ -141,12 +158,12 @@ def barrier(world):
         dist.barrier()
 
 
-def max_over_ranks(v, world):
+def max_over_ranks(v, world, device="cuda"):
     if world == 1:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -203,36 +220,112 @@ def fp_peak_tflops(dtype):
 
 
 # ---- CPU baseline (the reference on this host's cores) -----------------------------------------
-def cpu_czt_baseline(x, a, w, m, seconds=4.0, threads=None):
-    import ctypes as C
+def cpu_model():
+    """The reference's bench_environment() line (bench.cpp:100-129) when the reference is built,
+    else /proc/cpuinfo's model name (what that function reads)."""
+    try:
+        import oracle
+        R = oracle.ref()
+        if R is not None:
+            return R.skr_bench_environment().decode()
+    except Exception:
+        pass
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return "cpu: " + line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown cpu"
 
+
+def _measure_cpu(run, total, seconds, threads):
+    """run(count, threads) -> wall seconds; grows the sample until it takes >= seconds / 2 (or the
+    whole workload). Returns (units/s, count, seconds)."""
+    run(min(total, threads), threads)   # warm-up: page in, start threads
+    cnt = min(total, 2 * threads)
+    dt = run(cnt, threads)
+    while dt < seconds / 2 and cnt < total:
+        cnt = min(total, max(cnt * 2, int(cnt * seconds / 2 / max(dt, 1e-4))))
+        dt = run(cnt, threads)
+    return cnt / dt, cnt, dt
+
+
+def cpu_baseline(run, total, what, seconds, kind, unit=UNIT):
+    """The reference CPU path at all host threads and at one thread."""
+    T = os.cpu_count() or 1
+    v, c, dt = _measure_cpu(run, total, seconds, T)
+    v1, c1, dt1 = _measure_cpu(run, total, seconds / 2, 1)
+    return {"value": v, "unit": unit, "cores": T, "kind": kind, "value_t1": v1, "cores_t1": 1,
+            "cpu_model": cpu_model(),
+            "sample": f"{what}: {c} units on {T} threads in {dt:.2f} s; {c1} units on 1 thread in {dt1:.2f} s"}
+
+
+def ref_runners(x_czt=None, czt=None, x_zoom=None, zoom=None, x_px=None, px=None):
+    """run(count, threads) closures over the compiled reference (oracle/_ref: CztPlan::execute,
+    zoom_fft, FftPlan::forward + restated H, plan reuse, shared plan) — or the C port when the
+    reference was not built. Returns (dict of closures, kind)."""
     import oracle
-    threads = threads or os.cpu_count() or 1
-    n = x.shape[1]
     R = oracle.ref()
     kind = "reference" if R is not None else "port"
-    xs = np.ascontiguousarray(x)
-    if R is not None:
-        p = R.skr_czt_plan_create(n, a.real, a.imag, w.real, w.imag, m)
+    runs = {}
+    if czt is not None:
+        n, a, w, m = czt
+        xs = np.ascontiguousarray(x_czt, dtype=np.float64)
+        if R is not None:
+            p = R.skr_czt_plan_create(n, a.real, a.imag, w.real, w.imag, m)
+            runs["czt"] = lambda cnt, th: R.skr_czt_batch(p, oracle._p(xs), n, cnt, th, None)
+        else:
+            plan = oracle.CztPlan(n, a, w, m)
+            runs["czt"] = lambda cnt, th: oracle.port().sko_bench_czt(plan._h, oracle._p(xs), n, cnt, th, None)
+        runs["_keep_czt"] = xs
+    if zoom is not None:
+        n, f1, f2, fs, d, taps, n_fft = zoom
+        xz = np.ascontiguousarray(x_zoom, dtype=np.float64)
+        if R is not None:
+            zp = R.skr_zoom_plan_create(n, f1, f2, fs, 0.0, 0, d, 0.0, taps, 1, 0, 1)
+            if n_fft:
+                R.skr_zoom_plan_set_n_fft(zp, n_fft)
+            runs["zoom"] = lambda cnt, th: R.skr_zoom_batch(zp, oracle._p(xz), n, fs, cnt, th, None, None, None, None)
+        else:
+            op = oracle.ZoomPlan(n, f1, f2, fs, decimation=d, num_taps=taps, **({"n_fft": n_fft} if n_fft else {}))
+            runs["zoom"] = lambda cnt, th: op.batch(xz[:cnt], th)
+        runs["_keep_zoom"] = xz
+    if px is not None and R is not None:
+        L, ref = px
+        xp = np.ascontiguousarray(x_px, dtype=np.float64)
+        rf = np.ascontiguousarray(ref, dtype=np.float64)
+        runs["px"] = lambda cnt, th: R.skr_transfer_batch(L, oracle._p(rf), oracle._p(xp), xp.shape[1], cnt, th,
+                                                          None, None)
+        runs["_keep_px"] = (xp, rf)
+    return runs, kind
 
-        def run(cnt):
-            return R.skr_czt_batch(p, oracle._p(xs), n, cnt, threads, None)
+
+def roofline_entry(bytes_per, flops_per, units, kern_s, hbm_gbs, fp_tflops, fp_name, kernel, traffic_prefix):
+    """roof time = max(bytes / HBM, flops / FP peak); frac = roof time / measured time,
+    reported in the bound's units."""
+    t_hbm = bytes_per * units / (hbm_gbs * 1e9)
+    t_fp = flops_per * units / (fp_tflops * 1e12)
+    tr = ncu_traffic(traffic_prefix) if traffic_prefix else None
+    if t_hbm >= t_fp:
+        ach, peak, unit, bound = bytes_per * units / kern_s / 1e9, hbm_gbs, "GB/s", "hbm"
     else:
-        plan = oracle.CztPlan(n, a, w, m)
+        ach, peak, unit, bound = flops_per * units / kern_s / 1e12, fp_tflops, "TFLOP/s", fp_name
+    return {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+            "traffic": (tr or {}).get("bytes"), "traffic_source": (tr or {}).get("source"),
+            "kernel": kernel, "kernel_ms": kern_s * 1e3, "bytes_per_unit": bytes_per, "flops_per_unit": flops_per,
+            "units_per_launch": units, "hbm_frac": bytes_per * units / kern_s / 1e9 / hbm_gbs,
+            "fp_frac": flops_per * units / kern_s / 1e12 / fp_tflops}
 
-        def run(cnt):
-            return oracle.port().sko_bench_czt(plan._h, oracle._p(xs), n, cnt, threads, None)
-    run(min(len(xs), threads))   # warm-up (page in, thread start)
-    cnt = min(len(xs), threads * 4)
-    dt = run(cnt)
-    while dt < seconds / 4 and cnt < len(xs):
-        cnt = min(len(xs), cnt * 4)
-        dt = run(cnt)
-    if R is not None:
-        R.skr_czt_plan_free(p)
-    return {"value": cnt / dt, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"{cnt} of the {len(xs)} cfg2 traces, plan reuse (CztPlan::execute), {threads} threads, "
-                      f"{dt:.2f} s wall"}
+
+# ---- the headline workload, shared by both arms -----------------------------------------------
+def headline_config(world):
+    return {"workload": "cfg2: Bluestein CZT of 4096 THz-TDS trace pairs = 8192 real traces, N=1024, "
+                        "M=2048 over 0.1-3 THz ((M-1) W step), L=4096, fp64",
+            "global_batch": 8192 * world, "per_gpu_batch": 8192,
+            "parallelism": f"dp{world} (independent traces, weak-scaled, no collective)",
+            "l2": "inputs 64 MiB + outputs 256 MiB per step > 126 MB L2 (no flush needed)"}
 
 
 # ---- our path ---------------------------------------------------------------------------------
@@ -241,7 +334,7 @@ def bench_ours(args):
 
     import paper_2108_03948_b200 as sk
     from paper_2108_03948_b200 import workloads as W
-    rank, world, local = dist_init()
+    rank, world, local = dist_init(args)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     pk = peaks()
@@ -249,8 +342,7 @@ def bench_ours(args):
     K, Wm = args.steps, args.warmup
 
     # ---- headline: cfg2 CZT fp64 -----------------------------------------------------------
-    pairs = args.pairs
-    x_host = W.cfg2_batch(pairs, 1024).astype(np.float64)      # 8192 x 1024 (refs then samples)
+    x_host = W.cfg2_batch(args.pairs, 1024).astype(np.float64)      # 8192 x 1024 (ref, sample pairs)
     B = x_host.shape[0]
     a, w = W.cfg2_czt_params(2048)
     plan = sk.CztPlanGPU(1024, a, w, 2048, sk.SKG_F64)
@@ -264,86 +356,66 @@ def bench_ours(args):
     per_step_launches = sk.launch_count() - l0
     with ClockSampler(local) as clk:
         total, per = time_device(fn, K, Wm, world)
-    launches = per_step_launches * K
     ms = total / K * 1e3
     value = world * B * K / total
     c = czt_counts(1024, 2048, 8)
     fp64_peak = fp_peak_tflops(torch.float64)
     kern_s = float(np.mean(per))
-    achieved_tf = c["flops"] * B / kern_s / 1e12
-    hbm_gbs = c["bytes"] * B / kern_s / 1e9
-    roof_t = max(c["bytes"] * B / (pk["hbm_gbs"] * 1e9), c["flops"] * B / (fp64_peak * 1e12))
-    kname = "k_czt_sf<double, 11, 8, 8"   # S=2 blocks of the L=4096 plan at L'=2048, one shared forward FFT
-    tr = ncu_traffic(kname)
+    kname = "k_czt_sf<double, 11"   # S=2 blocks of the L=4096 plan at L'=2048, one shared forward FFT
+    roof = roofline_entry(c["bytes"], c["flops"], B, kern_s, pk["hbm_gbs"], fp64_peak, "fp64", kname, kname)
+    roof["peak_source"] = "in-run cuBLAS DGEMM 4096^3 (MEASURED_PEAKS.json has no fp64 entry)"
+    roof["hbm_peak_source"] = pk["source"]
 
-    # ---- e2e: host buffers through the C ABI, H2D + kernel + D2H per step ---------------------
+    # ---- e2e: pinned host rows through the C ABI's host-buffer call (skg_czt_execute_host:
+    # chunked H2D / kernel / D2H on the library's streams), every step ---------------------------
     xh = torch.from_numpy(x_host).pin_memory()
     oh = torch.empty((B, 2048), dtype=torch.complex128).pin_memory()
-    chunks = 8
-    cs = B // chunks
-    s_copy = torch.cuda.Stream()
-    s_out = torch.cuda.Stream()
-    evs_in = [torch.cuda.Event() for _ in range(chunks)]
-    evs_k = [torch.cuda.Event() for _ in range(chunks)]
-
-    def e2e_step():
-        cur = torch.cuda.current_stream()
-        for i in range(chunks):
-            sl = slice(i * cs, (i + 1) * cs)
-            with torch.cuda.stream(s_copy):
-                xd[sl].copy_(xh[sl], non_blocking=True)
-                evs_in[i].record(s_copy)
-            cur.wait_event(evs_in[i])
-            plan.execute(xd[sl], out=out[sl])
-            evs_k[i].record(cur)
-            with torch.cuda.stream(s_out):
-                s_out.wait_event(evs_k[i])
-                oh[sl].copy_(out[sl], non_blocking=True)
-        cur.wait_stream(s_out)
-
+    e2e_fn = lambda: plan.execute_host(xh, out=oh)  # noqa: E731
     for _ in range(2):
-        e2e_step()
-    torch.cuda.synchronize()
+        e2e_fn()
+    l0 = sk.launch_count()
+    e2e_fn()
+    e2e_launches = sk.launch_count() - l0
     barrier(world)
+    ke = max(2, K // 2)
     t0 = time.perf_counter()
-    for _ in range(max(2, K // 2)):
-        e2e_step()
-    torch.cuda.synchronize()
+    for _ in range(ke):
+        e2e_fn()
     e2e_dt = max_over_ranks(time.perf_counter() - t0, world)
-    e2e_val = world * B * max(2, K // 2) / e2e_dt
-    # spot-check the e2e result against the device-resident result
-    ok_e2e = bool(torch.allclose(oh[:4].to(dev), out[:4]))
+    e2e_val = world * B * ke / e2e_dt
+    # every e2e row against the CPU oracle (the C restatement pinned to the reference at 0 ulp)
+    e2e_err = None
+    if not args.no_cpu:
+        import oracle as O
+        want = O.CztPlan(1024, a, w, 2048).batch_real(x_host, threads=os.cpu_count() or 4)
+        got = oh.numpy()
+        e2e_err = float(np.max(np.max(np.abs(got - want), axis=1) / np.max(np.abs(want), axis=1)))
 
     extra = {}
     if not args.quick and world == 1:   # single-GPU characterisation (the scaled metric is the headline)
-        extra = bench_extras(args, sk, W, dev, world, pk)
+        extra = bench_extras(args, sk, W, dev, world, pk, fp64_peak)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": Wm,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded THz-TDS pulse pairs, SURVEY §8d)",
-        "config": {"workload": "cfg2: Bluestein CZT, 4096 pairs = 8192 real traces, N=1024, M=2048, "
-                               "0.1-3 THz, L=4096, fp64", "global_batch": B * world, "per_gpu_batch": B,
-                   "parallelism": f"dp{world} (independent traces, no collective)",
-                   "l2": "inputs 64 MiB + outputs 256 MiB per step > 126 MB L2 (no flush needed)"},
-        "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": fp64_peak, "unit": "TFLOP/s",
-                     "frac": achieved_tf / fp64_peak, "traffic": (tr or {}).get("bytes"),
-                     "traffic_source": (tr or {}).get("source"),
-                     "peak_source": "in-run cuBLAS DGEMM 4096^3 (no fp64 entry in MEASURED_PEAKS.json)",
-                     "kernel": kname, "kernel_ms": kern_s * 1e3,
-                     "flops_per_trace": c["flops"], "bytes_per_trace": c["bytes"],
-                     "hbm_achieved_gbs": hbm_gbs, "hbm_peak_gbs": pk["hbm_gbs"], "hbm_frac": hbm_gbs / pk["hbm_gbs"],
-                     "roof_frac": roof_t / kern_s},
+        "config": headline_config(world),
+        "roofline": roof,
         "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(B * 1024 * 8),
-                "d2h_bytes_per_step": int(B * 2048 * 16), "chunks": chunks, "matches_device_result": ok_e2e},
-        "gpu_launches": int(launches),
+                "d2h_bytes_per_step": int(B * 2048 * 16), "api": "skg_czt_execute_host (pinned host rows)",
+                "launches_per_step": int(e2e_launches), "max_rel_err_vs_oracle_all_rows": e2e_err},
+        "gpu_launches": int(per_step_launches * K),
         "clocks": clk.summary(),
         "device": info,
     }
+    if world > 1:
+        line["nccl_log"] = os.environ.get("NCCL_DEBUG_FILE")
     if extra:
         line["extra"] = extra
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_czt_baseline(x_host, a, w, 2048, seconds=args.cpu_seconds)
+        runs, kind = ref_runners(x_czt=x_host, czt=(1024, a, w, 2048))
+        line["cpu_baseline"] = cpu_baseline(runs["czt"], B, "cfg2 traces, CztPlan::execute plan reuse, shared plan",
+                                            args.cpu_seconds, kind)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -351,12 +423,13 @@ def bench_ours(args):
         dist.destroy_process_group()
 
 
-def bench_extras(args, sk, W, dev, world, pk):
+def bench_extras(args, sk, W, dev, world, pk, fp64_peak):
     import torch
     res = {}
     K = max(3, args.steps // 2)
     Wm = 3
     fp32_peak = fp_peak_tflops(torch.float32)
+    peak_of = {"f64": (fp64_peak, "fp64"), "f32": (fp32_peak, "fp32")}
     # cfg2 fp32
     x = W.cfg2_batch(args.pairs, 1024)
     a, w = W.cfg2_czt_params(2048)
@@ -366,13 +439,19 @@ def bench_extras(args, sk, W, dev, world, pk):
     t, per = time_device(lambda: p32.execute(xd, out=out), K, Wm, world)
     c = czt_counts(1024, 2048, 4)
     ks = float(np.mean(per))
-    res["cfg2_czt_f32"] = {"traces_per_s": x.shape[0] * K / t, "kernel_ms": ks * 1e3,
-                           "tflops": c["flops"] * x.shape[0] / ks / 1e12, "fp32_peak_tflops": fp32_peak,
-                           "frac_fp32": c["flops"] * x.shape[0] / ks / 1e12 / fp32_peak,
-                           "hbm_gbs": c["bytes"] * x.shape[0] / ks / 1e9}
+    res["cfg2_czt_f32"] = {"traces_per_s": x.shape[0] * K / t,
+                           "roofline": roofline_entry(c["bytes"], c["flops"], x.shape[0], ks, pk["hbm_gbs"],
+                                                      fp32_peak, "fp32", "k_czt_sf<float, 11", "k_czt_sf<float, 11"),
+                           "fp32_peak_source": "in-run cuBLAS SGEMM 8192^3, TF32 off"}
     del xd, out
+    cpu = {}
     # cfg3 zoom (reference sizing n_fft 512, and the 2048 text variant), fp64 + fp32
     x3 = W.cfg3_batch(4096, 4096)
+    if not args.no_cpu:
+        for nf in (0, 2048):
+            runs, kind = ref_runners(x_zoom=x3, zoom=(4096, 0.4e12, 1.2e12, W.FS, 8, 65, nf))
+            cpu[nf] = cpu_baseline(runs["zoom"], x3.shape[0], f"cfg3 records, zoom_fft plan reuse (n_fft "
+                                   f"{nf or 512})", args.cpu_seconds / 2, kind)
     for prec, dt, s in (("f64", torch.float64, 8), ("f32", torch.float32, 4)):
         xd = torch.from_numpy(x3).to(dt).to(dev)
         for nf in (0, 2048):
@@ -380,12 +459,18 @@ def bench_extras(args, sk, W, dev, world, pk):
                                 decimation=8, num_taps=65)
             out = torch.empty((4096, zp.bins), dtype=torch.complex128 if prec == "f64" else torch.complex64,
                               device=dev)
+            l0 = sk.launch_count()
+            zp.execute(xd, out=out)
+            nl = sk.launch_count() - l0
             t, per = time_device(lambda: zp.execute(xd, out=out), K, Wm, world)
             ks = float(np.mean(per))
             cc = zoom_counts(4096, 8, 65, zp.n_fft, zp.bins, s)
-            res[f"cfg3_zoom_nfft{zp.n_fft}_{prec}"] = {
-                "traces_per_s": 4096 * K / t, "kernel_ms": ks * 1e3, "hbm_gbs": cc["bytes"] * 4096 / ks / 1e9,
-                "hbm_frac": cc["bytes"] * 4096 / ks / 1e9 / pk["hbm_gbs"], "tflops": cc["flops"] * 4096 / ks / 1e12}
+            e = {"traces_per_s": 4096 * K / t, "launches_per_call": nl,
+                 "roofline": roofline_entry(cc["bytes"], cc["flops"], 4096, ks, pk["hbm_gbs"], peak_of[prec][0],
+                                            peak_of[prec][1], "zoom call", None)}
+            if nf in cpu:
+                e["cpu_baseline"] = cpu[nf]
+            res[f"cfg3_zoom_nfft{zp.n_fft}_{prec}"] = e
         del xd
     # cfg4 cube: 65536 px x 2048 fp32 -> |H|, arg H on 4097 bins
     cube, ref = W.cfg4_cube(256, 256, 2048)
@@ -396,9 +481,15 @@ def bench_extras(args, sk, W, dev, world, pk):
     t, per = time_device(lambda: tp.execute(cd, mag, ph), K, Wm, world)
     ks = float(np.mean(per))
     hc = h_counts(2048, 8192, 4)
-    res["cfg4_cube_H_f32"] = {"pixels_per_s": cube.shape[0] * K / t, "kernel_ms": ks * 1e3,
-                              "hbm_gbs": hc["bytes"] * cube.shape[0] / ks / 1e9,
-                              "hbm_frac": hc["bytes"] * cube.shape[0] / ks / 1e9 / pk["hbm_gbs"]}
+    e = {"pixels_per_s": cube.shape[0] * K / t,
+         "roofline": roofline_entry(hc["bytes"], hc["flops"], cube.shape[0], ks, pk["hbm_gbs"], fp32_peak, "fp32",
+                                    "k_fft_r2c<float, 12", "k_fft_r2c<float, 12")}
+    if not args.no_cpu:
+        runs, kind = ref_runners(x_px=cube[:8192], px=(8192, ref))
+        if "px" in runs:
+            e["cpu_baseline"] = cpu_baseline(runs["px"], 8192, "cfg4 pixels, FftPlan(8192)::forward + restated H "
+                                             "(reference FFT, fp64)", args.cpu_seconds / 2, kind, unit="pixels/s")
+    res["cfg4_cube_H_f32"] = e
     del cd, mag, ph
     # SURVEY §8f rows 1-2, files -> files: 1024 cfg2 traces (N=1024 fp64) as reference-format CSV
     # (written once, untimed); a step = batched ingest -> fused band FFT 4096 (0.1-3 THz) -> batched
@@ -519,46 +610,67 @@ def bench_scan(args, sk, W):
 
 # ---- reference arm ----------------------------------------------------------------------------
 def bench_reference(args):
+    """The reference's own CPU implementation of the path (oracle/_ref: the unmodified reference
+    compiled from its sources; CztPlan::execute with plan reuse, as its bench harness runs it,
+    bench.cpp:194-204) on all host threads, on the same config as our arm. Rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    import oracle
     from paper_2108_03948_b200 import workloads as W
     threads = os.cpu_count() or 1
-    R = oracle.ref()
-    kind = "reference" if R is not None else "port"
     x = W.cfg2_batch(args.pairs, 1024)
     a, w = W.cfg2_czt_params(2048)
-    n, m = 1024, 2048
-    xs = np.ascontiguousarray(x)
-    if R is not None:
-        p = R.skr_czt_plan_create(n, a.real, a.imag, w.real, w.imag, m)
-        run = lambda cnt: R.skr_czt_batch(p, oracle._p(xs), n, cnt, threads, None)  # noqa: E731
-    else:
-        plan = oracle.CztPlan(n, a, w, m)
-        run = lambda cnt: oracle.port().sko_bench_czt(plan._h, oracle._p(xs), n, cnt, threads, None)  # noqa: E731
-    # size one step to ~`ref_step_s` seconds of wall time
-    dt = run(threads)
+    runs, kind = ref_runners(x_czt=x, czt=(1024, a, w, 2048))
+    run = runs["czt"]
+    # one step = the whole 8192-trace batch when that takes <= ref_step_s, else a bounded sample
+    dt = run(threads, threads)
     per_trace = dt / threads
-    cnt = int(min(len(xs), max(threads, args.ref_step_s / max(per_trace, 1e-9) * threads)))
+    cnt = int(min(len(x), max(threads, args.ref_step_s / max(per_trace, 1e-9) * threads)))
     for _ in range(args.warmup):
-        run(cnt)
+        run(cnt, threads)
     tot = 0.0
     for _ in range(args.steps):
-        tot += run(cnt)
+        tot += run(cnt, threads)
     value = cnt * args.steps / tot
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded THz-TDS pulse pairs)",
-            "config": {"workload": "cfg2: Bluestein CZT, N=1024, M=2048, 0.1-3 THz, L=4096, fp64 "
-                                   f"(bounded sample of {cnt} traces per step)", "global_batch": cnt,
-                       "parallelism": f"{threads} host threads"},
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded THz-TDS pulse pairs, SURVEY §8d)",
+            "config": headline_config(world),
             "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                             "sample": f"{cnt} traces per step, CztPlan::execute plan reuse, shared plan"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "cpu_model": cpu_model(),
+                             "sample": f"{cnt} of the {len(x)} cfg2 traces per step, CztPlan::execute plan reuse, "
+                                       f"shared plan, {threads} threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` outside torchrun: re-exec under torch.distributed.run with N ranks
+    (one process per GPU, 127.0.0.1 rendezvous), as the driver launches it."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
+def selftest_dist(args):
+    """CPU check of the multi-rank plumbing (gloo): launcher, rank / world discovery, barrier,
+    max-over-ranks timing and the rank-0-only JSON line — what --gpus N runs around the kernels."""
+    rank, world, _ = dist_init(args, backend="gloo")
+    per = [0.001 * (rank + 1)] * args.steps
+    total = max_over_ranks(sum(per), world, device="cpu")
+    barrier(world)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": world * 8192 * args.steps / total, "unit": UNIT,
+                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "selftest": "gloo",
+                          "max_over_ranks_s": total, "config": headline_config(world)}), flush=True)
+    import torch.distributed as dist
+    dist.destroy_process_group()
 
 
 def main():
@@ -572,9 +684,14 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=4.0)
     ap.add_argument("--ref-step-s", type=float, default=3.0)
+    ap.add_argument("--selftest-dist", action="store_true", help="CPU (gloo) check of the multi-rank plumbing")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)
+    if args.selftest_dist:
+        selftest_dist(args)
+    elif args.impl == "reference":
         bench_reference(args)
     else:
         bench_ours(args)

@@ -27,6 +27,10 @@ typedef enum skg_precision { SKG_F64 = 0, SKG_F32 = 1 } skg_precision;
 SK_API sk_status skg_device_info(int* device, int* sm_count, size_t* smem_optin, size_t* l2_bytes);
 /* number of kernels this library has launched in the process (evidence counter) */
 SK_API uint64_t skg_launch_count(void);
+/* Test hook: cap every persistent kernel grid at `cap` CTAs (0 = off, the default). The kernels
+ * loop over their units; a small cap drives every CTA through many units so parity tests cover
+ * the later waves (next-unit prefetch, workspace-slot reuse) at batch sizes an oracle checks fast. */
+SK_API void skg_debug_set_grid_cap(unsigned cap);
 /* cudaStreamSynchronize(stream) with the library's error reporting */
 SK_API sk_status skg_synchronize(void* stream);
 
@@ -127,6 +131,24 @@ SK_API sk_status skg_zoom_plan_info(const skg_zoom_plan* p, size_t* bins, double
                                     size_t* num_taps);
 SK_API sk_status skg_zoom_execute(const skg_zoom_plan* p, const void* d_x, size_t x_stride,
                                   size_t batch, void* d_out, size_t out_stride, void* stream);
+
+/* ---- host-buffer batched calls -----------------------------------------------------------------
+ * The batched counterparts of the reference's host-buffer one-shot calls (sk_czt, capi.cpp:197-205;
+ * sk_fft_spectrum; sk_zoom_spectrum): rows in host memory in, rows in host memory out. The library
+ * moves `chunk` rows at a time (0 = automatic, about 8 chunks) on its own streams so the H2D copy of
+ * one chunk, the kernel of the next and the D2H copy of a third overlap. Pinned caller buffers
+ * (cudaHostAlloc / cudaHostRegister) are copied directly; pageable ones through library-owned pinned
+ * staging. Strides are in elements as in the device calls. The calls return when every output row is
+ * in host memory. */
+SK_API sk_status skg_czt_execute_host(const skg_czt_plan* p, const void* h_x, int x_complex, size_t x_stride,
+                                      size_t batch, void* h_out, size_t out_stride, size_t chunk);
+SK_API sk_status skg_fft_spectrum_host(size_t n, size_t transform_len, int precision, int layout, const void* h_x,
+                                       size_t x_stride, size_t batch, void* h_out, size_t out_stride, size_t chunk);
+SK_API sk_status skg_zoom_execute_host(const skg_zoom_plan* p, const void* h_x, size_t x_stride, size_t batch,
+                                       void* h_out, size_t out_stride, size_t chunk);
+SK_API sk_status skg_transfer_execute_host(const skg_transfer_plan* p, const void* h_x, size_t x_stride,
+                                           size_t batch, void* h_mag, void* h_phase, size_t mp_stride,
+                                           size_t chunk);
 
 #ifdef __cplusplus
 }

@@ -95,6 +95,8 @@ def port():
         L.sko_bench_fft_spectrum.argtypes = [sz, dp, sz, sz, C.c_int, dp]
         L.sko_bench_zoom.restype = C.c_double
         L.sko_bench_zoom.argtypes = [C.c_void_p, dp, sz, C.c_double, sz, C.c_int]
+        L.sko_batch_zoom.restype = C.c_double
+        L.sko_batch_zoom.argtypes = [C.c_void_p, dp, sz, C.c_double, sz, C.c_int, dp]
         _port = L
     return _port
 
@@ -137,6 +139,9 @@ def ref():
             L.skr_zoom_plan_free.argtypes = [C.c_void_p]
             L.skr_zoom_plan_set_n_fft.argtypes = [C.c_void_p, sz]
             L.skr_zoom_plan_set_taps.argtypes = [C.c_void_p, dp, sz]
+            L.skr_bench_environment.restype = C.c_char_p
+            L.skr_transfer_batch.restype = C.c_double
+            L.skr_transfer_batch.argtypes = [sz, dp, dp, sz, sz, C.c_int, dp, dp]
             L.skr_zoom_batch.restype = C.c_double
             L.skr_zoom_batch.argtypes = [C.c_void_p, dp, sz, C.c_double, sz, C.c_int, dp,
                                          C.POINTER(sz), dp, dp]
@@ -376,6 +381,15 @@ class ZoomPlan:
     def batch(self, x_real, threads=1):
         x_real = f64(x_real)
         return port().sko_bench_zoom(self._h, _p(x_real), self.n, self.fs, x_real.shape[0], threads)
+
+    def batch_out(self, x_real, threads=1):
+        """zoom_fft of every row (threaded), the band bins of each row."""
+        x_real = f64(x_real)
+        nb = self(x_real[0])[0].size
+        out = np.empty((x_real.shape[0], nb), np.complex128)
+        port().sko_batch_zoom(self._h, _p(x_real), self.n, self.fs, x_real.shape[0], threads,
+                              _p(out.view(np.float64)))
+        return out
 
     def __del__(self):
         if getattr(self, "_h", None):

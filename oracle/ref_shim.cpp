@@ -5,11 +5,14 @@
 // immutable plan (legal per numerics.hpp:24-26, czt.hpp:30-33). The reference's own sk_*
 // C ABI (capi.cpp) is linked into the same .so and is used directly for the one-shot paths.
 #include <chrono>
+#include <cmath>
+#include <string>
 #include <cstring>
 #include <functional>
 #include <thread>
 #include <vector>
 
+#include "bench.hpp"
 #include "czt.hpp"
 #include "numerics.hpp"
 #include "spectra.hpp"
@@ -137,6 +140,42 @@ double skr_zoom_batch(void* plan, const double* x_real, std::size_t n, double fs
             t.samples.assign(x_real + i * n, x_real + (i + 1) * n);
             const Spectrum s = zoom_fft(p, t);
             if (out) std::memcpy(out + 2 * i * s.size(), s.bins.data(), s.size() * sizeof(cplx));
+        }
+    });
+}
+
+// bench_environment() (bench.cpp:100-129): the CPU model / kernel / compiler line the reference's
+// own bench reports print beside their numbers
+const char* skr_bench_environment() {
+    static const std::string env = bench_environment();
+    return env.c_str();
+}
+
+// H(f) of `count` real traces against one reference trace on the reference's FFT: FftPlan(L).forward
+// of each zero-padded trace (bench.cpp:176-186) and of the reference once, then the restated
+// per-bin division H = X_s / X_ref, |H| = hypot, arg H = atan2 on the L/2 + 1 bins (
+// the reference has no H). mag / phase may be NULL (timing only).
+double skr_transfer_batch(std::size_t L, const double* ref, const double* x_real, std::size_t n, std::size_t count,
+                          int threads, double* mag, double* phase) {
+    FftPlan plan(L);
+    const std::size_t nb = L / 2 + 1;
+    ComplexBuffer xr(L, cplx(0.0, 0.0));
+    for (std::size_t i = 0; i < n; ++i) xr[i] = cplx(ref[i], 0.0);
+    plan.forward(xr);
+    return run_pool(count, threads, [&](std::size_t b, std::size_t e) {
+        ComplexBuffer buf(L);
+        std::vector<double> m(nb), p(nb);
+        for (std::size_t t = b; t < e; ++t) {
+            std::fill(buf.begin(), buf.end(), cplx(0.0, 0.0));
+            for (std::size_t i = 0; i < n; ++i) buf[i] = cplx(x_real[t * n + i], 0.0);
+            plan.forward(buf);
+            for (std::size_t k = 0; k < nb; ++k) {
+                const cplx h = buf[k] / xr[k];
+                m[k] = std::hypot(h.real(), h.imag());
+                p[k] = std::atan2(h.imag(), h.real());
+            }
+            if (mag) std::memcpy(mag + t * nb, m.data(), nb * sizeof(double));
+            if (phase) std::memcpy(phase + t * nb, p.data(), nb * sizeof(double));
         }
     });
 }

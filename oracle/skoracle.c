@@ -660,7 +660,7 @@ static void* run_job(void* arg) {
         sko_zoom_fft(p, j->x, j->n, j->fs, &nb, &fst, &fsp, NULL);
         double* o = (double*)malloc(2 * nb * sizeof(double));
         for (size_t t = j->begin; t < j->end; ++t)
-            sko_zoom_fft(p, j->x + t * j->n, j->n, j->fs, &nb, &fst, &fsp, o);
+            sko_zoom_fft(p, j->x + t * j->n, j->n, j->fs, &nb, &fst, &fsp, j->out ? j->out + 2 * t * nb : o);
         free(o);
     }
     return NULL;
@@ -703,5 +703,12 @@ double sko_bench_fft_spectrum(size_t L, const double* x_real, size_t n, size_t c
 double sko_bench_zoom(const sko_zoom_plan* p, const double* x_real, size_t n, double fs, size_t count,
                       int threads) {
     job_t j = {2, p, 0, x_real, n, fs, 0, 0, NULL};
+    return run_threads(j, count, threads);
+}
+
+/* the same, keeping every trace's band bins (count x bins interleaved complex) for parity checks */
+double sko_batch_zoom(const sko_zoom_plan* p, const double* x_real, size_t n, double fs, size_t count,
+                      int threads, double* out) {
+    job_t j = {2, p, 0, x_real, n, fs, 0, 0, out};
     return run_threads(j, count, threads);
 }

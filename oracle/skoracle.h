@@ -97,6 +97,8 @@ double sko_bench_fft_spectrum(size_t L, const double* x_real, size_t n, size_t c
                               int threads, double* out);
 double sko_bench_zoom(const sko_zoom_plan* p, const double* x_real, size_t n, double fs,
                       size_t count, int threads);
+double sko_batch_zoom(const sko_zoom_plan* p, const double* x_real, size_t n, double fs, size_t count,
+                      int threads, double* out);
 
 #ifdef __cplusplus
 }

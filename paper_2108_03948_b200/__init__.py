@@ -114,6 +114,7 @@ def _declare(L):
         "sk_zoom_spectrum": (st, [vp, vp, C.POINTER(vp)]),
         "skg_device_info": (st, [C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(sz), C.POINTER(sz)]),
         "skg_launch_count": (C.c_uint64, []),
+        "skg_debug_set_grid_cap": (None, [C.c_uint]),
         "skg_synchronize": (st, [vp]),
         "skg_fft_batch": (st, [sz, C.c_int, C.c_int, vp, sz, vp, sz, sz, vp]),
         "skg_fft_spectrum_batch": (st, [sz, sz, C.c_int, C.c_int, vp, sz, sz, vp, sz, vp]),
@@ -158,6 +159,10 @@ def _declare(L):
         "skg_zoom_plan_free": (None, [vp]),
         "skg_zoom_plan_info": (st, [vp, C.POINTER(sz), dp, dp, C.POINTER(sz), C.POINTER(sz), C.POINTER(sz)]),
         "skg_zoom_execute": (st, [vp, vp, sz, sz, vp, sz, vp]),
+        "skg_czt_execute_host": (st, [vp, vp, C.c_int, sz, sz, vp, sz, sz]),
+        "skg_fft_spectrum_host": (st, [sz, sz, C.c_int, C.c_int, vp, sz, sz, vp, sz, sz]),
+        "skg_zoom_execute_host": (st, [vp, vp, sz, sz, vp, sz, sz]),
+        "skg_transfer_execute_host": (st, [vp, vp, sz, sz, vp, vp, sz, sz]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -203,6 +208,22 @@ def last_error() -> str:
 
 def launch_count() -> int:
     return int(lib().skg_launch_count())
+
+
+class grid_cap:
+    """Context manager over the skg_debug_set_grid_cap test hook: persistent grids capped at
+    `cap` CTAs, so every CTA loops over many units (later waves, prefetch, slot reuse)."""
+
+    def __init__(self, cap):
+        self.cap = int(cap)
+
+    def __enter__(self):
+        lib().skg_debug_set_grid_cap(self.cap)
+        return self
+
+    def __exit__(self, *exc):
+        lib().skg_debug_set_grid_cap(0)
+        return False
 
 
 def device_info():
@@ -583,17 +604,49 @@ def _rows(x):
     """(batch, row stride) of a 1-D or 2-D tensor with unit inner stride."""
     if x.dim() == 1:
         x = x.unsqueeze(0)
-    assert x.stride(-1) == 1, "rows must be contiguous"
+    if x.dim() != 2 or x.stride(-1) != 1:
+        raise ValueError(f"expected 1-D or 2-D rows with unit inner stride, got shape {tuple(x.shape)} "
+                         f"stride {tuple(x.stride())}")
     return x, x.shape[0], x.stride(0)
+
+
+def _check_in(x, n, precision, what, complex_ok=False):
+    """Input rows for a plan: CUDA, the plan's precision, n samples per row (the C side reads
+    n * row-stride elements: a wrong dtype or row length would read past the buffer)."""
+    if not x.is_cuda:
+        raise ValueError(f"{what}: input must be a CUDA tensor")
+    if x.is_complex() and not complex_ok:
+        raise TypeError(f"{what}: input must be real, got {x.dtype}")
+    if _prec(x) != precision:
+        raise TypeError(f"{what}: input dtype {x.dtype} does not match the plan precision "
+                        f"({'fp64' if precision == SKG_F64 else 'fp32'})")
+    if x.shape[-1] != n:
+        raise ValueError(f"{what}: rows hold {x.shape[-1]} samples, the plan expects {n}")
+
+
+def _check_out(out, rows, cols, dtype, device, what):
+    """Caller-supplied output rows: right dtype, device, >= rows x cols, unit inner stride."""
+    if out.dtype != dtype:
+        raise TypeError(f"{what}: output dtype {out.dtype}, expected {dtype}")
+    if out.device != device:
+        raise ValueError(f"{what}: output on {out.device}, input on {device}")
+    o = out.unsqueeze(0) if out.dim() == 1 else out
+    if o.dim() != 2 or o.shape[0] < rows or o.shape[1] < cols or o.stride(-1) != 1:
+        raise ValueError(f"{what}: output must be ({rows}, >= {cols}) rows with unit inner stride, "
+                         f"got shape {tuple(out.shape)} stride {tuple(out.stride())}")
+    return o
 
 
 def fft_batch(x, inverse=False, out=None):
     """Complex FFT of each row of a complex CUDA tensor (skg_fft_batch)."""
     x, b, s = _rows(x)
     prec = _prec(x)
+    if not x.is_complex():
+        raise TypeError(f"fft_batch: complex rows expected, got {x.dtype}")
     out = torch_empty_like_rows(x) if out is None else out
-    _chk(lib().skg_fft_batch(x.shape[-1], int(inverse), prec, vp(x.data_ptr()), s, vp(out.data_ptr()),
-                             out.stride(0) if out.dim() == 2 else 0, b, _stream()))
+    o = _check_out(out, b, x.shape[-1], x.dtype, x.device, "fft_batch")
+    _chk(lib().skg_fft_batch(x.shape[-1], int(inverse), prec, vp(x.data_ptr()), s, vp(o.data_ptr()),
+                             o.stride(0), b, _stream()))
     return out
 
 
@@ -610,10 +663,91 @@ def fft_spectrum_batch(x, transform_len=0, layout=SKG_FULL, out=None):
     n = x.shape[-1]
     L = transform_len or next_pow2(n)
     nb = L if layout == SKG_FULL else L // 2 + 1
+    if x.is_complex():
+        raise TypeError(f"fft_spectrum_batch: real trace rows expected, got {x.dtype}")
     if out is None:
         out = torch.empty((b, nb), dtype=_cdtype(prec), device=x.device)
-    _chk(lib().skg_fft_spectrum_batch(n, L, prec, layout, vp(x.data_ptr()), s, b, vp(out.data_ptr()),
-                                      out.stride(0), _stream()))
+    o = _check_out(out, b, nb, _cdtype(prec), x.device, "fft_spectrum_batch")
+    _chk(lib().skg_fft_spectrum_batch(n, L, prec, layout, vp(x.data_ptr()), s, b, vp(o.data_ptr()),
+                                      o.stride(0), _stream()))
+    return out
+
+
+def _np_cdtype(prec):
+    return np.complex128 if prec == SKG_F64 else np.complex64
+
+
+def _host_rows(x, n, precision, what, complex_ok=False):
+    """(array, batch, row stride in elements, data pointer, is_complex) of host rows: a numpy array
+    or a CPU torch tensor (pinned or pageable) of the plan precision, unit inner stride."""
+    if hasattr(x, "is_cuda"):
+        if x.is_cuda:
+            raise ValueError(f"{what}: host rows expected, got a CUDA tensor (use execute)")
+        t = x.unsqueeze(0) if x.dim() == 1 else x
+        if t.dim() != 2 or t.stride(-1) != 1:
+            raise ValueError(f"{what}: 1-D or 2-D rows with unit inner stride expected")
+        if t.is_complex() and not complex_ok:
+            raise TypeError(f"{what}: real rows expected")
+        if _prec(t) != precision:
+            raise TypeError(f"{what}: dtype {t.dtype} does not match the plan precision")
+        if t.shape[-1] != n:
+            raise ValueError(f"{what}: rows hold {t.shape[-1]} samples, the plan expects {n}")
+        return t, t.shape[0], t.stride(0), vp(t.data_ptr()), t.is_complex()
+    a = np.asarray(x)
+    a = a[None] if a.ndim == 1 else a
+    if a.ndim != 2 or a.strides[-1] != a.itemsize:
+        raise ValueError(f"{what}: 1-D or 2-D rows with unit inner stride expected")
+    is_c = np.iscomplexobj(a)
+    if is_c and not complex_ok:
+        raise TypeError(f"{what}: real rows expected")
+    want = {SKG_F64: (np.float64, np.complex128), SKG_F32: (np.float32, np.complex64)}[precision]
+    if a.dtype not in want:
+        raise TypeError(f"{what}: dtype {a.dtype} does not match the plan precision")
+    if a.shape[-1] != n:
+        raise ValueError(f"{what}: rows hold {a.shape[-1]} samples, the plan expects {n}")
+    return a, a.shape[0], a.strides[0] // a.itemsize, vp(a.ctypes.data), is_c
+
+
+def _host_out(out, rows, cols, dtype, what):
+    if out is None:
+        return np.empty((rows, cols), dtype)
+    if hasattr(out, "is_cuda"):
+        import torch
+        td = {np.complex128: torch.complex128, np.complex64: torch.complex64, np.float64: torch.float64,
+              np.float32: torch.float32}[np.dtype(dtype).type]
+        if out.is_cuda or out.dtype != td:
+            raise TypeError(f"{what}: host output of dtype {td} expected")
+        o = out.unsqueeze(0) if out.dim() == 1 else out
+        if o.dim() != 2 or o.shape[0] < rows or o.shape[1] < cols or o.stride(-1) != 1:
+            raise ValueError(f"{what}: output must be ({rows}, >= {cols}) rows with unit inner stride")
+        return out
+    o = out[None] if out.ndim == 1 else out
+    if out.dtype != dtype or o.ndim != 2 or o.shape[0] < rows or o.shape[1] < cols or o.strides[-1] != o.itemsize:
+        raise ValueError(f"{what}: output must be ({rows}, >= {cols}) {np.dtype(dtype)} rows with unit inner stride")
+    return out
+
+
+def _host_ptr(a):
+    return vp(a.data_ptr()) if hasattr(a, "data_ptr") else vp(a.ctypes.data)
+
+
+def _host_stride(a):
+    if hasattr(a, "is_cuda"):
+        return a.stride(0) if a.dim() == 2 else a.shape[-1]
+    return a.strides[0] // a.itemsize if a.ndim == 2 else a.shape[-1]
+
+
+def fft_spectrum_host(x, transform_len=0, layout=SKG_FULL, precision=None, out=None, chunk=0):
+    """Zero-padded spectra of host trace rows through the library pipeline (skg_fft_spectrum_host)."""
+    a = x if hasattr(x, "is_cuda") else np.asarray(x)
+    dt = a.dtype
+    prec = precision if precision is not None else (SKG_F32 if str(dt) in ("float32", "torch.float32") else SKG_F64)
+    n = a.shape[-1]
+    x2, b, s, ptr, _ = _host_rows(a, n, prec, "fft_spectrum_host")
+    L = transform_len or next_pow2(n)
+    nb = L if layout == SKG_FULL else L // 2 + 1
+    out = _host_out(out, b, nb, _np_cdtype(prec), "fft_spectrum_host")
+    _chk(lib().skg_fft_spectrum_host(n, L, prec, layout, ptr, s, b, _host_ptr(out), _host_stride(out), chunk))
     return out
 
 
@@ -675,11 +809,21 @@ class CztPlanGPU:
     def execute(self, x, out=None):
         torch = _torch()
         x, b, s = _rows(x)
+        _check_in(x, self.n, self.precision, "CztPlanGPU.execute", complex_ok=True)
         is_c = x.is_complex()
         if out is None:
             out = torch.empty((b, self.m), dtype=_cdtype(self.precision), device=x.device)
-        _chk(lib().skg_czt_execute(self._h, vp(x.data_ptr()), int(is_c), s, b, vp(out.data_ptr()),
-                                   out.stride(0), _stream()))
+        o = _check_out(out, b, self.m, _cdtype(self.precision), x.device, "CztPlanGPU.execute")
+        _chk(lib().skg_czt_execute(self._h, vp(x.data_ptr()), int(is_c), s, b, vp(o.data_ptr()),
+                                   o.stride(0), _stream()))
+        return out
+
+    def execute_host(self, x, out=None, chunk=0):
+        """Host rows in, host rows out through the library's chunked pipeline (skg_czt_execute_host).
+        x: numpy array or CPU tensor (pinned or pageable) of the plan's precision."""
+        x2, b, s, ptr, is_c = _host_rows(x, self.n, self.precision, "CztPlanGPU.execute_host", complex_ok=True)
+        out = _host_out(out, b, self.m, _np_cdtype(self.precision), "CztPlanGPU.execute_host")
+        _chk(lib().skg_czt_execute_host(self._h, ptr, int(is_c), s, b, _host_ptr(out), _host_stride(out), chunk))
         return out
 
     def __del__(self, _rel=_release):
@@ -706,15 +850,33 @@ class TransferPlanGPU:
     def execute(self, x, mag=None, phase=None, h=None):
         torch = _torch()
         x, b, s = _rows(x)
+        _check_in(x, self.n, self.precision, "TransferPlanGPU.execute")
         rd = torch.float64 if self.precision == SKG_F64 else torch.float32
         if mag is None:
             mag = torch.empty((b, self.bins), dtype=rd, device=x.device)
         if phase is None:
             phase = torch.empty((b, self.bins), dtype=rd, device=x.device)
-        _chk(lib().skg_transfer_execute(self._h, vp(x.data_ptr()), s, b, vp(mag.data_ptr()),
-                                        vp(phase.data_ptr()), mag.stride(0),
-                                        vp(h.data_ptr()) if h is not None else None,
-                                        h.stride(0) if h is not None else 0, _stream()))
+        m2 = _check_out(mag, b, self.bins, rd, x.device, "TransferPlanGPU.execute (|H|)")
+        p2 = _check_out(phase, b, self.bins, rd, x.device, "TransferPlanGPU.execute (arg H)")
+        if m2.stride(0) != p2.stride(0):
+            raise ValueError("TransferPlanGPU.execute: |H| and arg H rows must share one stride")
+        h2 = None if h is None else _check_out(h, b, self.bins, _cdtype(self.precision), x.device,
+                                               "TransferPlanGPU.execute (H)")
+        _chk(lib().skg_transfer_execute(self._h, vp(x.data_ptr()), s, b, vp(m2.data_ptr()),
+                                        vp(p2.data_ptr()), m2.stride(0),
+                                        vp(h2.data_ptr()) if h2 is not None else None,
+                                        h2.stride(0) if h2 is not None else 0, _stream()))
+        return mag, phase
+
+    def execute_host(self, x, mag=None, phase=None, chunk=0):
+        x2, b, s, ptr, _ = _host_rows(x, self.n, self.precision, "TransferPlanGPU.execute_host")
+        rd = np.float64 if self.precision == SKG_F64 else np.float32
+        mag = _host_out(mag, b, self.bins, rd, "TransferPlanGPU.execute_host")
+        phase = _host_out(phase, b, self.bins, rd, "TransferPlanGPU.execute_host")
+        if _host_stride(mag) != _host_stride(phase):
+            raise ValueError("TransferPlanGPU.execute_host: |H| and arg H rows must share one stride")
+        _chk(lib().skg_transfer_execute_host(self._h, ptr, s, b, _host_ptr(mag), _host_ptr(phase), _host_stride(mag),
+                                             chunk))
         return mag, phase
 
     def __del__(self, _rel=_release):
@@ -748,10 +910,18 @@ class ZoomPlanGPU:
     def execute(self, x, out=None):
         torch = _torch()
         x, b, s = _rows(x)
+        _check_in(x, self.input_len, self.precision, "ZoomPlanGPU.execute")
         if out is None:
             out = torch.empty((b, self.bins), dtype=_cdtype(self.precision), device=x.device)
-        _chk(lib().skg_zoom_execute(self._h, vp(x.data_ptr()), s, b, vp(out.data_ptr()), out.stride(0),
+        o = _check_out(out, b, self.bins, _cdtype(self.precision), x.device, "ZoomPlanGPU.execute")
+        _chk(lib().skg_zoom_execute(self._h, vp(x.data_ptr()), s, b, vp(o.data_ptr()), o.stride(0),
                                     _stream()))
+        return out
+
+    def execute_host(self, x, out=None, chunk=0):
+        x2, b, s, ptr, _ = _host_rows(x, self.input_len, self.precision, "ZoomPlanGPU.execute_host")
+        out = _host_out(out, b, self.bins, _np_cdtype(self.precision), "ZoomPlanGPU.execute_host")
+        _chk(lib().skg_zoom_execute_host(self._h, ptr, s, b, _host_ptr(out), _host_stride(out), chunk))
         return out
 
     def __del__(self, _rel=_release):

@@ -13,6 +13,7 @@
 
 #include "analysis.hpp"
 #include "host.hpp"
+#include "staging.hpp"
 #include "io.hpp"
 #include "spectralkit.h"
 #include "spectralkit_gpu.h"
@@ -92,6 +93,19 @@ sk_status bad_arg(const char* msg) {
     return SK_ERR_INVALID_ARGUMENT;
 }
 
+// Row-stride and precision checks of the batched entry points: with more than one row, a stride
+// shorter than the row would make rows overlap (reads past the end of a caller's buffer, writes
+// over the next row).
+void need_stride(const char* fn, const char* what, size_t batch, size_t stride, size_t row) {
+    if (batch > 1 && stride < row)
+        throw std::invalid_argument(std::string(fn) + ": " + what + " stride " + std::to_string(stride) +
+                                    " is shorter than the row (" + std::to_string(row) + ")");
+}
+void need_precision(const char* fn, int precision) {
+    if (precision != SKG_F64 && precision != SKG_F32)
+        throw std::invalid_argument(std::string(fn) + ": precision must be SKG_F64 or SKG_F32");
+}
+
 // types.cpp:20-27
 void validate_trace(const sk_trace& t) {
     if (t.samples.empty()) throw std::invalid_argument("trace: no samples");
@@ -115,63 +129,18 @@ void split(const std::vector<cd>& x, double* re, double* im) {
     }
 }
 
-// one-shot staging: host -> device -> host on the per-thread default stream
-// Host-call staging: each calling thread keeps grow-only pinned host and device buffers, so a
-// single-trace C-ABI call costs two small copies and one kernel — no cudaMalloc/cudaFree (which
-// synchronise the device) and no pageable-memory bounce per call. Buffers are per device.
-struct Workspace {
-    struct Buf {
-        void* p = nullptr;
-        size_t cap = 0;
-    };
-    int dev = -1;
-    Buf hin, hout, din, dout;
-    static void grow(Buf& b, size_t bytes, bool host) {
-        if (bytes <= b.cap) return;
-        if (b.p) host ? cudaFreeHost(b.p) : cudaFree(b.p);
-        b.p = nullptr;
-        b.cap = 0;
-        const size_t cap = std::max<size_t>(bytes, 1 << 16);
-        skg::check(host ? cudaHostAlloc(&b.p, cap, cudaHostAllocDefault) : cudaMalloc(&b.p, cap),
-                   host ? "cudaHostAlloc" : "cudaMalloc");
-        b.cap = cap;
-    }
-    void bind() {
-        int d = 0;
-        skg::check(cudaGetDevice(&d), "cudaGetDevice");
-        if (d != dev) {   // a different device than last time: drop the old buffers' capacities
-            hin = hout = din = dout = Buf{};
-            dev = d;
-        }
-    }
-};
-thread_local Workspace t_ws;
-
+// one-shot staging: host -> device -> host on the per-thread default stream, through the
+// per-thread grow-only pinned / device slots of skg::CallStage (no cudaMalloc / cudaFree per call)
 struct Stage {
     struct Ptr {
         void* p = nullptr;
     };
-    cudaStream_t st = cudaStreamPerThread;
+    skg::CallStage cs;
+    cudaStream_t st = cs.stream();
     Ptr in, out;
-    void put(const void* h, size_t bytes) {
-        skg::require_device();
-        t_ws.bind();
-        Workspace::grow(t_ws.hin, bytes, true);
-        Workspace::grow(t_ws.din, bytes, false);
-        std::memcpy(t_ws.hin.p, h, bytes);
-        skg::check(cudaMemcpyAsync(t_ws.din.p, t_ws.hin.p, bytes, cudaMemcpyHostToDevice, st), "H2D");
-        in.p = t_ws.din.p;
-    }
-    void alloc_out(size_t bytes) {
-        Workspace::grow(t_ws.dout, bytes, false);
-        out.p = t_ws.dout.p;
-    }
-    void get(void* h, size_t bytes) {
-        Workspace::grow(t_ws.hout, bytes, true);
-        skg::check(cudaMemcpyAsync(t_ws.hout.p, out.p, bytes, cudaMemcpyDeviceToHost, st), "D2H");
-        skg::check(cudaStreamSynchronize(st), "sync");
-        std::memcpy(h, t_ws.hout.p, bytes);
-    }
+    void put(const void* h, size_t bytes) { in.p = cs.up(h, bytes); }
+    void alloc_out(size_t bytes) { out.p = cs.scratch(bytes); }
+    void get(void* h, size_t bytes) { cs.down(h, out.p, bytes); }
 };
 
 void fft_inplace(double* re, double* im, size_t n, bool inverse) {   // numerics.cpp:102-120
@@ -290,10 +259,9 @@ sk_status sk_dft_naive(const double* re, const double* im, size_t n, double* out
         }
         Stage s;
         s.put(x.data(), n * sizeof(cd));
-        skg::DevMem dtw(n * sizeof(cd));
-        dtw.upload(tw.data(), n * sizeof(cd), s.st);
+        void* dtw = s.cs.up(tw.data(), n * sizeof(cd));
         s.alloc_out(n * sizeof(cd));
-        skg::check(skg::launch_dft_naive(s.in.p, (long long)n, dtw.p, s.out.p, s.st), "dft_naive");
+        skg::check(skg::launch_dft_naive(s.in.p, (long long)n, dtw, s.out.p, s.st), "dft_naive");
         skg::count_launch();
         s.get(x.data(), n * sizeof(cd));
         split(x, out_re, out_im);
@@ -318,9 +286,9 @@ sk_status sk_czt_direct(const double* re, const double* im, size_t n, double a_r
         std::vector<cd> x = join(re, im, n);
         Stage s;
         s.put(x.data(), n * sizeof(cd));
-        skg::DevMem xa(n * sizeof(cd));
+        void* xa = s.cs.scratch(n * sizeof(cd));
         s.alloc_out(m * sizeof(cd));
-        skg::check(skg::launch_czt_direct(s.in.p, (long long)n, A.log_mag, A.q, W.log_mag, W.q, (long long)m, xa.p,
+        skg::check(skg::launch_czt_direct(s.in.p, (long long)n, A.log_mag, A.q, W.log_mag, W.q, (long long)m, xa,
                                           s.out.p, s.st),
                    "czt_direct");
         skg::count_launch(2);
@@ -799,6 +767,8 @@ sk_status skg_device_info(int* device, int* sm_count, size_t* smem_optin, size_t
 
 uint64_t skg_launch_count(void) { return skg::launch_counter().load(); }
 
+void skg_debug_set_grid_cap(unsigned cap) { skg::grid_cap_ref().store(cap); }
+
 sk_status skg_synchronize(void* stream) {
     return guarded([&] { skg::check(cudaStreamSynchronize((cudaStream_t)stream), "cudaStreamSynchronize"); });
 }
@@ -811,6 +781,9 @@ sk_status skg_fft_batch(size_t n, int inverse, int precision, const void* d_in, 
         if (!skg::is_pow2(n))
             throw std::invalid_argument("fft: length " + std::to_string(n) + " is not a power of two; zero_pad to " +
                                         std::to_string(skg::next_pow2(n)) + " first");
+        need_precision("skg_fft_batch", precision);
+        need_stride("skg_fft_batch", "input", batch, in_stride, n);
+        need_stride("skg_fft_batch", "output", batch, out_stride, n);
         skg::fft_c2c(n, inverse != 0, precision == SKG_F32, d_in, (long long)in_stride, d_out, (long long)out_stride,
                      (long long)batch, (cudaStream_t)stream);
     });
@@ -821,6 +794,10 @@ sk_status skg_fft_spectrum_batch(size_t n, size_t transform_len, int precision, 
     if (!d_x || !d_out) return bad_arg("skg_fft_spectrum_batch: null buffer");
     return guarded([&] {
         if (n == 0) throw std::invalid_argument("trace: no samples");
+        need_precision("skg_fft_spectrum_batch", precision);
+        const size_t len = transform_len ? transform_len : skg::next_pow2(n);
+        need_stride("skg_fft_spectrum_batch", "trace", batch, x_stride, n);
+        need_stride("skg_fft_spectrum_batch", "output", batch, out_stride, layout == SKG_HALF ? len / 2 + 1 : len);
         skg::fft_spectrum_batch(n, transform_len, precision == SKG_F32, layout, d_x, (long long)x_stride,
                                 (long long)batch, d_out, (long long)out_stride, (cudaStream_t)stream);
     });
@@ -843,6 +820,10 @@ sk_status skg_fft_spectrum_band_batch(size_t n, size_t transform_len, int precis
     if (!d_x || (!d_bins && !d_db)) return bad_arg("skg_fft_spectrum_band_batch: null buffer");
     return guarded([&] {
         if (n == 0) throw std::invalid_argument("trace: no samples");
+        need_precision("skg_fft_spectrum_band_batch", precision);
+        need_stride("skg_fft_spectrum_band_batch", "trace", batch, x_stride, n);
+        if (d_bins) need_stride("skg_fft_spectrum_band_batch", "bins", batch, bins_stride, count);
+        if (d_db) need_stride("skg_fft_spectrum_band_batch", "dB", batch, db_stride, count);
         skg::fft_spectrum_band_batch(n, transform_len, precision == SKG_F32, (long long)k_lo, (long long)count, d_x,
                                      (long long)x_stride, (long long)batch, d_bins, (long long)bins_stride, d_db,
                                      (long long)db_stride, (cudaStream_t)stream);
@@ -854,6 +835,10 @@ sk_status skg_band_db_batch(int precision, const void* d_in, size_t in_stride, s
     if (!d_in || (!d_bins && !d_db)) return bad_arg("skg_band_db_batch: null buffer");
     if (count == 0) return bad_arg("slice_band: no bins fall inside the requested band");
     return guarded([&] {
+        need_precision("skg_band_db_batch", precision);
+        need_stride("skg_band_db_batch", "input", batch, in_stride, k_lo + count);
+        if (d_bins) need_stride("skg_band_db_batch", "bins", batch, bins_stride, count);
+        if (d_db) need_stride("skg_band_db_batch", "dB", batch, db_stride, count);
         skg::band_db_batch(precision == SKG_F32, d_in, (long long)in_stride, (long long)k_lo, (long long)count,
                            (long long)batch, d_bins, (long long)bins_stride, d_db, (long long)db_stride,
                            (cudaStream_t)stream);
@@ -864,6 +849,7 @@ sk_status skg_czt_plan_create(size_t n, double a_re, double a_im, double w_re, d
                               skg_czt_plan** out) {
     if (!out) return bad_arg("skg_czt_plan_create: null output");
     return guarded([&] {
+        need_precision("skg_czt_plan_create", precision);
         auto p = std::make_unique<skg::CztPlanG>(n, cd(a_re, a_im), cd(w_re, w_im), m);
         *out = new skg_czt_plan{std::move(p), precision == SKG_F32};
     });
@@ -875,6 +861,8 @@ sk_status skg_czt_execute(const skg_czt_plan* p, const void* d_x, int x_complex,
                           void* d_out, size_t out_stride, void* stream) {
     if (!p || !d_x || !d_out) return bad_arg("skg_czt_execute: null argument");
     return guarded([&] {
+        need_stride("skg_czt_execute", "trace", batch, x_stride, p->p->input_size());
+        need_stride("skg_czt_execute", "output", batch, out_stride, p->p->output_size());
         p->p->execute(d_x, x_complex != 0, (long long)x_stride, (long long)batch, d_out, (long long)out_stride, p->f32,
                       (cudaStream_t)stream);
     });
@@ -884,6 +872,7 @@ sk_status skg_transfer_plan_create(const double* ref, size_t n, size_t transform
                                    skg_transfer_plan** out) {
     if (!ref || !out) return bad_arg("skg_transfer_plan_create: null argument");
     return guarded([&] {
+        need_precision("skg_transfer_plan_create", precision);
         auto p = std::make_unique<skg::TransferPlanG>(ref, n, transform_len, precision == SKG_F32);
         *out = new skg_transfer_plan{std::move(p)};
     });
@@ -901,6 +890,9 @@ sk_status skg_transfer_execute(const skg_transfer_plan* p, const void* d_x, size
                                void* stream) {
     if (!p || !d_x || !d_mag || !d_phase) return bad_arg("skg_transfer_execute: null argument");
     return guarded([&] {
+        need_stride("skg_transfer_execute", "trace", batch, x_stride, p->p->input_size());
+        need_stride("skg_transfer_execute", "|H| / arg H", batch, mp_stride, p->p->bins());
+        if (d_h) need_stride("skg_transfer_execute", "H", batch, h_stride, p->p->bins());
         p->p->execute(d_x, (long long)x_stride, (long long)batch, d_mag, d_phase, (long long)mp_stride, d_h,
                       (long long)h_stride, (cudaStream_t)stream);
     });
@@ -910,6 +902,7 @@ sk_status skg_zoom_plan_create(size_t input_len, double f1, double f2, double fs
                                const skg_zoom_ext* ext, int precision, skg_zoom_plan** out) {
     if (!out) return bad_arg("skg_zoom_plan_create: null output");
     return guarded([&] {
+        need_precision("skg_zoom_plan_create", precision);
         auto p = std::make_unique<skg::ZoomPlanG>(input_len, f1, f2, fs, to_opts(opts), ext ? ext->n_fft : 0,
                                                   ext ? ext->taps : nullptr, ext ? ext->num_taps : 0);
         *out = new skg_zoom_plan{std::move(p), precision == SKG_F32};
@@ -932,8 +925,89 @@ sk_status skg_zoom_execute(const skg_zoom_plan* p, const void* d_x, size_t x_str
                            size_t out_stride, void* stream) {
     if (!p || !d_x || !d_out) return bad_arg("skg_zoom_execute: null argument");
     return guarded([&] {
+        need_stride("skg_zoom_execute", "trace", batch, x_stride, p->p->input_len);
+        if (p->p->k_hi >= p->p->k_lo) need_stride("skg_zoom_execute", "output", batch, out_stride, p->p->bins());
         p->p->execute(d_x, (long long)x_stride, (long long)batch, d_out, (long long)out_stride, p->f32,
                       (cudaStream_t)stream);
+    });
+}
+
+
+// ---- host-buffer batched calls (staging.hpp pipeline) ---------------------------------------------
+sk_status skg_czt_execute_host(const skg_czt_plan* p, const void* h_x, int x_complex, size_t x_stride, size_t batch,
+                               void* h_out, size_t out_stride, size_t chunk) {
+    if (!p || !h_x || !h_out) return bad_arg("skg_czt_execute_host: null argument");
+    return guarded([&] {
+        const skg::CztPlanG& g = *p->p;
+        const size_t n = g.input_size(), m = g.output_size();
+        need_stride("skg_czt_execute_host", "trace", batch, x_stride, n);
+        need_stride("skg_czt_execute_host", "output", batch, out_stride, m);
+        const size_t rs = p->f32 ? 4 : 8, es = x_complex ? 2 * rs : rs;
+        skg::HostPlane in{const_cast<void*>(h_x), x_stride * es, n * es};
+        skg::HostPlane out{h_out, out_stride * 2 * rs, m * 2 * rs};
+        skg::run_host_batched(in, {out}, (long long)batch, (long long)chunk,
+                              [&](const void* dx, void* const* dout, long long rows, cudaStream_t st) {
+                                  g.execute(dx, x_complex != 0, (long long)n, rows, dout[0], (long long)m, p->f32, st);
+                              });
+    });
+}
+
+sk_status skg_fft_spectrum_host(size_t n, size_t transform_len, int precision, int layout, const void* h_x,
+                                size_t x_stride, size_t batch, void* h_out, size_t out_stride, size_t chunk) {
+    if (!h_x || !h_out) return bad_arg("skg_fft_spectrum_host: null buffer");
+    return guarded([&] {
+        if (n == 0) throw std::invalid_argument("trace: no samples");
+        need_precision("skg_fft_spectrum_host", precision);
+        const size_t len = transform_len ? transform_len : skg::next_pow2(n);
+        const size_t nb = layout == SKG_HALF ? len / 2 + 1 : len;
+        need_stride("skg_fft_spectrum_host", "trace", batch, x_stride, n);
+        need_stride("skg_fft_spectrum_host", "output", batch, out_stride, nb);
+        const bool f32 = precision == SKG_F32;
+        const size_t rs = f32 ? 4 : 8;
+        skg::HostPlane in{const_cast<void*>(h_x), x_stride * rs, n * rs};
+        skg::HostPlane out{h_out, out_stride * 2 * rs, nb * 2 * rs};
+        skg::run_host_batched(in, {out}, (long long)batch, (long long)chunk,
+                              [&](const void* dx, void* const* dout, long long rows, cudaStream_t st) {
+                                  skg::fft_spectrum_batch(n, len, f32, layout, dx, (long long)n, rows, dout[0],
+                                                          (long long)nb, st);
+                              });
+    });
+}
+
+sk_status skg_zoom_execute_host(const skg_zoom_plan* p, const void* h_x, size_t x_stride, size_t batch, void* h_out,
+                                size_t out_stride, size_t chunk) {
+    if (!p || !h_x || !h_out) return bad_arg("skg_zoom_execute_host: null argument");
+    return guarded([&] {
+        const skg::ZoomPlanG& z = *p->p;
+        if (z.k_lo > z.k_hi) throw std::invalid_argument("zoom_fft: no transform bins fall inside the band");
+        const size_t n = z.input_len, nb = z.bins();
+        need_stride("skg_zoom_execute_host", "trace", batch, x_stride, n);
+        need_stride("skg_zoom_execute_host", "output", batch, out_stride, nb);
+        const size_t rs = p->f32 ? 4 : 8;
+        skg::HostPlane in{const_cast<void*>(h_x), x_stride * rs, n * rs};
+        skg::HostPlane out{h_out, out_stride * 2 * rs, nb * 2 * rs};
+        skg::run_host_batched(in, {out}, (long long)batch, (long long)chunk,
+                              [&](const void* dx, void* const* dout, long long rows, cudaStream_t st) {
+                                  z.execute(dx, (long long)n, rows, dout[0], (long long)nb, p->f32, st);
+                              });
+    });
+}
+
+sk_status skg_transfer_execute_host(const skg_transfer_plan* p, const void* h_x, size_t x_stride, size_t batch,
+                                    void* h_mag, void* h_phase, size_t mp_stride, size_t chunk) {
+    if (!p || !h_x || !h_mag || !h_phase) return bad_arg("skg_transfer_execute_host: null argument");
+    return guarded([&] {
+        const skg::TransferPlanG& t = *p->p;
+        const size_t n = t.input_size(), nb = t.bins();
+        need_stride("skg_transfer_execute_host", "trace", batch, x_stride, n);
+        need_stride("skg_transfer_execute_host", "|H| / arg H", batch, mp_stride, nb);
+        const size_t rs = t.f32() ? 4 : 8;
+        skg::HostPlane in{const_cast<void*>(h_x), x_stride * rs, n * rs};
+        skg::HostPlane mag{h_mag, mp_stride * rs, nb * rs}, ph{h_phase, mp_stride * rs, nb * rs};
+        skg::run_host_batched(in, {mag, ph}, (long long)batch, (long long)chunk,
+                              [&](const void* dx, void* const* dout, long long rows, cudaStream_t st) {
+                                  t.execute(dx, (long long)n, rows, dout[0], dout[1], (long long)nb, nullptr, 0, st);
+                              });
     });
 }
 

@@ -58,6 +58,12 @@ int current_device() {
     return d;
 }
 
+std::atomic<unsigned>& grid_cap_ref() {
+    static std::atomic<unsigned> c{0};
+    return c;
+}
+unsigned grid_cap() { return grid_cap_ref().load(std::memory_order_relaxed); }
+
 std::atomic<uint64_t>& launch_counter() {
     static std::atomic<uint64_t> c{0};
     return c;
@@ -456,9 +462,8 @@ CztPlanG::CztPlanG(size_t n, cd a, cd w, size_t m) : n_(n), m_(m) {
 }
 
 const CztPlanG::Dev& CztPlanG::dev(bool f32) const {
-    std::call_once(once_[f32 ? 1 : 0], [&] {
-        require_device();
-        Dev& d = dev_[f32 ? 1 : 0];
+    require_device();
+    return devs_.get(f32, [&](Dev& d) {
         d.cin = to_device(cin_, f32);
         d.cout = to_device(cout_, f32);
         // kernel spectrum: forward FFT of the circular chirp on the GPU in fp64, scaled by 1/L so the
@@ -502,7 +507,6 @@ const CztPlanG::Dev& CztPlanG::dev(bool f32) const {
         }
         check(cudaStreamSynchronize(nullptr), "czt plan upload");
     });
-    return dev_[f32 ? 1 : 0];
 }
 
 void CztPlanG::execute(const void* x, bool complex_in, long long x_stride, long long batch, void* out,
@@ -734,13 +738,24 @@ TransferPlanG::TransferPlanG(const double* ref, size_t n, size_t len, bool f32) 
     fft_spectrum_batch(n, len_, false, 1, dref.p, 0, 1, dx.p, 0, nullptr);
     xref_.resize(bins());
     check(cudaMemcpy(xref_.data(), dx.p, bins() * sizeof(cd), cudaMemcpyDeviceToHost), "D2H");
-    std::vector<cd> r(bins());
+    // 1 / X_ref = conj(v) / |v| / |v|: no |v|^2 underflow for tiny bins (the oracle divides directly;
+    // its quotient is inf / NaN only where X_ref is exactly 0, and there H is reported as 0)
+    rtab_h_.resize(bins());
     for (size_t k = 0; k < bins(); ++k) {
         const cd v = xref_[k];
-        const double den = v.real() * v.real() + v.imag() * v.imag();
-        r[k] = den > 0.0 ? cd(v.real() / den, -v.imag() / den) : cd(0.0, 0.0);
+        const double mag = std::hypot(v.real(), v.imag());
+        if (mag > 0.0) {
+            const double s = 1.0 / mag;
+            rtab_h_[k] = cd(v.real() * s * s, -v.imag() * s * s);
+        } else {
+            rtab_h_[k] = cd(0.0, 0.0);
+        }
     }
-    rtab_ = to_device(r, f32);
+    rtab(f32);
+}
+
+const void* TransferPlanG::rtab(bool f32) const {
+    return rtab_.get(f32, [&](DevMem& d) { d = to_device(rtab_h_, f32); }).p;
 }
 
 void TransferPlanG::execute(const void* x, long long x_stride, long long batch, void* mag, void* phase,
@@ -754,10 +769,10 @@ void TransferPlanG::execute(const void* x, long long x_stride, long long batch, 
     cudaError_t e;
     if (f32_)
         e = launch_fft_r2c<float>(lgM, (long long)n_, (const float*)x, x_stride, batch, tw, post, 2, h, h_stride,
-                                  rtab_.p, (float*)mag, (float*)phase, mp_stride, 0, 0, st);
+                                  rtab(true), (float*)mag, (float*)phase, mp_stride, 0, 0, st);
     else
         e = launch_fft_r2c<double>(lgM, (long long)n_, (const double*)x, x_stride, batch, tw, post, 2, h, h_stride,
-                                   rtab_.p, (double*)mag, (double*)phase, mp_stride, 0, 0, st);
+                                   rtab(false), (double*)mag, (double*)phase, mp_stride, 0, 0, st);
     check(e, "transfer launch");
     count_launch();
 }

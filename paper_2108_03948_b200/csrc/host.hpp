@@ -31,6 +31,7 @@ int current_device();
 // stream-ordered work buffer from the default pool (kept cached across synchronisations); free with cudaFreeAsync
 void* stream_alloc(size_t bytes, cudaStream_t st);
 std::atomic<uint64_t>& launch_counter();
+std::atomic<unsigned>& grid_cap_ref();   // skg_debug_set_grid_cap
 inline void count_launch(int n = 1) { launch_counter().fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
 // ---- numerics restated from the reference (fp64, host) ----------------------------------
@@ -60,6 +61,27 @@ struct DevMem {
 };
 // fp64 complex host table -> device table in the requested precision
 DevMem to_device(const std::vector<cd>& h, bool f32);
+
+// Plan tables keyed by (device, precision): a plan shared by threads bound to different GPUs
+// builds one set of device tables per GPU on first use there (the Stockham twiddles are keyed the
+// same way), so no kernel is ever handed another device's pointers.
+template <typename D> class PerDevice {
+  public:
+    template <typename F> const D& get(bool f32, F&& build) const {
+        const int key = current_device() * 2 + (f32 ? 1 : 0);
+        std::lock_guard<std::mutex> lk(mu_);
+        for (const auto& e : sets_)
+            if (e.first == key) return *e.second;
+        auto d = std::make_unique<D>();
+        build(*d);
+        sets_.emplace_back(key, std::move(d));
+        return *sets_.back().second;
+    }
+
+  private:
+    mutable std::mutex mu_;
+    mutable std::vector<std::pair<int, std::unique_ptr<D>>> sets_;
+};
 
 // cached per-device twiddle tables for the Stockham engine (FftGeom<log2L>)
 const void* stockham_twiddles(int log2L, bool f32);
@@ -101,10 +123,7 @@ class CztPlanG {
     int log2L_;   // of Ls_
     std::vector<cd> cin_, cout_, kern_;
     std::vector<cd> kern_sf_, cout_sf_;   // nseg x Ls kernel segments, nseg x seg output chirps
-    mutable std::once_flag once_[2];
-    mutable Dev dev_[2];
-    mutable DevMem work_;   // four-step scratch (lazily sized)
-    mutable std::mutex work_mu_;
+    PerDevice<Dev> devs_;
 };
 
 // zero-padded spectrum of real traces; layout 0 full, 1 half (pow2 only)
@@ -129,7 +148,10 @@ class TransferPlanG {
   public:
     TransferPlanG(const double* ref, size_t n, size_t len, bool f32);
     size_t bins() const { return len_ / 2 + 1; }
+    size_t input_size() const { return n_; }
+    bool f32() const { return f32_; }
     const std::vector<cd>& reference_spectrum() const { return xref_; }
+    const void* rtab(bool f32) const;   // device 1 / X_ref on the current device
     void execute(const void* x, long long x_stride, long long batch, void* mag, void* phase,
                  long long mp_stride, void* h, long long h_stride, cudaStream_t st) const;
 
@@ -137,7 +159,8 @@ class TransferPlanG {
     size_t n_, len_;
     bool f32_;
     std::vector<cd> xref_;
-    DevMem rtab_;
+    std::vector<cd> rtab_h_;   // 1 / X_ref, fp64
+    PerDevice<DevMem> rtab_;
 };
 
 struct ZoomOptionsG {                 // ZoomOptions, zoomfft.hpp:17-26
@@ -190,8 +213,7 @@ class ZoomPlanG {                     // ZoomFftPlan + make_zoom_plan, zoomfft.h
     const Dev& dev(bool f32) const;
     void compute_band();
     bool spectral_route_ok() const;
-    mutable std::once_flag once_[2];
-    mutable Dev dev_[2];
+    PerDevice<Dev> devs_;
     std::unique_ptr<CztPlanG> bluestein_;   // n_fft not a power of two (dft_any route)
 };
 

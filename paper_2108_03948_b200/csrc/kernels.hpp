@@ -6,6 +6,11 @@
 
 namespace skg {
 
+// Test hook (skg_debug_set_grid_cap): upper bound on every persistent grid, 0 = none. Lets the
+// parity tests drive the persistent loops (later units, L2 prefetch, workspace-slot reuse) through
+// many waves at batch sizes the CPU oracle checks in seconds.
+unsigned grid_cap();
+
 // One row of the launch table: which single-CTA sizes exist.
 constexpr int kMaxLog2F64 = 13;   // 8192 complex fp64 = 136 KB padded SMEM
 constexpr int kMaxLog2F32 = 14;   // 16384 complex fp32

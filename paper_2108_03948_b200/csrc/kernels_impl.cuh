@@ -42,7 +42,8 @@ template <typename K> inline unsigned persistent_grid(K kernel, int block, size_
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem) != cudaSuccess || per_sm < 1)
         per_sm = 1;
-    const long long cap = (long long)per_sm * sms;
+    long long cap = (long long)per_sm * sms;
+    if (const unsigned gc = grid_cap(); gc && gc < cap) cap = gc;
     return (unsigned)(units < cap ? (units > 0 ? units : 1) : cap);
 }
 

@@ -15,6 +15,7 @@
 #include "analysis.hpp"
 #include "host.hpp"
 #include "io.hpp"
+#include "staging.hpp"
 
 namespace skg {
 cudaError_t launch_dft_naive(const void* x, long long n, const void* tw, void* out, cudaStream_t st);
@@ -30,22 +31,8 @@ namespace spectral {
 namespace {
 #define kStream cudaStreamPerThread
 
-// host span -> device buffer -> kernel -> host vector
-struct Dev {
-    skg::DevMem m;
-    explicit Dev(size_t bytes) : m(bytes) {}
-    void* p() const { return m.p; }
-};
-Dev up(const void* h, size_t bytes) {
-    skg::require_device();
-    Dev d(bytes);
-    skg::check(cudaMemcpyAsync(d.p(), h, bytes, cudaMemcpyHostToDevice, kStream), "H2D");
-    return d;
-}
-void down(void* h, const Dev& d, size_t bytes) {
-    skg::check(cudaMemcpyAsync(h, d.p(), bytes, cudaMemcpyDeviceToHost, kStream), "D2H");
-    skg::check(cudaStreamSynchronize(kStream), "sync");
-}
+// host span -> device slot -> kernel -> host vector: every call stages through the calling thread's
+// grow-only pinned / device slots (skg::CallStage), never a cudaMalloc / cudaFree per call
 }  // namespace
 
 // ---- types.cpp ---------------------------------------------------------------------------------
@@ -83,11 +70,14 @@ ComplexBuffer dft_naive(std::span<const cplx> x) {
         const double ang = -2.0 * M_PI * static_cast<double>(r) / static_cast<double>(n);
         tw[r] = cplx(std::cos(ang), std::sin(ang));
     }
-    Dev dx = up(x.data(), n * sizeof(cplx)), dt = up(tw.data(), n * sizeof(cplx)), dy(n * sizeof(cplx));
-    skg::check(skg::launch_dft_naive(dx.p(), (long long)n, dt.p(), dy.p(), kStream), "dft_naive");
+    skg::CallStage cs;
+    void* dx = cs.up(x.data(), n * sizeof(cplx));
+    void* dt = cs.up(tw.data(), n * sizeof(cplx));
+    void* dy = cs.scratch(n * sizeof(cplx));
+    skg::check(skg::launch_dft_naive(dx, (long long)n, dt, dy, kStream), "dft_naive");
     skg::count_launch();
     ComplexBuffer y(n);
-    down(y.data(), dy, n * sizeof(cplx));
+    cs.down(y.data(), dy, n * sizeof(cplx));
     return y;
 }
 
@@ -97,9 +87,10 @@ FftPlan::FftPlan(std::size_t n) : n_(n) {
 
 void FftPlan::run(std::span<cplx> a, bool invert) const {
     if (a.size() != n_) throw std::invalid_argument("FftPlan: buffer size does not match plan");
-    Dev d = up(a.data(), n_ * sizeof(cplx));
-    skg::fft_c2c(n_, invert, false, d.p(), 0, d.p(), 0, 1, kStream);
-    down(a.data(), d, n_ * sizeof(cplx));
+    skg::CallStage cs;
+    void* d = cs.up(a.data(), n_ * sizeof(cplx));
+    skg::fft_c2c(n_, invert, false, d, 0, d, 0, 1, kStream);
+    cs.down(a.data(), d, n_ * sizeof(cplx));
 }
 void FftPlan::forward(std::span<cplx> data) const { run(data, false); }
 void FftPlan::inverse(std::span<cplx> data) const { run(data, true); }
@@ -142,13 +133,16 @@ ComplexBuffer czt_direct(std::span<const cplx> x, const CztParams& p) {
     if (x.empty()) throw std::invalid_argument("czt_direct: empty input");
     const skg::PolarPow A(p.a), W(p.w);
     const size_t n = x.size();
-    Dev dx = up(x.data(), n * sizeof(cplx)), xa(n * sizeof(cplx)), dy(p.m * sizeof(cplx));
-    skg::check(skg::launch_czt_direct(dx.p(), (long long)n, A.log_mag, A.q, W.log_mag, W.q, (long long)p.m, xa.p(),
-                                      dy.p(), kStream),
+    skg::CallStage cs;
+    void* dx = cs.up(x.data(), n * sizeof(cplx));
+    void* xa = cs.scratch(n * sizeof(cplx));
+    void* dy = cs.scratch(p.m * sizeof(cplx));
+    skg::check(skg::launch_czt_direct(dx, (long long)n, A.log_mag, A.q, W.log_mag, W.q, (long long)p.m, xa,
+                                      dy, kStream),
                "czt_direct");
     skg::count_launch(2);
     ComplexBuffer y(p.m);
-    down(y.data(), dy, p.m * sizeof(cplx));
+    cs.down(y.data(), dy, p.m * sizeof(cplx));
     return y;
 }
 
@@ -165,17 +159,21 @@ void CztPlan::execute(std::span<const cplx> x, std::span<cplx> conv_scratch, std
     if (x.size() != input_size()) throw std::invalid_argument("CztPlan: input length does not match plan");
     if (conv_scratch.size() != conv_size() || out.size() != output_size())
         throw std::invalid_argument("CztPlan: scratch/output size mismatch");
-    Dev dx = up(x.data(), x.size() * sizeof(cplx)), dy(out.size() * sizeof(cplx));
-    G(impl_).execute(dx.p(), true, 0, 1, dy.p(), 0, false, kStream);
-    down(out.data(), dy, out.size() * sizeof(cplx));
+    skg::CallStage cs;
+    void* dx = cs.up(x.data(), x.size() * sizeof(cplx));
+    void* dy = cs.scratch(out.size() * sizeof(cplx));
+    G(impl_).execute(dx, true, 0, 1, dy, 0, false, kStream);
+    cs.down(out.data(), dy, out.size() * sizeof(cplx));
 }
 
 ComplexBuffer CztPlan::execute(std::span<const cplx> x) const {
     if (x.size() != input_size()) throw std::invalid_argument("CztPlan: input length does not match plan");
     ComplexBuffer out(output_size());
-    Dev dx = up(x.data(), x.size() * sizeof(cplx)), dy(out.size() * sizeof(cplx));
-    G(impl_).execute(dx.p(), true, 0, 1, dy.p(), 0, false, kStream);
-    down(out.data(), dy, out.size() * sizeof(cplx));
+    skg::CallStage cs;
+    void* dx = cs.up(x.data(), x.size() * sizeof(cplx));
+    void* dy = cs.scratch(out.size() * sizeof(cplx));
+    G(impl_).execute(dx, true, 0, 1, dy, 0, false, kStream);
+    cs.down(out.data(), dy, out.size() * sizeof(cplx));
     return out;
 }
 
@@ -204,11 +202,13 @@ Spectrum czt_spectrum(const Trace& trace, double f1, double f2, std::size_t m) {
     const CztParams p = czt_params_for_band(f1, f2, trace.sample_rate_hz, m);
     const size_t n = trace.samples.size();
     skg::CztPlanG plan(n, p.a, p.w, p.m);
-    Dev dx = up(trace.samples.data(), n * sizeof(double)), dy(m * sizeof(cplx));
-    plan.execute(dx.p(), false, 0, 1, dy.p(), 0, false, kStream);
+    skg::CallStage cs;
+    void* dx = cs.up(trace.samples.data(), n * sizeof(double));
+    void* dy = cs.scratch(m * sizeof(cplx));
+    plan.execute(dx, false, 0, 1, dy, 0, false, kStream);
     Spectrum s;
     s.bins.resize(m);
-    down(s.bins.data(), dy, m * sizeof(cplx));
+    cs.down(s.bins.data(), dy, m * sizeof(cplx));
     s.f_start_hz = f1;
     s.f_step_hz = (f2 - f1) / static_cast<double>(m);
     s.source_n = n;
@@ -221,11 +221,13 @@ Spectrum fft_spectrum(const Trace& t, std::size_t transform_len) {
     const size_t n = t.size();
     const size_t len = transform_len == 0 ? skg::next_pow2(n) : transform_len;
     if (len < n) throw std::invalid_argument("fft_spectrum: transform length shorter than the trace");
-    Dev dx = up(t.samples.data(), n * sizeof(double)), dy(len * sizeof(cplx));
-    skg::fft_spectrum_batch(n, len, false, 0, dx.p(), 0, 1, dy.p(), 0, kStream);
+    skg::CallStage cs;
+    void* dx = cs.up(t.samples.data(), n * sizeof(double));
+    void* dy = cs.scratch(len * sizeof(cplx));
+    skg::fft_spectrum_batch(n, len, false, 0, dx, 0, 1, dy, 0, kStream);
     Spectrum s;
     s.bins.resize(len);
-    down(s.bins.data(), dy, len * sizeof(cplx));
+    cs.down(s.bins.data(), dy, len * sizeof(cplx));
     s.f_start_hz = 0.0;
     s.f_step_hz = t.sample_rate_hz / static_cast<double>(len);
     s.source_n = len;
@@ -262,13 +264,14 @@ static ComplexBuffer shift_impl(const double* xr, const cplx* xc, size_t n, doub
     if (!(fs > 0.0)) throw std::invalid_argument("frequency_shift: sample rate must be positive");
     ComplexBuffer y(n);
     if (n == 0) return y;
-    Dev dx = xr ? up(xr, n * sizeof(double)) : up(xc, n * sizeof(cplx));
-    Dev dy(n * sizeof(cplx));
-    skg::check(skg::launch_freq_shift(xr ? (const double*)dx.p() : nullptr, xr ? nullptr : dx.p(), (long long)n,
-                                      -f / fs, dy.p(), kStream),
+    skg::CallStage cs;
+    void* dx = xr ? cs.up(xr, n * sizeof(double)) : cs.up(xc, n * sizeof(cplx));
+    void* dy = cs.scratch(n * sizeof(cplx));
+    skg::check(skg::launch_freq_shift(xr ? (const double*)dx : nullptr, xr ? nullptr : dx, (long long)n,
+                                      -f / fs, dy, kStream),
                "frequency_shift");
     skg::count_launch();
-    down(y.data(), dy, n * sizeof(cplx));
+    cs.down(y.data(), dy, n * sizeof(cplx));
     return y;
 }
 ComplexBuffer frequency_shift(std::span<const double> x, double f, double fs) {
@@ -282,13 +285,15 @@ static ComplexBuffer fd_impl(std::span<const cplx> x, std::span<const double> ta
     const size_t n = x.size();
     ComplexBuffer out(n / (d ? d : 1));
     if (out.empty()) return out;
-    Dev dx = up(x.data(), n * sizeof(cplx)), dt = up(taps.data(), taps.size() * sizeof(double));
-    Dev dy(out.size() * sizeof(cplx));
-    skg::check(skg::launch_filter_decimate(dx.p(), (long long)n, (const double*)dt.p(), (int)taps.size(), (int)d,
-                                           circular ? 1 : 0, dy.p(), (long long)out.size(), kStream),
+    skg::CallStage cs;
+    void* dx = cs.up(x.data(), n * sizeof(cplx));
+    void* dt = cs.up(taps.data(), taps.size() * sizeof(double));
+    void* dy = cs.scratch(out.size() * sizeof(cplx));
+    skg::check(skg::launch_filter_decimate(dx, (long long)n, (const double*)dt, (int)taps.size(), (int)d,
+                                           circular ? 1 : 0, dy, (long long)out.size(), kStream),
                "filter_decimate");
     skg::count_launch();
-    down(out.data(), dy, out.size() * sizeof(cplx));
+    cs.down(out.data(), dy, out.size() * sizeof(cplx));
     return out;
 }
 ComplexBuffer filter_decimate(std::span<const cplx> x, std::span<const double> taps, std::size_t d) {
@@ -387,11 +392,13 @@ Spectrum zoom_fft(const ZoomFftPlan& plan, const Trace& t) {   // zoomfft.cpp:18
     }
     const skg::ZoomPlanG& z = *dev->plan;
     if (z.k_lo > z.k_hi) throw std::invalid_argument("zoom_fft: no transform bins fall inside the band");
-    Dev dx = up(t.samples.data(), t.size() * sizeof(double)), dy(z.bins() * sizeof(cplx));
-    z.execute(dx.p(), 0, 1, dy.p(), 0, false, kStream);
+    skg::CallStage cs;
+    void* dx = cs.up(t.samples.data(), t.size() * sizeof(double));
+    void* dy = cs.scratch(z.bins() * sizeof(cplx));
+    z.execute(dx, 0, 1, dy, 0, false, kStream);
     Spectrum s;
     s.bins.resize(z.bins());
-    down(s.bins.data(), dy, z.bins() * sizeof(cplx));
+    cs.down(s.bins.data(), dy, z.bins() * sizeof(cplx));
     s.f_start_hz = z.f_start_hz();
     s.f_step_hz = z.f_step_hz();
     s.source_n = z.n_fft;

@@ -155,9 +155,8 @@ ZoomArgs make_args(const ZoomPlanG& p) {
 }  // namespace
 
 const ZoomPlanG::Dev& ZoomPlanG::dev(bool f32) const {
-    std::call_once(once_[f32 ? 1 : 0], [&] {
-        require_device();
-        Dev& d = dev_[f32 ? 1 : 0];
+    require_device();
+    return devs_.get(f32, [&](Dev& d) {
         const ZoomArgs a = make_args(*this);
         const double qc = -center_hz / sample_rate_hz;   // zoomfft.cpp:174
         const int D = a.D, T = a.T;
@@ -204,7 +203,6 @@ const ZoomPlanG::Dev& ZoomPlanG::dev(bool f32) const {
             d.hf = to_device(hf, f32);
         }
     });
-    return dev_[f32 ? 1 : 0];
 }
 
 void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void* out, long long out_stride,
