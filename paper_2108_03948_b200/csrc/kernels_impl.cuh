@@ -550,7 +550,9 @@ cudaError_t run_czt(long long N, long long M, bool complex_in, const void* x, lo
     if constexpr (FftGeom<LOG2L>::NT >= 32) {
         const size_t rts = rt_smem_bytes<T, LOG2L>(N, seg_len);
         static const bool rt_off = getenv("SKG_CZT_NO_RT") != nullptr;
-        if (!rt_off && rts <= (size_t)smem_optin() && batch >= 8) {
+        // the route depends on the plan only, never on the batch size, so a batch split into chunks
+        // (skg_*_host) gives bit-identical rows
+        if (!rt_off && rts <= (size_t)smem_optin()) {
             auto launch = [&](auto kern) {
                 cudaError_t e = prep_smem(kern, rts);
                 if (e != cudaSuccess) return e;
@@ -653,7 +655,6 @@ cudaError_t run_czt_sf(long long N, long long M, bool complex_in, const void* x,
         return cudaErrorNotSupported;
     } else {
         const size_t lim = (size_t)smem_optin();
-        if (batch < 8) return cudaErrorNotSupported;
         // configurations in preference order (measured on configs[1]); SKG_CZT_SF_CFG="rg,ts" pins one
         static const char* env = getenv("SKG_CZT_SF_CFG");
         int want_rg = 0, want_ts = -1;
