@@ -11,6 +11,7 @@
 
 #include "fft_device.cuh"
 #include "kernels.hpp"
+#include "kernels_czt_tm.cuh"
 
 namespace skg {
 
@@ -659,6 +660,26 @@ cudaError_t run_czt_sf(long long N, long long M, bool complex_in, const void* x,
         static const char* env = getenv("SKG_CZT_SF_CFG");
         int want_rg = 0, want_ts = -1;
         if (env) sscanf(env, "%d,%d", &want_rg, &want_ts);
+        // tensor-memory variant first (kernels_czt_tm.cuh): 128-thread transforms (L = 2048) whose
+        // tables + parked spectra fit the 512 TMEM columns; SKG_CZT_NO_TM=1 for the A/B
+        static const bool no_tm = getenv("SKG_CZT_NO_TM") != nullptr;
+        if constexpr (FftGeom<LOG2L>::NT == 128) {
+            constexpr int RG = 4;
+            using TK = TmCfg<T, LOG2L, NZ, NO, RG>;
+            if (!no_tm && !want_rg && TK::cols(nseg) <= 512 && TK::smem_bytes() <= lim) {
+                auto launch = [&](auto kern) {
+                    cudaError_t e = prep_smem(kern, TK::smem_bytes());
+                    if (e != cudaSuccess) return e;
+                    const unsigned g = persistent_grid(kern, TK::BLOCK, TK::smem_bytes(), (batch + RG - 1) / RG);
+                    kern<<<g, TK::BLOCK, TK::smem_bytes(), st>>>(x, x_stride, N, M, batch, nseg, seg_len, (C*)out,
+                                                                 out_stride, (const C*)tw, (const C*)cin,
+                                                                 (const C*)khat, (const C*)cout);
+                    return cudaGetLastError();
+                };
+                return complex_in ? launch(k_czt_tm<T, LOG2L, NZ, NO, true, RG>)
+                                  : launch(k_czt_tm<T, LOG2L, NZ, NO, false, RG>);
+            }
+        }
         auto go = [&](auto rgc, auto tsc) -> cudaError_t {
             constexpr int RG = decltype(rgc)::value, TS = decltype(tsc)::value;
             if (want_rg && (want_rg != RG || want_ts != TS)) return cudaErrorNotSupported;
