@@ -20,6 +20,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "tmem.cuh"
+
 namespace skg {
 
 template <typename T> struct CxT;
@@ -344,9 +346,12 @@ struct GroupSync {
 };
 
 // One Stockham pass. v[q] holds position tid + NT*q on entry and exit.
-template <bool INV, int S, int NZ, int NO, int LOG2L, typename C, typename SYNC = CtaSync>
+// TMT: the pass is a last radix-16 pass with one butterfly per thread (k = tid) and its fifteen
+// twiddles W^{jk} come precomputed from this thread's TMEM lane at `tmt` (16 complex, j = 0..15;
+// kernels_czt_tm.cuh) instead of being formed by products from the per-digit tables.
+template <bool INV, int S, int NZ, int NO, int LOG2L, typename C, typename SYNC = CtaSync, bool TMT = false>
 __device__ __forceinline__ void stockham_pass(C (&v)[FftGeom<LOG2L>::EPT], C* sm, const C* __restrict__ tw,
-                                              int tid, bool active = true, SYNC sync = SYNC()) {
+                                              int tid, bool active = true, SYNC sync = SYNC(), uint32_t tmt = 0) {
     using G = FftGeom<LOG2L>;
     constexpr int R = G::radix(S);
     constexpr int p = G::pval(S);
@@ -359,7 +364,17 @@ __device__ __forceinline__ void stockham_pass(C (&v)[FftGeom<LOG2L>::EPT], C* sm
         for (int j = 0; j < R; ++j) u[j] = v[b + B * j];
         const int i = tid + G::NT * b;
         const int k = i & (p - 1);
-        if constexpr (p > 1) {
+        if constexpr (TMT && last && B == 1 && R == 16) {
+            constexpr int K4 = 16 / CxWords<C>::W;
+#pragma unroll
+            for (int c = 0; c < 16 / K4; ++c) {
+                C w[K4];
+                tmem_get<C, K4>(tmt + c * 16, w);
+#pragma unroll
+                for (int i = 0; i < K4; ++i)
+                    if (c * K4 + i >= 1) u[c * K4 + i] = twmul<INV>(u[c * K4 + i], w[i]);
+            }
+        } else if constexpr (p > 1) {
             // W^{jk} for j = 1 (and 2, 4, 8 in fp32) from the per-digit tables
             auto wj = [&](int jj) {
                 C w = tw[G::tw_off(S, 0) + jj * 16 + (k & 15)];
@@ -398,19 +413,20 @@ __device__ __forceinline__ void stockham_pass(C (&v)[FftGeom<LOG2L>::EPT], C* sm
 
 // Full transform: NZ = leading nonzero inputs of the first radix-16 pass (1..16),
 // NO = leading outputs needed from the last radix-16 pass (4, 8 or 16).
-template <bool INV, int LOG2L, int NZ = 16, int NO = 16, typename C, typename SYNC = CtaSync>
+// TMT: last-pass twiddles from TMEM at lane address `tmt` (see stockham_pass)
+template <bool INV, int LOG2L, int NZ = 16, int NO = 16, typename C, typename SYNC = CtaSync, bool TMT = false>
 __device__ __forceinline__ void block_fft(C (&v)[FftGeom<LOG2L>::EPT], C* sm, const C* __restrict__ tw, int tid,
-                                          bool active = true, SYNC sync = SYNC()) {
+                                          bool active = true, SYNC sync = SYNC(), uint32_t tmt = 0) {
     using G = FftGeom<LOG2L>;
     if constexpr (G::L < 16) {
         dft_r<G::L, INV, 16, 16>(v);
     } else {
         constexpr int nz = G::radix(0) == 16 ? NZ : 16;
         constexpr int no = G::radix(G::P - 1) == 16 ? NO : 16;
-        stockham_pass<INV, 0, nz, (G::P == 1 ? no : 16), LOG2L, C, SYNC>(v, sm, tw, tid, active, sync);
-        if constexpr (G::P > 1) stockham_pass<INV, 1, 16, (G::P == 2 ? no : 16), LOG2L, C, SYNC>(v, sm, tw, tid, active, sync);
-        if constexpr (G::P > 2) stockham_pass<INV, 2, 16, (G::P == 3 ? no : 16), LOG2L, C, SYNC>(v, sm, tw, tid, active, sync);
-        if constexpr (G::P > 3) stockham_pass<INV, 3, 16, (G::P == 4 ? no : 16), LOG2L, C, SYNC>(v, sm, tw, tid, active, sync);
+        stockham_pass<INV, 0, nz, (G::P == 1 ? no : 16), LOG2L, C, SYNC, TMT && G::P == 1>(v, sm, tw, tid, active, sync, tmt);
+        if constexpr (G::P > 1) stockham_pass<INV, 1, 16, (G::P == 2 ? no : 16), LOG2L, C, SYNC, TMT && G::P == 2>(v, sm, tw, tid, active, sync, tmt);
+        if constexpr (G::P > 2) stockham_pass<INV, 2, 16, (G::P == 3 ? no : 16), LOG2L, C, SYNC, TMT && G::P == 3>(v, sm, tw, tid, active, sync, tmt);
+        if constexpr (G::P > 3) stockham_pass<INV, 3, 16, (G::P == 4 ? no : 16), LOG2L, C, SYNC, TMT && G::P == 4>(v, sm, tw, tid, active, sync, tmt);
         static_assert(G::P <= 4, "single-CTA engine handles L <= 65536");
     }
 }

@@ -219,6 +219,20 @@ const void* cached(int kind, int a, int b, bool f32, const std::function<std::ve
 
 int single_cta_max_log2(bool f32) { return f32 ? kMaxLog2F32 : kMaxLog2F64; }
 
+// W_L^{j k}, k < L/16, j < 16 (row k): the last radix-16 Stockham pass's twiddles per butterfly,
+// with the reference's phase reduction (numerics.cpp:122-128); read once per CTA into TMEM
+const void* last_pass_twiddles(int log2L, bool f32) {
+    require_device();
+    return cached(5, log2L, 0, f32, [&] {
+        const size_t L = size_t{1} << log2L, P = L / 16;
+        std::vector<cd> v(L);
+        const double q = -1.0 / static_cast<double>(L);
+        for (size_t k = 0; k < P; ++k)
+            for (size_t j = 0; j < 16; ++j) v[k * 16 + j] = cis_cycles(q, static_cast<double>(j * k));
+        return v;
+    });
+}
+
 namespace {
 // W_L^{r k2}, r < 8, k2 < L/8: the cluster FFT's inter-CTA twiddles (fp64 phase reduction)
 const void* cluster_twiddles(int log2L, bool f32) {
@@ -562,10 +576,10 @@ void CztPlanG::execute(const void* x, bool complex_in, long long x_stride, long 
         void* yw = stream_alloc((size_t)slots * Ls_ * (f32 ? 8 : 16), st);
         e = f32 ? launch_czt_sf<float>(log2L_, N, (long long)m_, complex_in, x, x_stride, batch, (int)nseg_,
                                        (long long)seg_, out, out_stride, tw, d.cin.p, d.khat_sf.p, d.cout_sf.p, yw,
-                                       slots, st)
+                                       slots, last_pass_twiddles(log2L_, f32), st)
                 : launch_czt_sf<double>(log2L_, N, (long long)m_, complex_in, x, x_stride, batch, (int)nseg_,
                                         (long long)seg_, out, out_stride, tw, d.cin.p, d.khat_sf.p, d.cout_sf.p, yw,
-                                        slots, st);
+                                        slots, last_pass_twiddles(log2L_, f32), st);
         cudaFreeAsync(yw, st);
         if (e != cudaErrorNotSupported) {
             check(e, "czt launch");

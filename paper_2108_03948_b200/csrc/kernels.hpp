@@ -50,11 +50,13 @@ cudaError_t launch_czt(int log2L, long long N, long long M, bool complex_in, con
 // cout = nseg x seg_len output chirps W^{(s seg + k)^2/2}. cudaErrorNotSupported when the
 // geometry has no instantiation or the per-CTA shared memory does not fit (caller falls back).
 // ywork (optional): ywork_slots x L complex scratch that lets more transform groups share an SM.
+// twl (optional): (L/16) x 16 table W_L^{j k}, the last radix-16 pass's twiddles, which the TMEM
+// variant keeps per thread (kernels_czt_tm.cuh).
 template <typename T>
 cudaError_t launch_czt_sf(int log2L, long long N, long long M, bool complex_in, const void* x, long long x_stride,
                           long long batch, int nseg, long long seg_len, void* out, long long out_stride,
                           const void* tw, const void* cin, const void* khat, const void* cout, void* ywork,
-                          long long ywork_slots, cudaStream_t st);
+                          long long ywork_slots, const void* twl, cudaStream_t st);
 
 // ---- four-step passes for L = R * C beyond one CTA (kernels_4step.cuh) ----------------------
 // in_kind: 0 complex x, 1 real x, 2 real x * chirp, 3 complex x * chirp, 4 work buffer Y

@@ -15,9 +15,11 @@
 // thread t sees the same lane, so the trace-independent tables are stored once per CTA):
 //   [0, KH)            K̂_s[t + NT q], s < nseg, q < EPT        (nseg * EPT * W columns)
 //   [KH, KH + CO)      cout_s[t + NT q], q < NO (zero past m)   (nseg * NOC * W)
-//   [.., + CI)         cin[t + NT q], q < NXC (zero past N)     (NXC * W)
+//   TWT: [.., + 16 W)  the last pass's twiddles W_L^{j t}, j < 16 (cin is read through L1)
+//   else [.., + CI)    cin[t + NT q], q < NXC (zero past N)     (NXC * W; twiddles formed by products)
 //   [.., + Y)          Y of group g, g < RG                      (RG * EPT * W)
 // W = 32-bit words per complex (4 fp64, 2 fp32); NOC / NXC round NO / NX up to whole 16-word chunks.
+// fp64 configs[1] (nseg 2, NO 8): 128 + 64 + 64 + 256 = 512 columns with TWT.
 #pragma once
 
 #include "fft_device.cuh"
@@ -25,7 +27,7 @@
 
 namespace skg {
 
-template <typename T, int LOG2L, int NZ, int NO, int RG> struct TmCfg {
+template <typename T, int LOG2L, int NZ, int NO, int RG, bool TWT> struct TmCfg {
     using C = cx_t<T>;
     using G = FftGeom<LOG2L>;
     static constexpr int W = CxWords<C>::W;
@@ -36,19 +38,21 @@ template <typename T, int LOG2L, int NZ, int NO, int RG> struct TmCfg {
     static constexpr int BLOCK = G::NT * RG;
     __host__ __device__ static constexpr int col_co(int nseg) { return nseg * G::EPT * W; }
     __host__ __device__ static constexpr int col_ci(int nseg) { return col_co(nseg) + nseg * NOC * W; }
-    __host__ __device__ static constexpr int col_y(int nseg) { return col_ci(nseg) + NXC * W; }
+    __host__ __device__ static constexpr int col_y(int nseg) { return col_ci(nseg) + (TWT ? 16 : NXC) * W; }
     __host__ __device__ static constexpr int cols(int nseg) { return col_y(nseg) + RG * G::EPT * W; }
     static constexpr size_t smem_bytes() { return ((size_t)RG * G::SMEM + G::TW_ALLOC) * sizeof(C) + 16; }
 };
 
-template <typename T, int LOG2L, int NZ, int NO, bool CPLX, int RG>
-__global__ void __launch_bounds__(TmCfg<T, LOG2L, NZ, NO, RG>::BLOCK, 1)
+template <typename T, int LOG2L, int NZ, int NO, bool CPLX, int RG, bool TWT>
+__global__ void __launch_bounds__(TmCfg<T, LOG2L, NZ, NO, RG, TWT>::BLOCK, 1)
 k_czt_tm(const void* __restrict__ xin, long long x_stride, long long N, long long M, long long batch, int nseg,
          long long seg_len, cx_t<T>* __restrict__ out, long long out_stride, const cx_t<T>* __restrict__ tw,
-         const cx_t<T>* __restrict__ cin, const cx_t<T>* __restrict__ khat, const cx_t<T>* __restrict__ cout) {
+         const cx_t<T>* __restrict__ cin, const cx_t<T>* __restrict__ khat, const cx_t<T>* __restrict__ cout,
+         const cx_t<T>* __restrict__ twl) {
     using C = cx_t<T>;
     using G = FftGeom<LOG2L>;
-    using K = TmCfg<T, LOG2L, NZ, NO, RG>;
+    using K = TmCfg<T, LOG2L, NZ, NO, RG, TWT>;
+    static_assert(!TWT || (G::radix(G::P - 1) == 16 && G::NT == G::pval(G::P - 1)), "one last-pass butterfly per thread");
     static_assert(G::NT == 128, "TMEM lane = thread index within a 128-thread transform group");
     constexpr int K4 = K::K4, W = K::W, EPT = G::EPT;
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -59,6 +63,7 @@ k_czt_tm(const void* __restrict__ xin, long long x_stride, long long N, long lon
     uint32_t* tslot = reinterpret_cast<uint32_t*>(tws + G::TW_ALLOC);
     load_twiddles<LOG2L>(tws, tw);
     const uint32_t tb = tmem_alloc_cta<512>(tslot);   // includes the barrier that publishes the twiddles
+    const uint32_t tl = tmem_lane_addr(tb, 0);         // this thread's lane, column 0
     const uint32_t c_co = K::col_co(nseg), c_ci = K::col_ci(nseg), c_y = K::col_y(nseg) + gid * EPT * W;
     if (gid == 0) {   // group 0 writes the CTA's tables into lanes 0..127
         C t[K4];
@@ -67,7 +72,7 @@ k_czt_tm(const void* __restrict__ xin, long long x_stride, long long N, long lon
             for (int c = 0; c < EPT / K4; ++c) {
 #pragma unroll
                 for (int i = 0; i < K4; ++i) t[i] = __ldg(khat + (long long)s * G::L + tid + G::NT * (c * K4 + i));
-                tmem_put<C, K4>(tb, (s * EPT + c * K4) * W, t);
+                tmem_put<C, K4>(tl + (s * EPT + c * K4) * W, t);
             }
             const long long m_here = min(seg_len, M - s * seg_len);
 #pragma unroll
@@ -77,17 +82,26 @@ k_czt_tm(const void* __restrict__ xin, long long x_stride, long long N, long lon
                     const long long pos = tid + G::NT * (c * K4 + i);
                     t[i] = pos < m_here ? __ldg(cout + s * seg_len + pos) : czero<C>();
                 }
-                tmem_put<C, K4>(tb, c_co + (s * K::NOC + c * K4) * W, t);
+                tmem_put<C, K4>(tl + c_co + (s * K::NOC + c * K4) * W, t);
             }
         }
+        if constexpr (TWT) {
 #pragma unroll
-        for (int c = 0; c < K::NXC / K4; ++c) {
+            for (int c = 0; c < 16 / K4; ++c) {
 #pragma unroll
-            for (int i = 0; i < K4; ++i) {
-                const long long pos = tid + G::NT * (c * K4 + i);
-                t[i] = pos < N ? __ldg(cin + pos) : czero<C>();
+                for (int i = 0; i < K4; ++i) t[i] = __ldg(twl + tid * 16 + c * K4 + i);
+                tmem_put<C, K4>(tl + c_ci + c * K4 * W, t);
             }
-            tmem_put<C, K4>(tb, c_ci + c * K4 * W, t);
+        } else {
+#pragma unroll
+            for (int c = 0; c < K::NXC / K4; ++c) {
+#pragma unroll
+                for (int i = 0; i < K4; ++i) {
+                    const long long pos = tid + G::NT * (c * K4 + i);
+                    t[i] = pos < N ? __ldg(cin + pos) : czero<C>();
+                }
+                tmem_put<C, K4>(tl + c_ci + c * K4 * W, t);
+            }
         }
         tmem_wait_st();
     }
@@ -96,49 +110,63 @@ k_czt_tm(const void* __restrict__ xin, long long x_stride, long long N, long lon
     tmem_fence_after_sync();
     const GroupSync gsync{1 + gid, G::NT};
     using XT = typename std::conditional<CPLX, C, T>::type;
+    const int n32 = (int)N;   // N <= L and the segment bounds fit 32 bits (L = 2048)
     for (long long b = (long long)blockIdx.x * RG + gid; b < batch; b += (long long)gridDim.x * RG) {
+        const XT* xb = reinterpret_cast<const XT*>(xin) + b * x_stride;
         XT xr[K::NX];
 #pragma unroll
         for (int q = 0; q < K::NX; ++q) {
-            const long long pos = tid + (long long)G::NT * q;
+            const int pos = tid + G::NT * q;
             if constexpr (CPLX) xr[q] = czero<C>();
             else xr[q] = (T)0;
-            if (pos < N) xr[q] = __ldg(reinterpret_cast<const XT*>(xin) + b * x_stride + pos);
+            if (pos < n32) xr[q] = __ldg(xb + pos);
         }
-        {   // the group's next trace into L2
-            const long long bn = b + (long long)gridDim.x * RG;
-            if (bn < batch) {
+        if (b + (long long)gridDim.x * RG < batch) {   // the group's next trace into L2
+            const XT* xn = xb + (long long)gridDim.x * RG * x_stride;
 #pragma unroll
-                for (int q = 0; q < K::NX; ++q) {
-                    const long long pos = tid + (long long)G::NT * q;
-                    if (pos < N) prefetch_l2(reinterpret_cast<const XT*>(xin) + bn * x_stride + pos);
-                }
+            for (int q = 0; q < K::NX; ++q) {
+                const int pos = tid + G::NT * q;
+                if (pos < n32) prefetch_l2(xn + pos);
             }
         }
         C v[EPT];
 #pragma unroll
         for (int q = K::NX; q < EPT; ++q) v[q] = czero<C>();
+        if constexpr (TWT) {
 #pragma unroll
-        for (int c = 0; c < K::NXC / K4; ++c) {
-            C ch[K4];
-            tmem_get<C, K4>(tb, c_ci + c * K4 * W, ch);
+            for (int q = 0; q < K::NX; ++q) {
+                const int pos = tid + G::NT * q;
+                v[q] = czero<C>();
+                if (pos < n32) {
+                    const C ch = __ldg(cin + pos);
+                    if constexpr (CPLX) v[q] = cmul(xr[q], ch);
+                    else v[q] = rmul(xr[q], ch);
+                }
+            }
+        } else {
 #pragma unroll
-            for (int i = 0; i < K4; ++i) {
-                const int q = c * K4 + i;
-                if (q < K::NX) {   // cin is zero past N, so the padded samples stay zero
-                    if constexpr (CPLX) v[q] = cmul(xr[q], ch[i]);
-                    else v[q] = rmul(xr[q], ch[i]);
+            for (int c = 0; c < K::NXC / K4; ++c) {
+                C ch[K4];
+                tmem_get<C, K4>(tl + c_ci + c * K4 * W, ch);
+#pragma unroll
+                for (int i = 0; i < K4; ++i) {
+                    const int q = c * K4 + i;
+                    if (q < K::NX) {   // cin is zero past N, so the padded samples stay zero
+                        if constexpr (CPLX) v[q] = cmul(xr[q], ch[i]);
+                        else v[q] = rmul(xr[q], ch[i]);
+                    }
                 }
             }
         }
-        block_fft<false, LOG2L, NZ>(v, sm, tws, tid, true, gsync);
+        const uint32_t tmt = tl + c_ci;   // TWT: the last pass's twiddles
+        block_fft<false, LOG2L, NZ, 16, C, GroupSync, TWT>(v, sm, tws, tid, true, gsync, tmt);
         if (nseg > 1) {
 #pragma unroll
             for (int c = 0; c < EPT / K4; ++c) {
                 C t[K4];
 #pragma unroll
                 for (int i = 0; i < K4; ++i) t[i] = v[c * K4 + i];
-                tmem_put<C, K4>(tb, c_y + c * K4 * W, t);
+                tmem_put<C, K4>(tl + c_y + c * K4 * W, t);
             }
         }
         for (int sg = 0; sg < nseg; ++sg) {
@@ -147,7 +175,7 @@ k_czt_tm(const void* __restrict__ xin, long long x_stride, long long N, long lon
 #pragma unroll
                 for (int c = 0; c < EPT / K4; ++c) {
                     C t[K4];
-                    tmem_get<C, K4>(tb, c_y + c * K4 * W, t);
+                    tmem_get<C, K4>(tl + c_y + c * K4 * W, t);
 #pragma unroll
                     for (int i = 0; i < K4; ++i) v[c * K4 + i] = t[i];
                 }
@@ -155,21 +183,21 @@ k_czt_tm(const void* __restrict__ xin, long long x_stride, long long N, long lon
 #pragma unroll
             for (int c = 0; c < EPT / K4; ++c) {
                 C kh[K4];
-                tmem_get<C, K4>(tb, (sg * EPT + c * K4) * W, kh);
+                tmem_get<C, K4>(tl + (sg * EPT + c * K4) * W, kh);
 #pragma unroll
                 for (int i = 0; i < K4; ++i) v[c * K4 + i] = cmul(v[c * K4 + i], kh[i]);
             }
-            block_fft<true, LOG2L, 16, NO>(v, sm, tws, tid, true, gsync);
-            const long long m_here = min(seg_len, M - sg * seg_len);
+            block_fft<true, LOG2L, 16, NO, C, GroupSync, TWT>(v, sm, tws, tid, true, gsync, tmt);
+            const int m_here = (int)min(seg_len, M - sg * seg_len);
             C* o = out + b * out_stride + sg * seg_len;
 #pragma unroll
             for (int c = 0; c < K::NOC / K4; ++c) {
                 C co[K4];
-                tmem_get<C, K4>(tb, c_co + (sg * K::NOC + c * K4) * W, co);
+                tmem_get<C, K4>(tl + c_co + (sg * K::NOC + c * K4) * W, co);
 #pragma unroll
                 for (int i = 0; i < K4; ++i) {
                     const int q = c * K4 + i;
-                    const long long pos = tid + (long long)G::NT * q;
+                    const int pos = tid + G::NT * q;
                     if (q < NO && pos < m_here) o[pos] = cmul(v[q], co[i]);
                 }
             }

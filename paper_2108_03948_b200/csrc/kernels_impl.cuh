@@ -650,7 +650,8 @@ cudaError_t launch_fft_r2c_impl(int log2M, long long N, const T* x, long long x_
 template <typename T, int LOG2L, int NZ, int NO>
 cudaError_t run_czt_sf(long long N, long long M, bool complex_in, const void* x, long long x_stride, long long batch,
                        int nseg, long long seg_len, void* out, long long out_stride, const void* tw, const void* cin,
-                       const void* khat, const void* cout, void* ywork, long long ywork_slots, cudaStream_t st) {
+                       const void* khat, const void* cout, void* ywork, long long ywork_slots, const void* twl,
+                       cudaStream_t st) {
     using C = cx_t<T>;
     if constexpr (FftGeom<LOG2L>::NT < 32) {
         return cudaErrorNotSupported;
@@ -663,22 +664,33 @@ cudaError_t run_czt_sf(long long N, long long M, bool complex_in, const void* x,
         // tensor-memory variant first (kernels_czt_tm.cuh): 128-thread transforms (L = 2048) whose
         // tables + parked spectra fit the 512 TMEM columns; SKG_CZT_NO_TM=1 for the A/B
         static const bool no_tm = getenv("SKG_CZT_NO_TM") != nullptr;
+        static const int tm_rg = getenv("SKG_CZT_TM_RG") ? atoi(getenv("SKG_CZT_TM_RG")) : 0;
+        static const bool no_twt = getenv("SKG_CZT_NO_TWT") != nullptr;
+        auto go_tm = [&](auto rgc, auto twc) -> cudaError_t {
+            constexpr int RG = decltype(rgc)::value;
+            constexpr bool TWT = decltype(twc)::value != 0;
+            using TK = TmCfg<T, LOG2L, NZ, NO, RG, TWT>;
+            if (no_tm || want_rg || (tm_rg && tm_rg != RG) || (TWT && (no_twt || !twl)) || TK::cols(nseg) > 512 ||
+                TK::smem_bytes() > lim)
+                return cudaErrorNotSupported;
+            auto launch = [&](auto kern) {
+                cudaError_t e = prep_smem(kern, TK::smem_bytes());
+                if (e != cudaSuccess) return e;
+                const unsigned g = persistent_grid(kern, TK::BLOCK, TK::smem_bytes(), (batch + RG - 1) / RG);
+                kern<<<g, TK::BLOCK, TK::smem_bytes(), st>>>(x, x_stride, N, M, batch, nseg, seg_len, (C*)out,
+                                                             out_stride, (const C*)tw, (const C*)cin, (const C*)khat,
+                                                             (const C*)cout, (const C*)twl);
+                return cudaGetLastError();
+            };
+            return complex_in ? launch(k_czt_tm<T, LOG2L, NZ, NO, true, RG, TWT>)
+                              : launch(k_czt_tm<T, LOG2L, NZ, NO, false, RG, TWT>);
+        };
         if constexpr (FftGeom<LOG2L>::NT == 128) {
-            constexpr int RG = 4;
-            using TK = TmCfg<T, LOG2L, NZ, NO, RG>;
-            if (!no_tm && !want_rg && TK::cols(nseg) <= 512 && TK::smem_bytes() <= lim) {
-                auto launch = [&](auto kern) {
-                    cudaError_t e = prep_smem(kern, TK::smem_bytes());
-                    if (e != cudaSuccess) return e;
-                    const unsigned g = persistent_grid(kern, TK::BLOCK, TK::smem_bytes(), (batch + RG - 1) / RG);
-                    kern<<<g, TK::BLOCK, TK::smem_bytes(), st>>>(x, x_stride, N, M, batch, nseg, seg_len, (C*)out,
-                                                                 out_stride, (const C*)tw, (const C*)cin,
-                                                                 (const C*)khat, (const C*)cout);
-                    return cudaGetLastError();
-                };
-                return complex_in ? launch(k_czt_tm<T, LOG2L, NZ, NO, true, RG>)
-                                  : launch(k_czt_tm<T, LOG2L, NZ, NO, false, RG>);
-            }
+            cudaError_t e0;
+            // 4 groups measured best for both precisions (fp32 cfg2: 6 groups 0.137 ms, 8 groups 0.155 ms
+            // against 0.136 ms — fewer registers per thread spill)
+            if ((e0 = go_tm(IC<4>{}, IC<1>{})) != cudaErrorNotSupported) return e0;
+            if ((e0 = go_tm(IC<4>{}, IC<0>{})) != cudaErrorNotSupported) return e0;
         }
         auto go = [&](auto rgc, auto tsc) -> cudaError_t {
             constexpr int RG = decltype(rgc)::value, TS = decltype(tsc)::value;
@@ -716,7 +728,7 @@ template <typename T>
 cudaError_t launch_czt_sf_impl(int log2L, long long N, long long M, bool complex_in, const void* x, long long x_stride,
                                long long batch, int nseg, long long seg_len, void* out, long long out_stride,
                                const void* tw, const void* cin, const void* khat, const void* cout, void* ywork,
-                               long long ywork_slots, cudaStream_t st) {
+                               long long ywork_slots, const void* twl, cudaStream_t st) {
     if (log2L < 9 || log2L > 12) return cudaErrorNotSupported;   // instantiated for 512..4096
     return dispatch_log2<9, 12>(log2L, [&](auto lg) {
         constexpr int LG = decltype(lg)::value;
@@ -729,9 +741,9 @@ cudaError_t launch_czt_sf_impl(int log2L, long long N, long long M, bool complex
                 constexpr int NZ = decltype(z)::value;
                 if (no == 8)
                     return run_czt_sf<T, LG, NZ, 8>(N, M, complex_in, x, x_stride, batch, nseg, seg_len, out,
-                                                    out_stride, tw, cin, khat, cout, ywork, ywork_slots, st);
+                                                    out_stride, tw, cin, khat, cout, ywork, ywork_slots, twl, st);
                 return run_czt_sf<T, LG, NZ, 16>(N, M, complex_in, x, x_stride, batch, nseg, seg_len, out, out_stride,
-                                                 tw, cin, khat, cout, ywork, ywork_slots, st);
+                                                 tw, cin, khat, cout, ywork, ywork_slots, twl, st);
             });
         }
     });

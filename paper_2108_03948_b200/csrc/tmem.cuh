@@ -127,20 +127,20 @@ template <> struct CxWords<float2> {
     }
 };
 
-// K complex values (K * W == 16 words) starting at column `col` of this thread's lane
-template <typename C, int K> __device__ __forceinline__ void tmem_get(uint32_t base, uint32_t col, C (&v)[K]) {
+// K complex values (K * W == 16 words) at `lane_col` = this thread's lane address (tmem_lane_addr) + column
+template <typename C, int K> __device__ __forceinline__ void tmem_get(uint32_t lane_col, C (&v)[K]) {
     static_assert(K * CxWords<C>::W == 16, "16-word chunk");
     uint32_t r[16];
-    tmem_ld16_wait(tmem_lane_addr(base, col), r);
+    tmem_ld16_wait(lane_col, r);
 #pragma unroll
     for (int i = 0; i < K; ++i) v[i] = CxWords<C>::get(r + i * CxWords<C>::W);
 }
-template <typename C, int K> __device__ __forceinline__ void tmem_put(uint32_t base, uint32_t col, const C (&v)[K]) {
+template <typename C, int K> __device__ __forceinline__ void tmem_put(uint32_t lane_col, const C (&v)[K]) {
     static_assert(K * CxWords<C>::W == 16, "16-word chunk");
     uint32_t r[16];
 #pragma unroll
     for (int i = 0; i < K; ++i) CxWords<C>::put(r + i * CxWords<C>::W, v[i]);
-    tmem_st16(tmem_lane_addr(base, col), r);
+    tmem_st16(lane_col, r);
 }
 
 }  // namespace skg
