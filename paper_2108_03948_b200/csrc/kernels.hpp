@@ -116,6 +116,12 @@ int zoom_pfir_lh(const ZoomArgs& a);
 cudaError_t launch_zoom_pfir(const ZoomArgs& a, bool f32, const void* x, long long xs, long long batch,
                              const void* gph, const void* gnat, const void* S, void* zb, long long z_stride,
                              cudaStream_t st);
+// the phase-lane FIR fed by a TMA pipeline of whole records (kernels_zoom_tfir.cu): circular,
+// untrimmed, power-of-two U, D in {4, 8, 16}, 16-byte aligned rows
+bool zoom_tfir_fits(const ZoomArgs& a, bool f32, const void* x, long long x_stride);
+cudaError_t launch_zoom_tfir(const ZoomArgs& a, bool f32, const void* x, long long xs, long long batch,
+                             const void* gph, const void* gnat, const void* S, void* zb, long long z_stride,
+                             cudaStream_t st);
 // the phase-lane FIR and the short FFT + band gather in one kernel (kernels_zoom_fused.cu); returns
 // cudaErrorNotSupported outside its instantiated geometry (the caller then runs the split route)
 cudaError_t launch_zoom_pfir_fft(const ZoomArgs& a, int lh, int log2n, bool f32, const void* x, long long xs,

@@ -240,7 +240,8 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
         count_launch();
         return;
     }
-    if (single && pfir && !force && !split_only) {
+    const bool tfir = zoom_tfir_fits(a, f32, x, x_stride);
+    if (single && pfir && !tfir && !force && !split_only) {
         // FIR and short FFT in one kernel where instantiated (configs[2] geometry)
         const cudaError_t e = launch_zoom_pfir_fft(a, zoom_pfir_lh(a), lg, f32, x, x_stride, batch, d.g.p, d.gn.p,
                                                    d.sdec.p, stockham_twiddles(lg, f32), (int)k_lo, (int)bins(),
@@ -251,7 +252,7 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
             return;
         }
     }
-    if (single && (wfir || pfir || cfir) && !force) {
+    if (single && (tfir || wfir || pfir || cfir) && !force) {
         // warp-chunk FIR -> work rows (L2-resident chunk of records) -> FFT + band gather
         const size_t cs = f32 ? 8 : 16, es = f32 ? 4 : 8;
         const long long zrow = a.nout;
@@ -266,7 +267,9 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
             // phase-lane FIR where it exists (power-of-two D <= 16), else the constant-bank FIR for the
             // specialised (D, T) pairs, else the warp-window FIR (all three measured within a few
             // percent of each other on cfg3)
-            if (pfir)
+            if (tfir)
+                check(launch_zoom_tfir(a, f32, xb, x_stride, nb, d.g.p, d.gn.p, d.sdec.p, zb, zrow, st), "zoom fir");
+            else if (pfir)
                 check(launch_zoom_pfir(a, f32, xb, x_stride, nb, d.g.p, d.gn.p, d.sdec.p, zb, zrow, st), "zoom fir");
             else if (cfir)
                 check(launch_zoom_cfir(a, f32, xb, x_stride, nb, d.gh.data(), d.gn.p, d.sdec.p, zb, zrow, st),
