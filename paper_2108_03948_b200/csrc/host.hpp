@@ -209,6 +209,7 @@ class ZoomPlanG {                     // ZoomFftPlan + make_zoom_plan, zoomfft.h
         DevMem g, gn, sdec, wrap, band;
         DevMem shift, hf;     // frequency-domain route: e^{-i2pi fc n/fs} (n < U), DFT_U of the taps
         std::vector<cd> gh;   // host copy of g (phase rows, fp64) for the constant-bank FIR
+        std::vector<cd> gnh;  // host copy of g in natural order (fp64) for the whole-output FIR
     };
     const Dev& dev(bool f32) const;
     void compute_band();

@@ -122,6 +122,12 @@ bool zoom_tfir_fits(const ZoomArgs& a, bool f32, const void* x, long long x_stri
 cudaError_t launch_zoom_tfir(const ZoomArgs& a, bool f32, const void* x, long long xs, long long batch,
                              const void* gph, const void* gnat, const void* S, void* zb, long long z_stride,
                              cudaStream_t st);
+// whole-output FIR with constant-bank taps and cp.async-filled polyphase rows (kernels_zoom_pcfir.cu):
+// circular, untrimmed, nout a multiple of 256, (D, T) in {(8, 65), (8, 101)}; gnat_host = the plan's
+// natural-order taps as interleaved fp64 complex
+bool zoom_pcfir_fits(const ZoomArgs& a, bool f32);
+cudaError_t launch_zoom_pcfir(const ZoomArgs& a, bool f32, const void* x, long long xs, long long batch,
+                              const void* gnat_host, const void* S, void* zb, long long z_stride, cudaStream_t st);
 // the phase-lane FIR and the short FFT + band gather in one kernel (kernels_zoom_fused.cu); returns
 // cudaErrorNotSupported outside its instantiated geometry (the caller then runs the split route)
 cudaError_t launch_zoom_pfir_fft(const ZoomArgs& a, int lh, int log2n, bool f32, const void* x, long long xs,

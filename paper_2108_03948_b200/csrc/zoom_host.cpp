@@ -174,6 +174,7 @@ const ZoomPlanG::Dev& ZoomPlanG::dev(bool f32) const {
         std::vector<cd> gn(static_cast<size_t>(std::max(T, 1)), cd(0.0, 0.0));   // natural order (wrap terms)
         for (int t = 0; t < T; ++t) gn[static_cast<size_t>(t)] = filter_taps[t] * cis_cycles(-qc, static_cast<double>(t));
         d.gn = to_device(gn, f32);
+        d.gnh = gn;
         // S[m] = e^{i 2pi qc (m + trim) D} (the shift table sampled at the decimation points)
         std::vector<cd> S(decimated_len);
         for (size_t m = 0; m < decimated_len; ++m)
@@ -240,8 +241,9 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
         count_launch();
         return;
     }
-    const bool tfir = zoom_tfir_fits(a, f32, x, x_stride);
-    if (single && pfir && !tfir && !force && !split_only) {
+    const bool pcfir = zoom_pcfir_fits(a, f32);
+    const bool tfir = !pcfir && zoom_tfir_fits(a, f32, x, x_stride);
+    if (single && pfir && !tfir && !pcfir && !force && !split_only) {
         // FIR and short FFT in one kernel where instantiated (configs[2] geometry)
         const cudaError_t e = launch_zoom_pfir_fft(a, zoom_pfir_lh(a), lg, f32, x, x_stride, batch, d.g.p, d.gn.p,
                                                    d.sdec.p, stockham_twiddles(lg, f32), (int)k_lo, (int)bins(),
@@ -252,7 +254,7 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
             return;
         }
     }
-    if (single && (tfir || wfir || pfir || cfir) && !force) {
+    if (single && (pcfir || tfir || wfir || pfir || cfir) && !force) {
         // warp-chunk FIR -> work rows (L2-resident chunk of records) -> FFT + band gather
         const size_t cs = f32 ? 8 : 16, es = f32 ? 4 : 8;
         const long long zrow = a.nout;
@@ -267,7 +269,9 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
             // phase-lane FIR where it exists (power-of-two D <= 16), else the constant-bank FIR for the
             // specialised (D, T) pairs, else the warp-window FIR (all three measured within a few
             // percent of each other on cfg3)
-            if (tfir)
+            if (pcfir)
+                check(launch_zoom_pcfir(a, f32, xb, x_stride, nb, d.gnh.data(), d.sdec.p, zb, zrow, st), "zoom fir");
+            else if (tfir)
                 check(launch_zoom_tfir(a, f32, xb, x_stride, nb, d.g.p, d.gn.p, d.sdec.p, zb, zrow, st), "zoom fir");
             else if (pfir)
                 check(launch_zoom_pfir(a, f32, xb, x_stride, nb, d.g.p, d.gn.p, d.sdec.p, zb, zrow, st), "zoom fir");
