@@ -125,9 +125,13 @@ cudaError_t launch_zoom_tfir(const ZoomArgs& a, bool f32, const void* x, long lo
 // whole-output FIR with constant-bank taps and cp.async-filled polyphase rows (kernels_zoom_pcfir.cu):
 // circular, untrimmed, nout a multiple of 256, (D, T) in {(8, 65), (8, 101)}; gnat_host = the plan's
 // natural-order taps as interleaved fp64 complex
+// fuse: the n_fft = 512 transform + band gather in the same launch (zoom_pcfir_fused_fits), output
+// straight to out; else the decimated rows to zb
 bool zoom_pcfir_fits(const ZoomArgs& a, bool f32);
+bool zoom_pcfir_fused_fits(const ZoomArgs& a, bool f32, int log2n);
 cudaError_t launch_zoom_pcfir(const ZoomArgs& a, bool f32, const void* x, long long xs, long long batch,
-                              const void* gnat_host, const void* S, void* zb, long long z_stride, cudaStream_t st);
+                              const void* gnat_host, const void* S, void* zb, long long z_stride, bool fuse,
+                              const void* tw, const void* band, void* out, long long out_stride, cudaStream_t st);
 // the phase-lane FIR and the short FFT + band gather in one kernel (kernels_zoom_fused.cu); returns
 // cudaErrorNotSupported outside its instantiated geometry (the caller then runs the split route)
 cudaError_t launch_zoom_pfir_fft(const ZoomArgs& a, int lh, int log2n, bool f32, const void* x, long long xs,

@@ -48,14 +48,28 @@ template <typename T> struct PcGeom {
 
 // buffers per warp: fp32 double-buffers its parts; fp64 parts are twice the size, so a warp fills
 // its one buffer and waits, and the other warps of the SM filter meanwhile (8 warps either way)
-template <typename T> __host__ __device__ constexpr int pc_nbuf() { return sizeof(T) == 8 ? 1 : 2; }
-constexpr int PC_WARPS = 8;
+#ifndef SKG_PC_F32_WARPS
+#define SKG_PC_F32_WARPS 12
+#endif
+#ifndef SKG_PC_F32_NBUF
+#define SKG_PC_F32_NBUF 1
+#endif
+template <typename T> __host__ __device__ constexpr int pc_nbuf() { return sizeof(T) == 8 ? 1 : SKG_PC_F32_NBUF; }
+template <typename T> __host__ __device__ constexpr int pc_warps() { return sizeof(T) == 8 ? 8 : SKG_PC_F32_WARPS; }
 
-template <typename T, int D, int NTAPS>
-__global__ void __launch_bounds__(PC_WARPS * 32, 1)
+struct WarpSync {
+    __device__ __forceinline__ void operator()() const { __syncwarp(); }
+};
+
+// FUSE: the warp also runs the record's 512-point transform (nout = 2 parts = n_fft) and the signed
+// band gather x band factor straight from the part buffer it has just consumed — one launch per
+// batch, no work rows (else the decimated rows go to zb for k_zoom_fftband)
+template <typename T, int D, int NTAPS, bool FUSE>
+__global__ void __launch_bounds__(pc_warps<T>() * 32, 1)
 k_zoom_pcfir(const T* __restrict__ x, long long x_stride, long long batch, ZoomArgs a,
              const __grid_constant__ PcTaps<T, NTAPS> tp, const cx_t<T>* __restrict__ S, cx_t<T>* __restrict__ zb,
-             long long z_stride) {
+             long long z_stride, const cx_t<T>* __restrict__ tw, const cx_t<T>* __restrict__ band,
+             cx_t<T>* __restrict__ out, long long out_stride) {
     using C = cx_t<T>;
     using PG = PcGeom<T>;
     constexpr int LH = (NTAPS + D - 1) / D;                        // taps per phase row
@@ -80,17 +94,21 @@ k_zoom_pcfir(const T* __restrict__ x, long long x_stride, long long batch, ZoomA
     // part buffers 16-byte aligned (window loads are LDS.128)
     const size_t boff = ((size_t)(a.nout + NTAPS) * sizeof(C) + (size_t)nw * NBUF * WTP * sizeof(T) + 15) / 16 * 16;
     T* bufs = reinterpret_cast<T*>(smraw + boff) + (size_t)warp * NBUF * BUF;
+    C* tws = reinterpret_cast<C*>(smraw + boff + (size_t)nw * NBUF * BUF * sizeof(T));   // FUSE: n_fft twiddles
     for (int i = threadIdx.x; i < a.nout; i += blockDim.x) s_S[i] = __ldg(S + i);
     for (int i = threadIdx.x; i < NTAPS; i += blockDim.x) s_g[i] = tp.g[i];
+    if constexpr (FUSE) load_twiddles<9>(tws, tw);
     __syncthreads();
-    const long long ntask = batch * parts;
-    const long long tstride = (long long)gridDim.x * nw;
+    // this warp's records b0 + k rstride, all parts in order: item i = (record k = i / parts, part i % parts)
+    const long long b0 = (long long)blockIdx.x * nw + warp, rstride = (long long)gridDim.x * nw;
+    const long long nrec = b0 < batch ? (batch - 1 - b0) / rstride + 1 : 0;
+    const long long nitem = nrec * parts;
     // copy geometry of this lane: phase ph, row-in-copy lq; destination base in a part buffer
     const int cph = lane % D, clq = lane / D;
     const int cdst = cph * PG::PSE + clq;
-    auto fill = [&](long long task, int slot) {
-        const long long b = task / parts;
-        const int p = (int)(task % parts);
+    auto fill = [&](long long item, int slot) {
+        const long long b = b0 + (item / parts) * rstride;
+        const int p = (int)(item % parts);
         const int r0 = p * PC_PART - PC_PRE;   // first row copied
         const T* src = x + b * x_stride + (long long)r0 * D + lane;
         T* dst = bufs + slot * BUF + cdst;
@@ -117,22 +135,22 @@ k_zoom_pcfir(const T* __restrict__ x, long long x_stride, long long batch, ZoomA
         }
         cp_async_commit();
     };
-    long long task = (long long)blockIdx.x * nw + warp;
-    if (NBUF == 2 && task < ntask) fill(task, 0);
-    for (int k = 0; task < ntask; task += tstride, ++k) {
-        const int slot = NBUF == 2 ? (k & 1) : 0;
+    if (NBUF == 2 && nitem > 0) fill(0, 0);
+    C keep[PC_K];   // FUSE: part 0's outputs while part 1 is filtered
+    for (long long item = 0; item < nitem; ++item) {
+        const int slot = NBUF == 2 ? (int)(item & 1) : 0;
         if (NBUF == 1) {
-            fill(task, 0);
+            fill(item, 0);
             cp_async_wait_all();
-        } else if (task + tstride < ntask) {
-            fill(task + tstride, slot ^ 1);
+        } else if (item + 1 < nitem) {
+            fill(item + 1, slot ^ 1);
             asm volatile("cp.async.wait_group 1;" ::: "memory");
         } else {
             cp_async_wait_all();
         }
         __syncwarp();
-        const long long b = task / parts;
-        const int p = (int)(task % parts);
+        const long long b = b0 + (item / parts) * rstride;
+        const int p = (int)(item % parts);
         const T* xb = bufs + slot * BUF;
         // this lane's outputs m = p * 256 + 8 lane + c; window of phase ph = part rows
         // [8 lane + PRE - WB, 8 lane + PRE + K): block `lane`, offset PRE - WB, then compile-time
@@ -207,23 +225,59 @@ k_zoom_pcfir(const T* __restrict__ x, long long x_stride, long long batch, ZoomA
                 }
             }
         }
-        C* zr = zb + b * z_stride + mb;
 #pragma unroll
-        for (int c = 0; c < PC_K; ++c) zr[c] = cmul(acc[c], s_S[mb + c]);
-        __syncwarp();   // the buffer is refilled by a later task
+        for (int c = 0; c < PC_K; ++c) acc[c] = cmul(acc[c], s_S[mb + c]);
+        if constexpr (!FUSE) {
+            C* zr = zb + b * z_stride + mb;
+#pragma unroll
+            for (int c = 0; c < PC_K; ++c) zr[c] = acc[c];
+        } else if (p == 0) {
+#pragma unroll
+            for (int c = 0; c < PC_K; ++c) keep[c] = acc[c];
+        } else {
+            // the whole decimated record is in registers (keep: part 0, acc: part 1): through the part
+            // buffer it was filtered from (now dead) into natural order, the 512-point transform by this
+            // warp (32 threads x 16), then the signed band bins x the band factor (zoomfft.cpp:208-235)
+            using G = FftGeom<9>;
+            C* fsm = reinterpret_cast<C*>(bufs + slot * BUF);
+            __syncwarp();
+#pragma unroll
+            for (int c = 0; c < PC_K; ++c) {
+                fsm[pad16(lane * PC_K + c)] = keep[c];
+                fsm[pad16(PC_PART + lane * PC_K + c)] = acc[c];
+            }
+            __syncwarp();
+            C v[G::EPT];
+#pragma unroll
+            for (int q = 0; q < G::EPT; ++q) v[q] = fsm[pad16(lane + G::NT * q)];
+            __syncwarp();
+            block_fft<false, 9, 16, 16, C, WarpSync>(v, fsm, tws, lane, true, WarpSync{});
+#pragma unroll
+            for (int q = 0; q < G::EPT; ++q) fsm[pad16(lane + G::NT * q)] = v[q];
+            __syncwarp();
+            C* o = out + b * out_stride;
+            for (int i = lane; i < a.nbins; i += 32) {
+                const int kb = a.k_lo + i;
+                const int idx = ((kb % G::L) + G::L) % G::L;
+                o[i] = cmul(fsm[pad16(idx)], __ldg(band + i));
+            }
+        }
+        __syncwarp();   // the buffer is refilled by a later item
     }
 }
 
 template <typename T, int D, int NTAPS>
-size_t pc_smem(const ZoomArgs& a, int nw) {
+size_t pc_smem(const ZoomArgs& a, int nw, bool fuse) {
     constexpr int WTP = (NTAPS - 1 + 3) / 4 * 4;
     return ((size_t)(a.nout + NTAPS) * sizeof(cx_t<T>) + (size_t)nw * pc_nbuf<T>() * WTP * sizeof(T) + 15) / 16 * 16 +
-           (size_t)nw * pc_nbuf<T>() * D * PcGeom<T>::PSE * sizeof(T);
+           (size_t)nw * pc_nbuf<T>() * D * PcGeom<T>::PSE * sizeof(T) +
+           (fuse ? (size_t)FftGeom<9>::TW_ALLOC * sizeof(cx_t<T>) : 0);
 }
 
 template <typename T, int D, int NTAPS>
 cudaError_t run_pcfir(const ZoomArgs& a, const T* x, long long xs, long long batch, const void* gnat_host,
-                      const void* S, void* zb, long long z_stride, cudaStream_t st) {
+                      const void* S, void* zb, long long z_stride, bool fuse, const void* tw, const void* band,
+                      void* out, long long out_stride, cudaStream_t st) {
     using C = cx_t<T>;
     PcTaps<T, NTAPS> tp;
     const double* gh = static_cast<const double*>(gnat_host);   // fp64 natural-order taps
@@ -231,21 +285,23 @@ cudaError_t run_pcfir(const ZoomArgs& a, const T* x, long long xs, long long bat
         tp.g[t].x = (T)gh[2 * t];
         tp.g[t].y = (T)gh[2 * t + 1];
     }
-    const int nw = PC_WARPS;
-    const size_t smem = pc_smem<T, D, NTAPS>(a, nw);
+    const int nw = pc_warps<T>();
+    const size_t smem = pc_smem<T, D, NTAPS>(a, nw, fuse);
     int dev = 0, optin = 0, sms = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (smem > (size_t)optin) return cudaErrorNotSupported;
-    auto kern = k_zoom_pcfir<T, D, NTAPS>;
-    cudaError_t e = prep_smem(kern, smem);
-    if (e != cudaSuccess) return e;
-    const long long tasks = batch * (a.nout / PC_PART);
-    long long grid = std::min<long long>((tasks + nw - 1) / nw, sms);
-    if (const unsigned gc = grid_cap(); gc && gc < grid) grid = gc;
-    kern<<<(unsigned)grid, nw * 32, smem, st>>>(x, xs, batch, a, tp, (const C*)S, (C*)zb, z_stride);
-    return cudaGetLastError();
+    auto launch = [&](auto kern) -> cudaError_t {
+        cudaError_t e = prep_smem(kern, smem);
+        if (e != cudaSuccess) return e;
+        long long grid = std::min<long long>((batch + nw - 1) / nw, sms);
+        if (const unsigned gc = grid_cap(); gc && gc < grid) grid = gc;
+        kern<<<(unsigned)grid, nw * 32, smem, st>>>(x, xs, batch, a, tp, (const C*)S, (C*)zb, z_stride, (const C*)tw,
+                                                     (const C*)band, (C*)out, out_stride);
+        return cudaGetLastError();
+    };
+    return fuse ? launch(k_zoom_pcfir<T, D, NTAPS, true>) : launch(k_zoom_pcfir<T, D, NTAPS, false>);
 }
 
 }  // namespace
@@ -261,14 +317,24 @@ bool zoom_pcfir_fits(const ZoomArgs& a, bool f32) {
     }
 }
 
+// the FIR and the n_fft = 512 transform + band in one launch: nout = 512 (two parts)
+bool zoom_pcfir_fused_fits(const ZoomArgs& a, bool f32, int log2n) {
+    static const bool off = std::getenv("SKG_ZOOM_NO_FUSE") != nullptr;
+    return !off && log2n == 9 && a.nout == 2 * PC_PART && zoom_pcfir_fits(a, f32);
+}
+
 cudaError_t launch_zoom_pcfir(const ZoomArgs& a, bool f32, const void* x, long long xs, long long batch,
-                              const void* gnat_host, const void* S, void* zb, long long z_stride, cudaStream_t st) {
+                              const void* gnat_host, const void* S, void* zb, long long z_stride, bool fuse,
+                              const void* tw, const void* band, void* out, long long out_stride, cudaStream_t st) {
     auto go = [&](auto tag) -> cudaError_t {
         using T = decltype(tag);
         const T* xt = static_cast<const T*>(x);
         switch (a.D * 1000 + a.T) {
-            case 8065: return run_pcfir<T, 8, 65>(a, xt, xs, batch, gnat_host, S, zb, z_stride, st);
-            case 8101: return run_pcfir<T, 8, 101>(a, xt, xs, batch, gnat_host, S, zb, z_stride, st);
+            case 8065:
+                return run_pcfir<T, 8, 65>(a, xt, xs, batch, gnat_host, S, zb, z_stride, fuse, tw, band, out, out_stride, st);
+            case 8101:
+                return run_pcfir<T, 8, 101>(a, xt, xs, batch, gnat_host, S, zb, z_stride, fuse, tw, band, out, out_stride,
+                                            st);
             default: return cudaErrorNotSupported;
         }
     };

@@ -241,8 +241,18 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
         count_launch();
         return;
     }
-    const bool pcfir = zoom_pcfir_fits(a, f32);
-    const bool tfir = !pcfir && zoom_tfir_fits(a, f32, x, x_stride);
+    // split route FIR: the TMA-fed phase-lane FIR where it fits (fp64 cfg3 n_fft 2048: 0.111 ms against
+    // 0.120 for the whole-output FIR + separate transform), else the whole-output FIR
+    const bool tfir = zoom_tfir_fits(a, f32, x, x_stride);
+    const bool pcfir = !tfir && zoom_pcfir_fits(a, f32);
+    if (!force && !split_only && zoom_pcfir_fused_fits(a, f32, lg)) {
+        // whole-output FIR + 512-point transform + band in one launch (kernels_zoom_pcfir.cu)
+        check(launch_zoom_pcfir(a, f32, x, x_stride, batch, d.gnh.data(), d.sdec.p, nullptr, 0, true,
+                                stockham_twiddles(lg, f32), d.band.p, out, out_stride, st),
+              "zoom fir+fft");
+        count_launch();
+        return;
+    }
     if (single && pfir && !tfir && !pcfir && !force && !split_only) {
         // FIR and short FFT in one kernel where instantiated (configs[2] geometry)
         const cudaError_t e = launch_zoom_pfir_fft(a, zoom_pfir_lh(a), lg, f32, x, x_stride, batch, d.g.p, d.gn.p,
@@ -270,7 +280,9 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
             // specialised (D, T) pairs, else the warp-window FIR (all three measured within a few
             // percent of each other on cfg3)
             if (pcfir)
-                check(launch_zoom_pcfir(a, f32, xb, x_stride, nb, d.gnh.data(), d.sdec.p, zb, zrow, st), "zoom fir");
+                check(launch_zoom_pcfir(a, f32, xb, x_stride, nb, d.gnh.data(), d.sdec.p, zb, zrow, false, nullptr,
+                                        nullptr, nullptr, 0, st),
+                      "zoom fir");
             else if (tfir)
                 check(launch_zoom_tfir(a, f32, xb, x_stride, nb, d.g.p, d.gn.p, d.sdec.p, zb, zrow, st), "zoom fir");
             else if (pfir)
