@@ -139,7 +139,7 @@ struct Stage {
     cudaStream_t st = cs.stream();
     Ptr in, out;
     void put(const void* h, size_t bytes) { in.p = cs.up(h, bytes); }
-    void alloc_out(size_t bytes) { out.p = cs.scratch(bytes); }
+    void alloc_out(size_t bytes) { out.p = cs.out(bytes); }
     void get(void* h, size_t bytes) { cs.down(h, out.p, bytes); }
 };
 

@@ -375,11 +375,17 @@ __device__ __forceinline__ void stockham_pass(C (&v)[FftGeom<LOG2L>::EPT], C* sm
                     if (c * K4 + i >= 1) u[c * K4 + i] = twmul<INV>(u[c * K4 + i], w[i]);
             }
         } else if constexpr (p > 1) {
-            // W^{jk} for j = 1 (and 2, 4, 8 in fp32) from the per-digit tables
+            // W^{jk} for j = 1 (and 2, 4, 8 in fp32) from the per-digit tables. The table geometry is
+            // forced to compile time: ptxas once kept a CALL to the (recursive) digit count in the
+            // pass loop.
+            constexpr int ND = G::digits(S);
+            constexpr int TO0 = G::tw_off(S, 0), TO1 = G::tw_off(S, 1), TO2 = G::tw_off(S, 2), TO3 = G::tw_off(S, 3);
+            static_assert(ND <= 4, "digits");
             auto wj = [&](int jj) {
-                C w = tw[G::tw_off(S, 0) + jj * 16 + (k & 15)];
-#pragma unroll
-                for (int d = 1; d < G::digits(S); ++d) w = cmul(w, tw[G::tw_off(S, d) + jj * 16 + ((k >> (4 * d)) & 15)]);
+                C w = tw[TO0 + jj * 16 + (k & 15)];
+                if constexpr (ND > 1) w = cmul(w, tw[TO1 + jj * 16 + ((k >> 4) & 15)]);
+                if constexpr (ND > 2) w = cmul(w, tw[TO2 + jj * 16 + ((k >> 8) & 15)]);
+                if constexpr (ND > 3) w = cmul(w, tw[TO3 + jj * 16 + ((k >> 12) & 15)]);
                 return w;
             };
             if constexpr (sizeof(sc_t<C>) == 8) {

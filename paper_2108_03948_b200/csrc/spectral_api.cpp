@@ -73,7 +73,7 @@ ComplexBuffer dft_naive(std::span<const cplx> x) {
     skg::CallStage cs;
     void* dx = cs.up(x.data(), n * sizeof(cplx));
     void* dt = cs.up(tw.data(), n * sizeof(cplx));
-    void* dy = cs.scratch(n * sizeof(cplx));
+    void* dy = cs.out(n * sizeof(cplx));
     skg::check(skg::launch_dft_naive(dx, (long long)n, dt, dy, kStream), "dft_naive");
     skg::count_launch();
     ComplexBuffer y(n);
@@ -136,7 +136,7 @@ ComplexBuffer czt_direct(std::span<const cplx> x, const CztParams& p) {
     skg::CallStage cs;
     void* dx = cs.up(x.data(), n * sizeof(cplx));
     void* xa = cs.scratch(n * sizeof(cplx));
-    void* dy = cs.scratch(p.m * sizeof(cplx));
+    void* dy = cs.out(p.m * sizeof(cplx));
     skg::check(skg::launch_czt_direct(dx, (long long)n, A.log_mag, A.q, W.log_mag, W.q, (long long)p.m, xa,
                                       dy, kStream),
                "czt_direct");
@@ -161,7 +161,7 @@ void CztPlan::execute(std::span<const cplx> x, std::span<cplx> conv_scratch, std
         throw std::invalid_argument("CztPlan: scratch/output size mismatch");
     skg::CallStage cs;
     void* dx = cs.up(x.data(), x.size() * sizeof(cplx));
-    void* dy = cs.scratch(out.size() * sizeof(cplx));
+    void* dy = cs.out(out.size() * sizeof(cplx));
     G(impl_).execute(dx, true, 0, 1, dy, 0, false, kStream);
     cs.down(out.data(), dy, out.size() * sizeof(cplx));
 }
@@ -171,7 +171,7 @@ ComplexBuffer CztPlan::execute(std::span<const cplx> x) const {
     ComplexBuffer out(output_size());
     skg::CallStage cs;
     void* dx = cs.up(x.data(), x.size() * sizeof(cplx));
-    void* dy = cs.scratch(out.size() * sizeof(cplx));
+    void* dy = cs.out(out.size() * sizeof(cplx));
     G(impl_).execute(dx, true, 0, 1, dy, 0, false, kStream);
     cs.down(out.data(), dy, out.size() * sizeof(cplx));
     return out;
@@ -204,7 +204,7 @@ Spectrum czt_spectrum(const Trace& trace, double f1, double f2, std::size_t m) {
     skg::CztPlanG plan(n, p.a, p.w, p.m);
     skg::CallStage cs;
     void* dx = cs.up(trace.samples.data(), n * sizeof(double));
-    void* dy = cs.scratch(m * sizeof(cplx));
+    void* dy = cs.out(m * sizeof(cplx));
     plan.execute(dx, false, 0, 1, dy, 0, false, kStream);
     Spectrum s;
     s.bins.resize(m);
@@ -223,7 +223,7 @@ Spectrum fft_spectrum(const Trace& t, std::size_t transform_len) {
     if (len < n) throw std::invalid_argument("fft_spectrum: transform length shorter than the trace");
     skg::CallStage cs;
     void* dx = cs.up(t.samples.data(), n * sizeof(double));
-    void* dy = cs.scratch(len * sizeof(cplx));
+    void* dy = cs.out(len * sizeof(cplx));
     skg::fft_spectrum_batch(n, len, false, 0, dx, 0, 1, dy, 0, kStream);
     Spectrum s;
     s.bins.resize(len);
@@ -266,7 +266,7 @@ static ComplexBuffer shift_impl(const double* xr, const cplx* xc, size_t n, doub
     if (n == 0) return y;
     skg::CallStage cs;
     void* dx = xr ? cs.up(xr, n * sizeof(double)) : cs.up(xc, n * sizeof(cplx));
-    void* dy = cs.scratch(n * sizeof(cplx));
+    void* dy = cs.out(n * sizeof(cplx));
     skg::check(skg::launch_freq_shift(xr ? (const double*)dx : nullptr, xr ? nullptr : dx, (long long)n,
                                       -f / fs, dy, kStream),
                "frequency_shift");
@@ -288,7 +288,7 @@ static ComplexBuffer fd_impl(std::span<const cplx> x, std::span<const double> ta
     skg::CallStage cs;
     void* dx = cs.up(x.data(), n * sizeof(cplx));
     void* dt = cs.up(taps.data(), taps.size() * sizeof(double));
-    void* dy = cs.scratch(out.size() * sizeof(cplx));
+    void* dy = cs.out(out.size() * sizeof(cplx));
     skg::check(skg::launch_filter_decimate(dx, (long long)n, (const double*)dt, (int)taps.size(), (int)d,
                                            circular ? 1 : 0, dy, (long long)out.size(), kStream),
                "filter_decimate");
@@ -394,7 +394,7 @@ Spectrum zoom_fft(const ZoomFftPlan& plan, const Trace& t) {   // zoomfft.cpp:18
     if (z.k_lo > z.k_hi) throw std::invalid_argument("zoom_fft: no transform bins fall inside the band");
     skg::CallStage cs;
     void* dx = cs.up(t.samples.data(), t.size() * sizeof(double));
-    void* dy = cs.scratch(z.bins() * sizeof(cplx));
+    void* dy = cs.out(z.bins() * sizeof(cplx));
     z.execute(dx, 0, 1, dy, 0, false, kStream);
     Spectrum s;
     s.bins.resize(z.bins());

@@ -22,7 +22,7 @@ struct Buf {
         release();
         host = pinned_host;
         const size_t c = std::max<size_t>(bytes, 1 << 16);
-        check(host ? cudaHostAlloc(&p, c, cudaHostAllocDefault) : cudaMalloc(&p, c),
+        check(host ? cudaHostAlloc(&p, c, cudaHostAllocMapped | cudaHostAllocPortable) : cudaMalloc(&p, c),
               host ? "cudaHostAlloc (staging)" : "cudaMalloc (staging)");
         cap = c;
     }
@@ -141,8 +141,30 @@ void* CallStage::scratch(size_t bytes) {
     return t.dslot[s].p;
 }
 
+void* CallStage::out(size_t bytes) {
+    if (bytes > kZeroCopyBytes) return scratch(bytes);
+    ThreadDev& t = td();
+    const int s = t.top++;
+    if ((int)t.dslot.size() <= s) {
+        t.dslot.resize(s + 1);
+        t.hslot.resize(s + 1);
+    }
+    t.hslot[s].grow(bytes, true);
+    void* dp = nullptr;   // the device view of the mapped pinned slot (the same address under UVA)
+    check(cudaHostGetDevicePointer(&dp, t.hslot[s].p, 0), "cudaHostGetDevicePointer");
+    t.pending = true;
+    return dp;
+}
+
 void CallStage::down(void* host, const void* dev, size_t bytes) {
     ThreadDev& t = td();
+    for (int s = mark_; s < t.top; ++s)   // an out() slot: the kernels wrote host memory directly
+        if (t.hslot[s].p && (dev == t.hslot[s].p) && bytes <= t.hslot[s].cap) {
+            check(cudaStreamSynchronize(stream()), "cudaStreamSynchronize");
+            t.pending = false;
+            std::memcpy(host, t.hslot[s].p, bytes);
+            return;
+        }
     const int s = t.top++;
     if ((int)t.dslot.size() <= s) {
         t.dslot.resize(s + 1);

@@ -30,6 +30,10 @@ class CallStage {
     void* up(const void* host, size_t bytes);
     // an uninitialised device slot
     void* scratch(size_t bytes);
+    // an output slot for down(): up to kZeroCopyBytes it is mapped pinned host memory the kernels
+    // write directly (no D2H copy; down() only synchronises and copies out), larger a device slot
+    static constexpr size_t kZeroCopyBytes = size_t{1} << 20;
+    void* out(size_t bytes);
     // device -> host through a pinned slot; synchronises stream()
     void down(void* host, const void* dev, size_t bytes);
     cudaStream_t stream() const { return cudaStreamPerThread; }
