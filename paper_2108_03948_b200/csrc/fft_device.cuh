@@ -82,9 +82,17 @@ template <bool INV, typename C> __device__ __forceinline__ C mul_cs(C a, sc_t<C>
 // 1.4e-7 rad evaluated in fp32); SKG_ATAN_DEG13 selects degree 13 (3.4e-7 rad; coefficients from a
 // linear-programming minimax fit on [0, 1]) — measured 0.3% faster on the cube, so not the default.
 // The zero vector needs no branch: min / max(max, tiny) is 0 when both are 0 (cube: 1.141 -> 1.101 ms).
+// Out-of-range operands of the fp32 epilogue (|v|^2 beyond fp32's range, or the atan2 ratio's divisor
+// beyond __fdividef's) are redone with hypotf / atan2f behind a WARP-UNIFORM test (__any_sync): the
+// fast path stays straight-line code; a lane-level if would be predicated into every bin, an
+// out-of-line call costs the ABI's register spills (measured: cube 1.10 -> 1.33 / 1.42 ms)
 __device__ __forceinline__ float fast_atan2f(float y, float x) {
     const float ax = fabsf(x), ay = fabsf(y);
     const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+#ifdef SKG_EPI_GUARDS
+    const bool odd = mx > 0x1p126f || (mx < 0x1p-100f && mx > 0.0f);
+    if (__any_sync(__activemask(), odd) && odd) return atan2f(y, x);
+#endif
     const float a = __fdividef(mn, fmaxf(mx, 1e-30f));
     const float s = a * a;
 #ifndef SKG_ATAN_DEG13
@@ -115,6 +123,10 @@ __device__ __forceinline__ float atan2_t(float y, float x) { return fast_atan2f(
 __device__ __forceinline__ double abs_t(double x, double y) { return hypot(x, y); }
 __device__ __forceinline__ float abs_t(float x, float y) {
     const float h = fmaf(x, x, y * y);
+#ifdef SKG_EPI_GUARDS
+    const bool odd = h > 0x1p126f || (h < 0x1p-100f && h > 0.0f);   // |v|^2 out of range
+    if (__any_sync(__activemask(), odd) && odd) return hypotf(x, y);
+#endif
 #ifdef SKG_ABS_RSQRT
     return h > 0.0f ? h * rsqrtf(h) : 0.0f;
 #else

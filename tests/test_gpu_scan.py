@@ -12,6 +12,25 @@ from paper_2108_03948_b200.workloads import SCAN_CASES
 pytestmark = pytest.mark.gpu
 
 
+# The picks that differ from the reference's, enumerated (case, route, separation index, column):
+# every one is a valley of a symmetric pair — the mirror bin about the centre or a bin at the fp64 noise
+# floor — decided by the last bits of the transform (tools/scan_ties.py lists them). Any other
+# difference, or one of these disappearing, fails.
+KNOWN_TIES = {("pow2", "fft", 26, 6), ("pow2", "czt", 23, 6), ("pow2", "czt", 33, 6)}
+
+
+def test_scan_ties_are_exactly_the_enumerated_ones(golden):
+    g = golden("scan")
+    found = set()
+    for name in SCAN_CASES:
+        got = sk.resolvability_scan(**SCAN_CASES[name])
+        for route in ("fft", "czt"):
+            a, b = got[route], g[f"{name}_{route}"]
+            for col in (2, 4, 6):
+                found |= {(name, route, int(i), col) for i in np.nonzero(a[:, col] != b[:, col])[0]}
+    assert found == KNOWN_TIES
+
+
 @pytest.mark.parametrize("name", list(SCAN_CASES))
 def test_scan_matches_reference(golden, name):
     g = golden("scan")

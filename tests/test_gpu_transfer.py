@@ -43,10 +43,15 @@ def test_cfg1_pair_fp64(golden):
 
 def test_cube_slice_fp32():
     """configs[3] shape on a 16 x 16 tile: 2048 samples fp32 -> FFT 8192 -> |H|, arg H on 4097 bins.
-    fp32 tolerance 1e-5 (relative L2) applies to the spectra X_s (the transform itself) and to |H| on the
-    SURVEY §8d mask (|X_ref| >= 1e-3 max); the complex H / phase carries the fp32 transform error
-    divided by small |X_s|, |X_ref|, so it is checked at 1e-5 on the better-conditioned 1e-2 mask and at
-    1e-4 on the 1e-3 mask."""
+    The transform itself (X_s) and |H| meet the fp32 north_star tolerance (1e-5 relative L2) on the
+    SURVEY §8d mask (|X_ref| >= 1e-3 max). H = X_s / X_ref is then held to a bound DERIVED from the
+    measured transform error instead of a blanket factor: with dX_s the fp32 spectrum's error (measured
+    per pixel against the fp64 oracle, same kernel, same instructions) and e = 1e-6 the epilogue's budget
+    (a few fp32 roundings, sqrt.approx 2^-23, the degree-15 atan 1.4e-7 rad),
+        |dH_k| <= |dX_s,k| / |X_ref,k| + e |H_k|        (per bin),
+    so the complex H error (as |H| e^{i arg H}) must stay within 2x that bin-wise bound in L2 and the
+    phase error weighted by |H_k| within 2x its per-bin maximum. The bound grows where |X_ref| is
+    small (an fp32 error divided by a small number): conditioning, not an algorithmic loss."""
     cube, ref = W.cfg4_cube(16, 16, 2048)
     plan = sk.TransferPlanGPU(ref, 8192, sk.SKG_F32)
     assert plan.bins == 4097
@@ -57,22 +62,43 @@ def test_cube_slice_fp32():
     m = _mask(xr)
     m2 = np.abs(xr) >= 1e-2 * np.max(np.abs(xr))
     magg, phg = mag.cpu().numpy(), ph.cpu().numpy()
-    worst_mag = worst_h = worst_h2 = worst_ph = worst_xs = 0.0
+    eps = 1e-6
+    worst_mag = worst_xs = worst_h2 = 0.0
     for i in range(cube.shape[0]):
         xs = O.fft_spectrum(cube[i].astype(np.float64), 1.0, 8192)[0][:4097]
-        worst_xs = max(worst_xs, np.linalg.norm(xs_gpu[i] - xs) / np.linalg.norm(xs))
+        dxs = xs_gpu[i].astype(np.complex128) - xs
+        worst_xs = max(worst_xs, np.linalg.norm(dxs) / np.linalg.norm(xs))
         H, M, P = O.transfer(xs, xr)
+        worst_mag = max(worst_mag, np.linalg.norm(magg[i][m] - M[m]) / np.linalg.norm(M[m]))
+        hg = magg[i][m] * np.exp(1j * phg[i][m].astype(np.float64))
+        bound_k = np.abs(dxs[m]) / np.abs(xr[m]) + eps * np.abs(H[m])   # per-bin derived bound
+        assert np.linalg.norm(hg - H[m]) <= 2 * np.linalg.norm(bound_k), i
+        dph = np.abs(_wrap(phg[i][m] - P[m])) * M[m]
+        assert np.max(dph) <= 2 * np.max(bound_k), i
         hg2 = magg[i][m2] * np.exp(1j * phg[i][m2].astype(np.float64))
         worst_h2 = max(worst_h2, np.linalg.norm(hg2 - H[m2]) / np.linalg.norm(H[m2]))
-        worst_mag = max(worst_mag, np.linalg.norm(magg[i][m] - M[m]) / np.linalg.norm(M[m]))
-        # magnitude and phase together: rel L2 of |H| e^{i arg H} (phase of near-zero bins carries no weight)
-        hg = magg[i][m] * np.exp(1j * phg[i][m].astype(np.float64))
-        worst_h = max(worst_h, np.linalg.norm(hg - H[m]) / np.linalg.norm(H[m]))
-        # phase alone, weighted by |H|: fp32 phase noise on a bin is ~eps * max|X| / |X_k|, so the
-        # phase error times |H_k| is bounded by the spectrum-wide fp32 error
-        worst_ph = max(worst_ph, np.max(np.abs(_wrap(phg[i][m] - P[m])) * M[m]) / M[m].max())
     assert worst_xs <= TOL_F32 and worst_mag <= TOL_F32 and worst_h2 <= TOL_F32
-    assert worst_h <= 10 * TOL_F32 and worst_ph <= 10 * TOL_F32
+
+
+@pytest.mark.parametrize("scale", [2.0 ** 60, 2.0 ** -44])
+def test_fp32_magnitude_range(scale):
+    """The fp32 epilogue's documented range: |H| from 2^-50 to 2^63 (|H|^2 inside fp32, the atan2 ratio's
+    divisor inside __fdividef's range). Guards for operands beyond it cost the cube 20-40%
+    whatever their form (predicated, out-of-line call, warp-uniform branch: 1.10 -> 1.33 / 1.42 / 1.52
+    ms), so they are a build option (-DSKG_EPI_GUARDS). At both ends of the range, sample = scale *
+    reference (scale a power of two: the fp32 transform scales exactly) must give scale * (the unscaled
+    result) bin for bin, to the epilogue's rounding."""
+    ref = W.cfg1_pair()[0][:1024].astype(np.float32).astype(np.float64)
+    plan = sk.TransferPlanGPU(ref, 4096, sk.SKG_F32)
+    x1 = torch.from_numpy(np.stack([ref] * 3).astype(np.float32)).to(DEV)
+    m1, p1 = plan.execute(x1)
+    ms, ps = plan.execute(x1 * scale)
+    m1, p1, ms, ps = (t.cpu().numpy().astype(np.float64) for t in (m1, p1, ms, ps))
+    xr = O.fft_spectrum(ref, 1.0, 4096)[0][:2049]
+    m = _mask(xr)
+    assert np.all(np.isfinite(ms[:, m])) and np.all(ms[:, m] > 0)
+    assert np.max(np.abs(ms[:, m] / scale - m1[:, m]) / m1[:, m]) <= 4e-7
+    assert np.max(np.abs(_wrap(ps[:, m] - p1[:, m]))) <= 1e-6
 
 
 def test_errors():
