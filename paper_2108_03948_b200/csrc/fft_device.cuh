@@ -54,6 +54,77 @@ template <typename C> __device__ __forceinline__ C cconj(C a) { return mk<C>(a.x
 template <typename C> __device__ __forceinline__ C cscale(C a, sc_t<C> s) { return mk<C>(a.x * s, a.y * s); }
 // real * complex
 template <typename C> __device__ __forceinline__ C rmul(sc_t<C> r, C a) { return mk<C>(r * a.x, r * a.y); }
+// ---- packed fp32 (sm_100a FADD2 / FMUL2 / FFMA2) --------------------------------------------------
+// Blackwell issues two fp32 operations per lane in one instruction (fma.rn.f32x2 & co.), at the same
+// flop rate as scalar FFMA (tools/micro/ffma2.cu: 238 against 233 flop/clk/SM) but half the issue
+// slots. A complex value is exactly such a pair, and the fp32 transforms are issue bound (the cube:
+// 70% issue active, FP instructions 62% of the stream), so float2 arithmetic is carried packed: a
+// complex add is one FADD2, a complex product an FMUL2 + FFMA2 (ptxas folds the broadcast / swapped
+// operands into the F32 / LO_HI operand selectors; only a swapped-and-negated operand costs a scalar
+// negate). Same formulas as the scalar code, fused where the scalar code's contraction fuses.
+#ifndef SKG_NO_F32X2
+namespace px {
+__device__ __forceinline__ unsigned long long pk(float lo, float hi) {
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float2 up(unsigned long long v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ float2 add(float2 a, float2 b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a.x, a.y)), "l"(pk(b.x, b.y)));
+    return up(r);
+}
+__device__ __forceinline__ float2 sub(float2 a, float2 b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a.x, a.y)), "l"(pk(b.x, b.y)));
+    return up(r);
+}
+__device__ __forceinline__ float2 mul(float2 a, float2 b) {
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk(a.x, a.y)), "l"(pk(b.x, b.y)));
+    return up(r);
+}
+__device__ __forceinline__ float2 fma(float2 a, float2 b, float2 c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk(a.x, a.y)), "l"(pk(b.x, b.y)), "l"(pk(c.x, c.y)));
+    return up(r);
+}
+__device__ __forceinline__ float2 bc(float v) { return make_float2(v, v); }
+}  // namespace px
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return px::add(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return px::sub(a, b); }
+// a b = a.x (b.x, b.y) + a.y (-b.y, b.x)
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return px::fma(px::bc(a.y), make_float2(-b.y, b.x), px::mul(px::bc(a.x), b));
+}
+// a conj(b) = b.x (a.x, a.y) + b.y (a.y, -a.x)
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+    return px::fma(px::bc(b.y), make_float2(a.y, -a.x), px::mul(px::bc(b.x), a));
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return px::mul(px::bc(s), a); }
+__device__ __forceinline__ float2 rmul(float r, float2 a) { return px::mul(px::bc(r), a); }
+template <bool INV> __device__ __forceinline__ float2 mul_w8(float2 a) {
+    // forward r (a.x + a.y, a.y - a.x) = r (a + (a.y, -a.x)); inverse r (a.x - a.y, a.x + a.y) = r (a + (-a.y, a.x))
+    const float r = 0.70710678118654752440f;
+    return px::mul(px::bc(r), px::add(a, INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x)));
+}
+template <bool INV> __device__ __forceinline__ float2 mul_w8_3(float2 a) {
+    // forward r (a.y - a.x, -(a.x + a.y)) = r ((a.y, -a.x) - a); inverse r (-(a.x + a.y), a.x - a.y) = r ((-a.y, a.x) - a)
+    const float r = 0.70710678118654752440f;
+    return px::mul(px::bc(r), px::sub(INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x), a));
+}
+// a e^{-/+ i theta}: forward c a + s (a.y, -a.x); inverse c a + s (-a.y, a.x)
+template <bool INV> __device__ __forceinline__ float2 mul_cs(float2 a, float c, float s) {
+    return px::fma(px::bc(s), INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x), px::mul(px::bc(c), a));
+}
+#endif
+
 // twiddle multiply: forward uses w, inverse uses conj(w)
 template <bool INV, typename C> __device__ __forceinline__ C twmul(C a, C w) {
     return INV ? cmulc(a, w) : cmul(a, w);
