@@ -355,6 +355,66 @@ void c2c_4step(const FourStep& f, bool inverse, int in_kind, const void* in, lon
         count_launch(2);
     }
 }
+
+// Real traces: Hermitian-half four-step (kernels_4step_real.cuh) — column pairs ride one complex column
+// transform, only the work rows k1 <= R/2 exist, the row pass stores each bin and its mirror.
+// layout 0: L bins, 1: L/2 + 1 bins. SKG_4STEP_REAL=0 selects the complex four-step (A/B).
+bool r2c_4step_enabled(const FourStep& f, bool f32) {
+    const char* e = std::getenv("SKG_4STEP_REAL");
+    if (e && e[0] == '0') return false;
+    return (1LL << f.lC) >= 2 * (f32 ? 16 : 8);
+}
+// One cooperative persistent launch for both passes with the work rows in an L2-resident ring (square
+// factorisations R = C, batches of at least a few grids of units; same arithmetic as the two launches, so
+// the results are identical bit for bit). SKG_4STEP_FUSED=0 disables it; SKG_4STEP_DELTA_X10 scales the
+// look-ahead (tenths of a grid of units, default 25).
+template <typename T>
+bool r2c_4step_fused(const FourStep& f, const void* in, long long in_stride, long long N, void* out,
+                     long long out_stride, int layout, long long batch, cudaStream_t st) {
+    const char* e = std::getenv("SKG_4STEP_FUSED");
+    if (e && e[0] == '0') return false;
+    if (f.lR != f.lC || f.lR < 8 || f.lR > 9) return false;
+    const int ups = launch_4step_rfused_ups<T>(f.lR);
+    if (ups <= 0) return false;
+    int grid = 0;
+    if (launch_4step_rfused<T>(f.lR, in, in_stride, N, nullptr, 1, 1, batch, f.twR, f.twL, out, out_stride, layout,
+                               nullptr, nullptr, &grid, st) != cudaSuccess || grid <= 0)
+        return false;
+    const char* dx = std::getenv("SKG_4STEP_DELTA_X10");
+    const long long x10 = dx ? std::max(1, std::atoi(dx)) : 25;
+    const long long delta = std::max<long long>(2, (grid * x10 / 10 + ups - 1) / ups);
+    const long long slots = delta + std::max<long long>(2, (2LL * grid + ups - 1) / ups);
+    if (batch < 2 * slots) return false;   // short batches: the two launches
+    const long long rows = (1LL << f.lR) / 2 + 1, Cn = 1LL << f.lC;
+    Scratch Y((size_t)slots * rows * Cn * 2 * sizeof(T), st);
+    Scratch cnt((size_t)batch * 2 * sizeof(unsigned), st);
+    check(cudaMemsetAsync(cnt.p, 0, (size_t)batch * 2 * sizeof(unsigned), st), "4step fused counters");
+    unsigned* col_done = static_cast<unsigned*>(cnt.p);
+    const char* dbg = std::getenv("SKG_ROWH_DBG");   // EXPERIMENT
+    check(launch_4step_rfused<T>(f.lR, in, in_stride, N, Y.p, (int)slots, (int)delta, batch, f.twR, f.twL, out,
+                                 out_stride, layout | (dbg ? std::atoi(dbg) << 1 : 0), col_done, col_done + batch, nullptr, st),
+          "4step real fused");
+    count_launch();
+    return true;
+}
+template <typename T>
+void r2c_4step(const FourStep& f, const void* in, long long in_stride, long long N, void* out, long long out_stride,
+               int layout, long long batch, cudaStream_t st) {
+    if (r2c_4step_fused<T>(f, in, in_stride, N, out, out_stride, layout, batch, st)) return;
+    const long long rows = (1LL << f.lR) / 2 + 1, Cn = 1LL << f.lC;
+    const long long per = rows * Cn * 2 * (long long)sizeof(T);
+    const long long ch = std::max<long long>(1, std::min<long long>(batch, (2048LL << 20) / per));
+    Scratch Y((size_t)ch * per, st);
+    for (long long b0 = 0; b0 < batch; b0 += ch) {
+        const long long nb = std::min(ch, batch - b0);
+        const void* src = static_cast<const char*>(in) + (size_t)b0 * in_stride * sizeof(T);
+        void* dst = static_cast<char*>(out) + (size_t)b0 * out_stride * 2 * sizeof(T);
+        check(launch_4step_colr<T>(f.lR, src, in_stride, N, Y.p, f.lC, nb, f.twR, f.twL, st), "4step real col");
+        const char* dbg = std::getenv("SKG_ROWH_DBG");   // EXPERIMENT
+        check(launch_4step_rowh<T>(f.lC, Y.p, f.lR, nb, f.twC, dst, out_stride, layout | (dbg ? std::atoi(dbg) << 1 : 0), st), "4step real row");
+        count_launch(2);
+    }
+}
 }  // namespace
 
 // ---- transforms -------------------------------------------------------------------------------
@@ -649,6 +709,11 @@ void fft_spectrum_batch(size_t n, size_t len, bool f32, int layout, const void* 
         // multi-pass: complex FFT of the zero-padded real rows (imaginary part synthesised as 0)
         FourStep f(lgM + 1, f32);
         const size_t cs = f32 ? 8 : 16;
+        if (r2c_4step_enabled(f, f32)) {
+            if (f32) r2c_4step<float>(f, x, x_stride, (long long)n, out, out_stride, layout, batch, st);
+            else r2c_4step<double>(f, x, x_stride, (long long)n, out, out_stride, layout, batch, st);
+            return;
+        }
         if (layout == 0) {
             if (f32) c2c_4step<float>(f, false, 1, x, x_stride, (long long)n, out, out_stride, batch, st);
             else c2c_4step<double>(f, false, 1, x, x_stride, (long long)n, out, out_stride, batch, st);

@@ -72,6 +72,23 @@ cudaError_t launch_4step_row(int log2C, int mode, void* Y, int log2R, long long 
                              const void* twL, const void* khat_p, void* out, long long out_stride, T scale,
                              int conj_out, cudaStream_t st);
 
+// real traces, Hermitian half (kernels_4step_real.cuh): column pass into (R/2 + 1) x C work rows, row pass with
+// the mirrored conjugate store; half != 0 writes the L/2 + 1 bin layout
+template <typename T>
+cudaError_t launch_4step_colr(int log2R, const void* x, long long x_stride, long long N, void* Y, int log2C,
+                              long long batch, const void* tw, const void* twL, cudaStream_t st);
+template <typename T>
+cudaError_t launch_4step_rowh(int log2C, const void* Y, int log2R, long long batch, const void* tw, void* out,
+                              long long out_stride, int half, cudaStream_t st);
+
+// both passes in one cooperative persistent launch, work rows in a ring of `slots` traces (square R = C = 2^lg);
+// grid_out != nullptr: only report the grid the launch would use. ups: units per trace step.
+template <typename T>
+cudaError_t launch_4step_rfused(int lg, const void* x, long long x_stride, long long N, void* Yring, int slots, int delta,
+                                long long batch, const void* tw, const void* twL, void* out, long long out_stride,
+                                int half, unsigned* col_done, unsigned* row_done, int* grid_out, cudaStream_t st);
+template <typename T> int launch_4step_rfused_ups(int lg);
+
 // ---- fused Zoom FFT (kernels_zoom.cu) --------------------------------------------------
 constexpr int kZoomK = 4;   // FIR outputs per thread
 struct ZoomArgs {

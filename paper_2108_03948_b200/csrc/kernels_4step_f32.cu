@@ -1,5 +1,5 @@
 // Instantiation of the four-step (multi-pass) kernels for float (see kernels_4step.cuh).
-#include "kernels_4step.cuh"
+#include "kernels_4step_real.cuh"
 
 namespace skg {
 
@@ -20,5 +20,27 @@ cudaError_t launch_4step_row<float>(int log2C, int mode, void* Y, int log2R, lon
     return launch_4step_row_impl<float>(log2C, mode, Y, log2R, batch, tw, twL, khat_p, out, out_stride, scale,
                                       conj_out, st);
 }
+
+template <>
+cudaError_t launch_4step_colr<float>(int log2R, const void* x, long long x_stride, long long N, void* Y, int log2C,
+                                   long long batch, const void* tw, const void* twL, cudaStream_t st) {
+    return launch_4step_colr_impl<float>(log2R, x, x_stride, N, Y, log2C, batch, tw, twL, st);
+}
+
+template <>
+cudaError_t launch_4step_rowh<float>(int log2C, const void* Y, int log2R, long long batch, const void* tw, void* out,
+                                   long long out_stride, int half, cudaStream_t st) {
+    return launch_4step_rowh_impl<float>(log2C, Y, log2R, batch, tw, out, out_stride, half, st);
+}
+
+template <>
+cudaError_t launch_4step_rfused<float>(int lg, const void* x, long long x_stride, long long N, void* Yring, int slots,
+                                     int delta, long long batch, const void* tw, const void* twL, void* out,
+                                     long long out_stride, int half, unsigned* col_done, unsigned* row_done,
+                                     int* grid_out, cudaStream_t st) {
+    return launch_4step_rfused_impl<float>(lg, x, x_stride, N, Yring, slots, delta, batch, tw, twL, out, out_stride, half,
+                                         col_done, row_done, grid_out, st);
+}
+template <> int launch_4step_rfused_ups<float>(int lg) { return fused_units_per_step<float>(lg); }
 
 }  // namespace skg

@@ -124,3 +124,68 @@ def test_long_fft_batches(prec, L, path, monkeypatch):
         assert rel_max_rows(cb, ref_back) <= TOL_F64
     else:
         assert rel_l2_rows(cb, ref_back) <= TOL_F32
+
+
+@pytest.mark.parametrize("real_path", ["1", "0"])
+@pytest.mark.parametrize("prec,L", [("f64", 32768), ("f64", 65536), ("f64", 262144), ("f32", 65536), ("f32", 131072),
+                                    ("f32", 262144), ("f32", 1048576)])
+def test_real_fourstep_paths(prec, L, real_path, monkeypatch):
+    """fft_spectrum beyond one CTA: the Hermitian-half four-step (kernels_4step_real.cuh: paired real
+    columns, work rows k1 <= R/2, mirrored conjugate store) and the complex four-step it replaces
+    (SKG_4STEP_REAL=0) against the oracle — every zero-padding class of the column pass (N = L/4, L/2,
+    L, and ragged lengths between), odd N, both layouts, more units than resident CTAs."""
+    monkeypatch.setenv("SKG_CLUSTER", "0")
+    monkeypatch.setenv("SKG_4STEP_REAL", real_path)
+    dt = torch.float64 if prec == "f64" else torch.float32
+    for n, b in ((L // 4, 9), (L // 4 - 3, 2), (L // 2 + 1, 2), (L, 2), (L - 1, 1), (7, 1)):
+        if L > 262144:
+            b = 1
+        x = W.sample_traces(b, n) if n >= 64 else np.arange(1.0, n + 1.0)[None, :] * np.ones((b, 1))
+        xd = torch.from_numpy(x).to(dt).to(DEV)
+        xin = xd.cpu().double().numpy()
+        want = O.fft_spectrum_batch(xin, L)
+        got = sk.fft_spectrum_batch(xd, L).cpu().numpy()
+        half = sk.fft_spectrum_batch(xd, L, layout=sk.SKG_HALF).cpu().numpy()
+        if prec == "f64":
+            assert rel_max_rows(got, want) <= TOL_F64, (n, b)
+        else:
+            assert rel_l2_rows(got, want) <= TOL_F32, (n, b)
+        np.testing.assert_array_equal(half, got[:, : L // 2 + 1])
+
+
+@pytest.mark.parametrize("variant", ["default", "short-lookahead", "small-grid"])
+@pytest.mark.parametrize("prec,L,b", [("f32", 65536, 300), ("f64", 65536, 200), ("f32", 262144, 64), ("f64", 262144, 64)])
+def test_real_fourstep_fused_ring(prec, L, b, variant, monkeypatch):
+    """The one-launch Hermitian four-step (k4_rfused: column and row units interleaved in one persistent
+    cooperative grid, work rows in an L2-resident ring reused every `slots` traces, release/acquire
+    counters between the passes) gives the two-launch path's bits for every trace, and the oracle's
+    spectrum on the first / middle / last traces — with the default look-ahead, with a look-ahead so short
+    that row units block on their column units and rows are staged late, and with a small grid."""
+    monkeypatch.setenv("SKG_CLUSTER", "0")
+    monkeypatch.setenv("SKG_4STEP_REAL", "1")
+    if variant == "short-lookahead":
+        monkeypatch.setenv("SKG_4STEP_DELTA_X10", "1")
+    dt = torch.float64 if prec == "f64" else torch.float32
+    n = L // 4 - 3
+    x = W.sample_traces(b, n)
+    xd = torch.from_numpy(x).to(dt).to(DEV)
+    xin = xd.cpu().double().numpy()
+    monkeypatch.setenv("SKG_4STEP_FUSED", "0")
+    two = sk.fft_spectrum_batch(xd, L)
+    two_half = sk.fft_spectrum_batch(xd, L, layout=sk.SKG_HALF)
+    monkeypatch.setenv("SKG_4STEP_FUSED", "1")
+    with sk.grid_cap(61 if variant == "small-grid" else 0):
+        n0 = sk.launch_count()
+        one = sk.fft_spectrum_batch(xd, L)
+        assert sk.launch_count() - n0 == 1, "the fused path did not run"
+        one_half = sk.fft_spectrum_batch(xd, L, layout=sk.SKG_HALF)
+        torch.cuda.synchronize()
+    assert torch.equal(one, two)
+    assert torch.equal(one_half, two_half)
+    got = one.cpu().numpy()
+    for i in (0, b // 2, b - 1):
+        want = O.fft_spectrum_batch(xin[i:i + 1], L)
+        if prec == "f64":
+            assert rel_max_rows(got[i:i + 1], want) <= TOL_F64
+        else:
+            assert rel_l2_rows(got[i:i + 1], want) <= TOL_F32

@@ -1,0 +1,18 @@
+"""One long zero-padded spectrum call (for ncu): python tools/fft4_one.py <f32|f64> <L> <batch>"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import paper_2108_03948_b200 as sk  # noqa: E402
+from paper_2108_03948_b200 import workloads as W  # noqa: E402
+
+prec, L, batch = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
+n = L // 4
+dt = torch.float64 if prec == "f64" else torch.float32
+x = torch.from_numpy(W.sample_traces(64, n)).to(dt).cuda().repeat(batch // 64, 1)
+out = sk.fft_spectrum_batch(x, L)
+sk.fft_spectrum_batch(x, L, out=out)
+torch.cuda.synchronize()
