@@ -383,16 +383,15 @@ bool r2c_4step_fused(const FourStep& f, const void* in, long long in_stride, lon
     const char* dx = std::getenv("SKG_4STEP_DELTA_X10");
     const long long x10 = dx ? std::max(1, std::atoi(dx)) : 25;
     const long long delta = std::max<long long>(2, (grid * x10 / 10 + ups - 1) / ups);
-    const long long slots = delta + std::max<long long>(2, (2LL * grid + ups - 1) / ups);
-    if (batch < 2 * slots) return false;   // short batches: the two launches
+    const long long slots = delta + (grid + ups - 1) / ups + 2;   // column start .. last row unit done
+    if (batch < slots) return false;   // short batches: the two launches
     const long long rows = (1LL << f.lR) / 2 + 1, Cn = 1LL << f.lC;
     Scratch Y((size_t)slots * rows * Cn * 2 * sizeof(T), st);
     Scratch cnt((size_t)batch * 2 * sizeof(unsigned), st);
     check(cudaMemsetAsync(cnt.p, 0, (size_t)batch * 2 * sizeof(unsigned), st), "4step fused counters");
     unsigned* col_done = static_cast<unsigned*>(cnt.p);
-    const char* dbg = std::getenv("SKG_ROWH_DBG");   // EXPERIMENT
     check(launch_4step_rfused<T>(f.lR, in, in_stride, N, Y.p, (int)slots, (int)delta, batch, f.twR, f.twL, out,
-                                 out_stride, layout | (dbg ? std::atoi(dbg) << 1 : 0), col_done, col_done + batch, nullptr, st),
+                                 out_stride, layout, col_done, col_done + batch, nullptr, st),
           "4step real fused");
     count_launch();
     return true;
@@ -410,8 +409,7 @@ void r2c_4step(const FourStep& f, const void* in, long long in_stride, long long
         const void* src = static_cast<const char*>(in) + (size_t)b0 * in_stride * sizeof(T);
         void* dst = static_cast<char*>(out) + (size_t)b0 * out_stride * 2 * sizeof(T);
         check(launch_4step_colr<T>(f.lR, src, in_stride, N, Y.p, f.lC, nb, f.twR, f.twL, st), "4step real col");
-        const char* dbg = std::getenv("SKG_ROWH_DBG");   // EXPERIMENT
-        check(launch_4step_rowh<T>(f.lC, Y.p, f.lR, nb, f.twC, dst, out_stride, layout | (dbg ? std::atoi(dbg) << 1 : 0), st), "4step real row");
+        check(launch_4step_rowh<T>(f.lC, Y.p, f.lR, nb, f.twC, dst, out_stride, layout, st), "4step real row");
         count_launch(2);
     }
 }

@@ -142,22 +142,11 @@ template <bool CS, typename C> __device__ __forceinline__ void st_out(C* p, C v)
 }
 template <typename T, int LOG2C, bool CS = false>
 __device__ __forceinline__ void rowh_store(const cx_t<T> (&v)[FftGeom<LOG2C>::EPT], cx_t<T>* __restrict__ o,
-                                           long long k1, long long R, int tid, bool half, int dbg = 0) {
+                                           long long k1, long long R, int tid, bool half) {
     using C = cx_t<T>;
     using G = FftGeom<LOG2C>;
     const long long L = R * G::L;
     const bool self = k1 == 0 || 2 * k1 == R;
-#ifdef SKG_ROWH_DEBUG
-    if (dbg) {   // timing experiments: 1 = no mirror store, 2 = mirror shifted onto aligned segments (wrong values)
-#pragma unroll
-        for (int q = 0; q < G::EPT; ++q) {
-            const long long idx = k1 + R * (tid + (long long)G::NT * q);
-            st_out<CS>(o + idx, v[q]);
-            if (dbg == 2 && idx + 1 < L) st_out<CS>(o + (L - idx - 1), cconj(v[q]));
-        }
-        return;
-    }
-#endif
 #pragma unroll
     for (int q = 0; q < G::EPT; ++q) {
         const long long idx = k1 + R * (tid + (long long)G::NT * q);
@@ -277,7 +266,7 @@ k4_rowh(const cx_t<T>* __restrict__ Y, int log2R, long long batch, const cx_t<T>
             for (int q = 0; q < G::EPT; ++q) v[q] = valid ? row[tid + G::NT * q] : czero<C>();
         }
         block_fft<false, LOG2C>(v, sm, tws, tid);
-        if (valid) rowh_store<T, LOG2C>(v, out + b * out_stride, k1, R, tid, (half & 1) != 0, half >> 1);
+        if (valid) rowh_store<T, LOG2C>(v, out + b * out_stride, k1, R, tid, half != 0);
     }
 }
 
@@ -404,6 +393,12 @@ template <int LOG2L, typename C> __device__ __forceinline__ void pass_read(C (&v
 #ifndef SKG_RFUSED_MINB_F32_256
 #define SKG_RFUSED_MINB_F32_256 3
 #endif
+#ifndef SKG_RFUSED_THREADS_F64
+#define SKG_RFUSED_THREADS_F64 512   // resident threads per SM the fp64 register cap targets
+#endif
+#ifndef SKG_RFUSED_MINB_F32_512
+#define SKG_RFUSED_MINB_F32_512 2   // 64 registers, 2 CTAs per SM: 2^18 fp32 4.76 -> 4.00 ms
+#endif
 template <typename T, int LG> struct FusedCfg {
     using G = FftGeom<LG>;
     static constexpr int W = Tile<T>::W;
@@ -418,7 +413,7 @@ template <typename T, int LG> struct FusedCfg {
     static constexpr size_t SMEM = ((size_t)W * (G::SMEM + 1) + G::TW_ALLOC + (size_t)W * (G::L / 2 + 1)) * sizeof(cx_t<T>);
     static constexpr bool OK = G::L >= 2 * W && G::P >= 2 && G::P <= 3 && BLOCK % 32 == 0;
     // registers: fp64 holds 16 complex = 64 registers of data (128 per thread); fp32 runs at 85 / 128
-    static constexpr int MINB = sizeof(T) == 8 ? 512 / BLOCK : (BLOCK >= 512 ? 1 : SKG_RFUSED_MINB_F32_256);
+    static constexpr int MINB = sizeof(T) == 8 ? SKG_RFUSED_THREADS_F64 / BLOCK : (BLOCK >= 512 ? SKG_RFUSED_MINB_F32_512 : SKG_RFUSED_MINB_F32_256);
 };
 
 #ifndef SKG_RFUSED_CS
@@ -519,7 +514,7 @@ k4_rfused(const T* __restrict__ x, long long x_stride, long long N, int vec, cx_
             stockham_pass<false, G::P - 1, 16, 16, LG>(v, sm, tws, tid);   // last pass: registers only
             const long long k1 = r0 + g;
             if (k1 < F::ROWS)
-                rowh_store<T, LG, SKG_RFUSED_CS != 0>(v, out + t * out_stride, k1, R, tid, (half & 1) != 0, half >> 1);
+                rowh_store<T, LG, SKG_RFUSED_CS != 0>(v, out + t * out_stride, k1, R, tid, half != 0);
         }
     }
 }
