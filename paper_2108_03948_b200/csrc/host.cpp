@@ -383,7 +383,9 @@ bool r2c_4step_fused(const FourStep& f, const void* in, long long in_stride, lon
     const char* dx = std::getenv("SKG_4STEP_DELTA_X10");
     const long long x10 = dx ? std::max(1, std::atoi(dx)) : 25;
     const long long delta = std::max<long long>(2, (grid * x10 / 10 + ups - 1) / ups);
-    const long long slots = delta + (grid + ups - 1) / ups + 2;   // column start .. last row unit done
+    // column start .. row units read; a ring twice as long measured slower (it spills from L2):
+    // FFT 2^16 fp64 3.28 -> 3.53 ms
+    const long long slots = delta + (grid + ups - 1) / ups + 2;
     if (batch < slots) return false;   // short batches: the two launches
     const long long rows = (1LL << f.lR) / 2 + 1, Cn = 1LL << f.lC;
     Scratch Y((size_t)slots * rows * Cn * 2 * sizeof(T), st);
@@ -581,6 +583,47 @@ const CztPlanG::Dev& CztPlanG::dev(bool f32) const {
     });
 }
 
+bool CztPlanG::czt_4step_fused(const FourStepRef& fr, bool f32, const void* x, bool complex_in, long long x_stride,
+                               long long N, const Dev& d, long long batch, void* out, long long out_stride,
+                               cudaStream_t st) const {
+    const FourStep& f = *static_cast<const FourStep*>(fr.p);
+    const char* e = std::getenv("SKG_4STEP_FUSED");
+    if (e && e[0] == '0') return false;
+    const size_t cs = f32 ? 8 : 16;
+    auto call = [&](const void* cinp, void* yring, int slots, int delta, void* dst, long long mh, unsigned* cnt,
+                    int* grid, int* ups) {
+        return f32 ? launch_4step_czt_fused<float>(f.lR, f.lC, x, complex_in ? 1 : 0, x_stride, N, cinp, yring, slots,
+                                                   delta, batch, f.twR, f.twC, f.twL, d.khat.p, dst, out_stride, mh,
+                                                   d.cout.p, cnt, grid, ups, st)
+                   : launch_4step_czt_fused<double>(f.lR, f.lC, x, complex_in ? 1 : 0, x_stride, N, cinp, yring, slots,
+                                                    delta, batch, f.twR, f.twC, f.twL, d.khat.p, dst, out_stride, mh,
+                                                    d.cout.p, cnt, grid, ups, st);
+    };
+    int grid = 0, ups = 0;
+    if (call(nullptr, nullptr, 1, 1, nullptr, 0, nullptr, &grid, &ups) != cudaSuccess || grid <= 0 || ups <= 0) {
+        cudaGetLastError();
+        return false;
+    }
+    const char* dx = std::getenv("SKG_4STEP_DELTA_X10");
+    const long long x10 = dx ? std::max(1, std::atoi(dx)) : 25;
+    const long long delta = std::max<long long>(1, (grid * x10 / 10 + ups - 1) / ups);
+    const long long slots = 2 * delta + (grid + ups - 1) / ups + 2;   // forward column start .. inverse column read
+    const size_t ring = (size_t)slots * (size_t)f.L * cs;
+    if (batch < slots || ring > (size_t{72} << 20)) return false;   // the ring has to stay L2 resident
+    Scratch Y(ring, st);
+    Scratch cnt((size_t)batch * 3 * sizeof(unsigned), st);
+    for (size_t sg = 0; sg < nseg_; ++sg) {
+        check(cudaMemsetAsync(cnt.p, 0, (size_t)batch * 3 * sizeof(unsigned), st), "czt fused counters");
+        void* dst = static_cast<char*>(out) + sg * seg_ * cs;
+        const void* cinp = static_cast<const char*>(d.cin.p) + sg * n_ * cs;
+        const long long mh = (long long)std::min(seg_, m_ - sg * seg_);
+        check(call(cinp, Y.p, (int)slots, (int)delta, dst, mh, static_cast<unsigned*>(cnt.p), nullptr, nullptr),
+              "czt 4step fused");
+        count_launch();
+    }
+    return true;
+}
+
 void CztPlanG::execute(const void* x, bool complex_in, long long x_stride, long long batch, void* out,
                        long long out_stride, bool f32, cudaStream_t st, size_t load_n) const {
     if (batch <= 0) return;
@@ -592,6 +635,10 @@ void CztPlanG::execute(const void* x, bool complex_in, long long x_stride, long 
         const size_t cs = f32 ? 8 : 16, es = complex_in ? cs : cs / 2;
         Scratch Y((size_t)std::min(ch, batch) * f.L * cs, st);
         const int kind = complex_in ? 3 : 2;
+        // one cooperative launch per segment with the work rows in an L2-resident ring (kernels_4step_czt.cuh);
+        // same unit arithmetic as the three launches below, which serve short batches, rings that would not
+        // fit in L2 and SKG_4STEP_FUSED=0
+        if (czt_4step_fused(FourStepRef{&f}, f32, x, complex_in, x_stride, N, d, batch, out, out_stride, st)) return;
         for (long long b0 = 0; b0 < batch; b0 += ch) {
             const long long nb = std::min(ch, batch - b0);
             const void* src = static_cast<const char*>(x) + (size_t)b0 * x_stride * es;

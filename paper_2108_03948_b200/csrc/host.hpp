@@ -97,6 +97,8 @@ int single_cta_max_log2(bool f32);
 void fft_c2c(size_t n, bool inverse, bool f32, const void* in, long long in_stride, void* out,
              long long out_stride, long long batch, cudaStream_t st);
 
+struct FourStepRef { const void* p; };   // host.cpp's four-step geometry, opaque here
+
 // Bluestein chirp-z plan (CztPlan, czt.cpp:85-137) with device tables
 class CztPlanG {
   public:
@@ -118,6 +120,9 @@ class CztPlanG {
         DevMem khat_sf, cout_sf;   // shared-forward tables (nseg > 1): per-block kernel spectra / out chirps
     };
     const Dev& dev(bool f32) const;
+    // multi-pass plans: the one-launch pipeline (kernels_4step_czt.cuh); false = not applicable
+    bool czt_4step_fused(const FourStepRef& f, bool f32, const void* x, bool complex_in, long long x_stride, long long N,
+                         const Dev& d, long long batch, void* out, long long out_stride, cudaStream_t st) const;
     size_t n_, m_, L_;
     size_t nseg_ = 1, seg_ = 0, Ls_ = 0;
     int log2L_;   // of Ls_

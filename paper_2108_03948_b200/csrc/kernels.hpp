@@ -89,6 +89,16 @@ cudaError_t launch_4step_rfused(int lg, const void* x, long long x_stride, long 
                                 int half, unsigned* col_done, unsigned* row_done, int* grid_out, cudaStream_t st);
 template <typename T> int launch_4step_rfused_ups(int lg);
 
+// multi-pass CZT in one cooperative persistent launch (kernels_4step_czt.cuh): forward column, row (Bluestein
+// middle) and inverse column units interleaved, work rows in a ring of `slots` traces; counters = 3 * batch
+// zeroed words; grid_out/ups_out != nullptr: only report the grid and the units per trace step.
+template <typename T>
+cudaError_t launch_4step_czt_fused(int lR, int lC, const void* x, int complex_in, long long x_stride, long long N,
+                                   const void* cin, void* Yring, int slots, int delta, long long batch, const void* twR,
+                                   const void* twC, const void* twL, const void* khat_p, void* out, long long out_stride,
+                                   long long M, const void* cout, unsigned* counters, int* grid_out, int* ups_out,
+                                   cudaStream_t st);
+
 // ---- fused Zoom FFT (kernels_zoom.cu) --------------------------------------------------
 constexpr int kZoomK = 4;   // FIR outputs per thread
 struct ZoomArgs {

@@ -25,6 +25,11 @@ namespace skg {
 #ifndef SKG_CZTF_MINB_F32
 #define SKG_CZTF_MINB_F32 3
 #endif
+// exchange barrier of a row transform under the row-major mapping: the NT threads of a row are a warp or
+// part of one (NT <= 32: __syncwarp), else a named barrier per row (ids 1.., 0 is __syncthreads)
+struct RowWarpSync {
+    __device__ __forceinline__ void operator()() const { __syncwarp(); }
+};
 template <typename T, int LR, int LC> struct CztFusedCfg {
     using GR = FftGeom<LR>;
     using GC = FftGeom<LC>;
@@ -152,11 +157,23 @@ k4_czt_fused(const void* __restrict__ xin, int complex_in, long long x_stride, l
             for (int q = 0; q < 16; ++q) v[q] = __ldcg(row + tb + GC::NT * q);
             const C* tl = twL + k1 * Cn;
             const C tw_a = __ldg(tl + tb), tw_s = __ldg(tl + GC::NT);
-            block_fft<false, LC>(v, smb, twsC, tb);
             const C* kp = khat_p + k1 * Cn;
+            // the kernel-spectrum row into L1 while the forward transform runs (an L2 round trip otherwise
+            // waited for between the two transforms)
+#pragma unroll
+            for (int q = 0; q < 16; ++q) prefetch_l1(kp + tb + GC::NT * q);
+            if constexpr (GC::NT <= 32) {
+                block_fft<false, LC, 16, 16, C, RowWarpSync>(v, smb, twsC, tb, true, RowWarpSync());
+            } else {
+                block_fft<false, LC, 16, 16, C, GroupSync>(v, smb, twsC, tb, true, GroupSync{1 + gb, GC::NT});
+            }
 #pragma unroll
             for (int q = 0; q < 16; ++q) v[q] = cmul(v[q], __ldg(kp + tb + GC::NT * q));
-            block_fft<true, LC>(v, smb, twsC, tb);
+            if constexpr (GC::NT <= 32) {
+                block_fft<true, LC, 16, 16, C, RowWarpSync>(v, smb, twsC, tb, true, RowWarpSync());
+            } else {
+                block_fft<true, LC, 16, 16, C, GroupSync>(v, smb, twsC, tb, true, GroupSync{1 + gb, GC::NT});
+            }
             twiddle_series(tw_a, tw_s, [&](int q, C w) { row[tb + GC::NT * q] = cmulc(v[q], w); });
             __syncwarp();
             if ((threadIdx.x & 31) == 0) red_release_inc(b_done + t);
@@ -165,6 +182,11 @@ k4_czt_fused(const void* __restrict__ xin, int complex_in, long long x_stride, l
             const long long n2 = (long long)idx * F::WA + g;
 #pragma unroll
             for (int q = 0; q < 16; ++q) v[q] = __ldcg(Yt + (tid + (long long)GR::NT * q) * Cn + n2);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {   // the output chirp into L1 while the transform runs
+                const long long n = (tid + (long long)GR::NT * q) * Cn + n2;
+                if (n < M && g % (128 / (int)sizeof(C)) == 0) prefetch_l1(cout + n);
+            }
             block_fft<true, LR>(v, sm, twsR, tid);
             // the first exchange of the transform consumed every load: the slot is free
             __syncwarp();

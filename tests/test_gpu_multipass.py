@@ -189,3 +189,43 @@ def test_real_fourstep_fused_ring(prec, L, b, variant, monkeypatch):
             assert rel_max_rows(got[i:i + 1], want) <= TOL_F64
         else:
             assert rel_l2_rows(got[i:i + 1], want) <= TOL_F32
+
+
+@pytest.mark.parametrize("variant", ["default", "short-lookahead", "small-grid"])
+@pytest.mark.parametrize("prec,n,m,b", [("f64", 3000, 12000, 200), ("f64", 16384, 16384, 100), ("f32", 16384, 16384, 200),
+                                        ("f32", 30000, 30000, 80), ("f32", 65536, 16384, 64), ("f64", 16384, 65536, 120),
+                                        ("f32", 65536, 262144, 48), ("f32", 200000, 20000, 16), ("f64", 300000, 100000, 10)])
+def test_czt_fourstep_fused_ring(prec, n, m, b, variant, monkeypatch):
+    """The one-launch multi-pass CZT (k4_czt_fused: forward column, Bluestein-middle row and inverse column
+    units interleaved in one persistent cooperative grid, work rows in an L2-resident ring) gives the
+    three-launch path's bits for every trace and the oracle's bins on the first / middle / last traces, for
+    square and 1:2 factorisations, with the default look-ahead, one so short that units block on their
+    producers, and a small grid."""
+    if variant == "short-lookahead":
+        monkeypatch.setenv("SKG_4STEP_DELTA_X10", "1")
+    dt = torch.float64 if prec == "f64" else torch.float32
+    x = W.sample_traces(b, n)
+    a, w = W.cfg2_czt_params(m)
+    xd = torch.from_numpy(x).to(dt).to(DEV)
+    xin = xd.cpu().double().numpy()
+    plan = sk.CztPlanGPU(n, a, w, m, sk.SKG_F64 if prec == "f64" else sk.SKG_F32)
+    monkeypatch.setenv("SKG_4STEP_FUSED", "0")
+    three = plan.execute(xd)   # (also builds the plan's device tables)
+    n0 = sk.launch_count()
+    three = plan.execute(xd)
+    n3 = sk.launch_count() - n0   # three launches per output segment
+    monkeypatch.setenv("SKG_4STEP_FUSED", "1")
+    with sk.grid_cap(61 if variant == "small-grid" else 0):
+        n0 = sk.launch_count()
+        one = plan.execute(xd)
+        assert 3 * (sk.launch_count() - n0) == n3, "the fused path did not run"
+        torch.cuda.synchronize()
+    assert torch.equal(one, three)
+    got = one.cpu().numpy()
+    oplan = O.CztPlan(n, a, w, m)
+    for i in (0, b // 2, b - 1):
+        want = oplan.batch_real(xin[i:i + 1])
+        if prec == "f64":
+            assert rel_max_rows(got[i:i + 1], want) <= TOL_F64
+        else:
+            assert rel_l2_rows(got[i:i + 1], want) <= TOL_F32
