@@ -154,6 +154,11 @@ cudaError_t launch_zoom_tfir(const ZoomArgs& a, bool f32, const void* x, long lo
 // natural-order taps as interleaved fp64 complex
 // fuse: the n_fft = 512 transform + band gather in the same launch (zoom_pcfir_fused_fits), output
 // straight to out; else the decimated rows to zb
+// raw-window whole-output FIR (kernels_zoom_rfir.cu): D in {4, 16}, 101 taps, untrimmed
+bool zoom_rfir_fits(const ZoomArgs& a, bool f32, const void* x, long long x_stride);
+cudaError_t launch_zoom_rfir(const ZoomArgs& a, bool f32, const void* x, long long xs, long long batch,
+                             const void* gnat_host, const void* gnat, const void* S, void* zb, long long z_stride,
+                             cudaStream_t st);
 bool zoom_pcfir_fits(const ZoomArgs& a, bool f32);
 bool zoom_pcfir_fused_fits(const ZoomArgs& a, bool f32, int log2n);
 cudaError_t launch_zoom_pcfir(const ZoomArgs& a, bool f32, const void* x, long long xs, long long batch,

@@ -1,0 +1,268 @@
+// kernels_zoom_rfir.cu — Zoom FFT FIR (filter_decimate / filter_decimate_circular, zoomfft.cpp:82-104)
+// for large decimations and ragged lengths: whole outputs per lane straight from a RAW (not polyphase)
+// window of the trace in shared memory.
+//
+// Same sum as the other FIR routes: u[m] = S[m] (sum_t g[t] x[mD - t] + wrap_m), complex taps
+// g[t] = h[t] e^{+i2pi fc t/fs} on real samples, samples outside [0, U) zero, the circular wrap terms of the
+// first outputs times e^{-i2pi fc U/fs}. The phase-lane FIR (kernels_zoom_fir.cuh) gives every lane one
+// polyphase row and sums the D partials of each output through shared memory: at D = 16 with 101 taps that
+// is 7 taps per lane per output against a 16-term cross-lane reduction — about 30 instructions per lane
+// per output for 14 useful FMAs (ncu: the fp32 FIR issue-bound at 62% issue / 23% warps, 2 TB/s on rows
+// the survey counts as HBM bound). Here:
+//   * a lane owns K consecutive outputs and sums ALL their taps (no partial sums cross lanes) from one
+//     contiguous window of (K - 1) D + T samples, read as 16-byte units; the window's units and the tap of
+//     every (sample, output) pair are compile-time, taps are constant-bank operands of the FMA
+//     (__grid_constant__ parameter block): ~2 K T FMAs + ((K - 1) D + T) / EU loads per lane per item;
+//   * a warp item = 32 K outputs of one record; its samples are copied global -> shared with 16-byte
+//     cp.async into the raw order plus one pad unit per lane stride K D (the lanes' window bases then sit
+//     an odd number of units apart: conflict-free LDS.128), double-buffered per warp where it fits; no
+//     barriers beyond the warp, any nout (ragged last item), any U (units straddling the record's ends are
+//     filled per element).
+// Geometry: trim = 0; (D, T, K) specialised below (the configs[4] sweep: D in {4, 16},
+// 101 taps). Output: decimated rows zb for k_zoom_fftband.
+#include "bulk_copy.cuh"
+#include "fft_device.cuh"
+#include "kernels.hpp"
+#include "kernels_impl.cuh"
+
+#include <utility>
+
+namespace skg {
+
+namespace {
+
+template <typename T, int NTAPS> struct RfTaps {
+    cx_t<T> g[NTAPS];   // natural order g[t]
+};
+
+template <typename T, int D, int NTAPS, int K> struct RfGeom {
+    static constexpr int EU = 16 / (int)sizeof(T);                 // elements per 16-byte unit
+    static constexpr int LS = K * D;                                 // lane stride (samples)
+    static constexpr int PART = 32 * K;                              // outputs per warp item
+    static constexpr int PADL = (NTAPS - 1 + LS - 1) / LS * LS;      // samples before the item's first output sample
+    static constexpr int SPAN = PADL + PART * D;                     // samples per item buffer (raw)
+    static constexpr int UNITS = SPAN / EU;                          // 16-byte units per item
+    static constexpr int LSP = LS + EU;                              // padded lane stride
+    static constexpr int BUF = (SPAN / LS) * LSP;                    // padded elements per item buffer
+    static constexpr int W0 = (PADL - (NTAPS - 1)) / EU * EU;        // window start relative to the lane base
+    static constexpr int W1 = PADL + (K - 1) * D + 1;                // window end (exclusive)
+    static constexpr int WU = (W1 - W0 + EU - 1) / EU;               // window units
+    static_assert(LS % EU == 0 && (LS / EU) % 2 == 0, "lane stride: an even number of units (odd once padded)");
+    __host__ __device__ static constexpr int pidx(int j) { return j + (j / LS) * EU; }
+};
+
+__device__ __forceinline__ void unit_elems(const float4& v, float (&e)[4]) {
+    e[0] = v.x, e[1] = v.y, e[2] = v.z, e[3] = v.w;
+}
+__device__ __forceinline__ void unit_elems(const double2& v, double (&e)[2]) { e[0] = v.x, e[1] = v.y; }
+
+#ifndef SKG_RFIR_WARPS
+#define SKG_RFIR_WARPS 4
+#endif
+template <typename T> __host__ __device__ constexpr int rf_nbuf() { return sizeof(T) == 8 ? 1 : 2; }
+
+template <typename T, int D, int NTAPS, int K>
+__global__ void __launch_bounds__(SKG_RFIR_WARPS * 32)
+k_zoom_rfir(const T* __restrict__ x, long long x_stride, unsigned batch, int aligned, ZoomArgs a,
+            const __grid_constant__ RfTaps<T, NTAPS> tp, const cx_t<T>* __restrict__ S, cx_t<T>* __restrict__ zb,
+            long long z_stride) {
+    using C = cx_t<T>;
+    using RG = RfGeom<T, D, NTAPS, K>;
+    constexpr int EU = RG::EU;
+    constexpr int NBUF = rf_nbuf<T>();
+    constexpr int WT = NTAPS - 1;                 // wrap samples x[U - s], s = 1..T-1
+    constexpr int WTU = (WT + EU - 1) / EU;       // as 16-byte units (the tail starts unit aligned: U, T - 1 are)
+    static_assert(WT % EU == 0, "tail of whole units");
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    // [taps g[t] (wrap terms' lane-varying reads)][per warp: NBUF x (item buffer + tail)]
+    C* s_g = reinterpret_cast<C*>(smraw);
+    constexpr int GB = (NTAPS * (int)sizeof(C) + 15) / 16 * 16;
+    constexpr int SLOT = RG::BUF + WTU * EU;      // elements per buffer slot
+    T* bufs = reinterpret_cast<T*>(smraw + GB) + (size_t)warp * NBUF * SLOT;
+    for (int i = threadIdx.x; i < NTAPS; i += blockDim.x) s_g[i] = tp.g[i];
+    __syncthreads();
+    const int U = (int)a.U;
+    const unsigned parts = (unsigned)(a.nout + RG::PART - 1) / RG::PART;
+    const unsigned nitem = batch * parts;   // < 2^31 (checked by the launcher)
+    const unsigned w0 = blockIdx.x * SKG_RFIR_WARPS + warp, wstride = gridDim.x * SKG_RFIR_WARPS;
+    const bool wrap = a.circular && a.mwrap > 0;
+    // fill: unit un of the item covers samples i0 + un EU .. + EU - 1, i0 = p PART D - PADL
+    auto fill = [&](unsigned item, int slot) {
+        const unsigned b = item / parts;
+        const int p = (int)(item - b * parts);
+        const int i0 = p * RG::PART * D - RG::PADL;
+        const T* xr = x + (long long)b * x_stride;
+        T* dst = bufs + slot * SLOT;
+#pragma unroll
+        for (int uu = 0; uu < (RG::UNITS + 31) / 32; ++uu) {
+            const int un = lane + 32 * uu;
+            if (RG::UNITS % 32 == 0 || un < RG::UNITS) {
+                const int j = un * EU, i = i0 + j;
+                T* d = dst + RG::pidx(j);
+                if (aligned && i >= 0 && i + EU <= U) {
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(d)), "l"(xr + i) : "memory");
+                } else {   // the record's ends, or rows that are not 16-byte aligned: element copies
+#pragma unroll
+                    for (int e = 0; e < EU; ++e) {
+                        if (i + e >= 0 && i + e < U) cp_async_el(d + e, xr + i + e, true);
+                        else d[e] = (T)0;
+                    }
+                }
+            }
+        }
+        if (p == 0 && wrap) {   // the record's last T - 1 samples, for the wrapped terms
+#pragma unroll
+            for (int k = lane; k < WTU; k += 32) {
+                if (aligned) {
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + RG::BUF + k * EU)),
+                                 "l"(xr + U - WT + k * EU)
+                                 : "memory");
+                } else {
+#pragma unroll
+                    for (int e = 0; e < EU; ++e) cp_async_el(dst + RG::BUF + k * EU + e, xr + U - WT + k * EU + e, true);
+                }
+            }
+        }
+        cp_async_commit();
+    };
+    static_assert(WTU <= 64, "tail units");
+    if (NBUF == 2 && w0 < nitem) fill(w0, 0);
+    int slot = 0;
+    for (unsigned item = w0; item < nitem; item += wstride) {
+        if (NBUF == 1) {
+            fill(item, 0);
+            cp_async_wait_all();
+        } else if (item + wstride < nitem) {
+            fill(item + wstride, slot ^ 1);
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            cp_async_wait_all();
+        }
+        __syncwarp();
+        const unsigned b = item / parts;
+        const int p = (int)(item - b * parts);
+        const T* wl = bufs + slot * SLOT + lane * RG::LSP;
+        C acc[K];
+#pragma unroll
+        for (int c = 0; c < K; ++c) acc[c] = czero<C>();
+        using VT = typename std::conditional<sizeof(T) == 8, double2, float4>::type;
+        // the lane's window, unit by unit: sample at relative position r = W0 + u EU + e feeds output c
+        // with tap t = PADL + c D - r (when 0 <= t < T); everything but the lane base is compile-time
+#pragma unroll
+        for (int u = 0; u < RG::WU; ++u) {
+            const int r0 = RG::W0 + u * EU;
+            const VT v = *reinterpret_cast<const VT*>(wl + RG::pidx(r0));
+            T e[EU];   // registers (no address taken)
+            unit_elems(v, e);
+#pragma unroll
+            for (int k2 = 0; k2 < EU; ++k2) {
+                const int r = r0 + k2;
+#pragma unroll
+                for (int c = 0; c < K; ++c) {
+                    const int t = RG::PADL + c * D - r;
+                    if (t >= 0 && t < NTAPS) {
+                        const C g = tp.g[t];
+                        acc[c].x = fma(g.x, e[k2], acc[c].x);
+                        acc[c].y = fma(g.y, e[k2], acc[c].y);
+                    }
+                }
+            }
+        }
+        const int mb = p * RG::PART + lane * K;
+        if (p == 0 && wrap) {
+            // wrapped terms cw[m] = w sum_{s=1}^{T-1-mD} g[mD + s] x[U - s], m < mwrap, from the staged tail
+            // (x[U - s] = tail[T - 1 - s]): lane i sums a quarter of output mw + i / 4, then the owner lane
+            // (m / K) collects them
+            const T* tail = bufs + slot * SLOT + RG::BUF;
+            for (int mw = 0; mw < a.mwrap; mw += 8) {
+                const int m = mw + (lane >> 2), q = lane & 3;
+                C v = czero<C>();
+                if (m < a.mwrap) {
+                    C v2 = czero<C>();   // two chains
+                    int s1 = 1 + q;
+                    for (; s1 + 4 <= WT - m * D; s1 += 8) {
+                        v = cadd(v, rmul(tail[WT - s1], s_g[m * D + s1]));
+                        v2 = cadd(v2, rmul(tail[WT - s1 - 4], s_g[m * D + s1 + 4]));
+                    }
+                    if (s1 <= WT - m * D) v = cadd(v, rmul(tail[WT - s1], s_g[m * D + s1]));
+                    v = cadd(v, v2);
+                }
+                v.x += __shfl_xor_sync(0xffffffffu, v.x, 1);
+                v.y += __shfl_xor_sync(0xffffffffu, v.y, 1);
+                v.x += __shfl_xor_sync(0xffffffffu, v.x, 2);
+                v.y += __shfl_xor_sync(0xffffffffu, v.y, 2);
+                v = cmul(v, mk<C>((T)a.wre, (T)a.wim));
+#pragma unroll
+                for (int c = 0; c < K; ++c) {
+                    // output mb + c of this lane takes lane 4 (mb + c - mw) when that is in range
+                    const int src = 4 * (mb + c - mw);
+                    C got;
+                    got.x = __shfl_sync(0xffffffffu, v.x, src & 31);
+                    got.y = __shfl_sync(0xffffffffu, v.y, src & 31);
+                    const T f = (T)(src >= 0 && src < 32 && mb + c < a.mwrap);   // arithmetic select: acc stays in registers
+                    acc[c].x = fma(f, got.x, acc[c].x);
+                    acc[c].y = fma(f, got.y, acc[c].y);
+                }
+            }
+        }
+        C* zr = zb + (long long)b * z_stride + mb;
+#pragma unroll
+        for (int c = 0; c < K; ++c)
+            if (mb + c < a.nout) zr[c] = cmul(acc[c], __ldg(S + mb + c));
+        __syncwarp();   // the buffer is refilled by a later item
+        if (NBUF == 2) slot ^= 1;
+    }
+}
+
+template <typename T, int D, int NTAPS, int K>
+cudaError_t run_rfir(const ZoomArgs& a, const T* x, long long xs, long long batch, const void* gnat_host,
+                     const void* S, void* zb, long long z_stride, cudaStream_t st) {
+    using C = cx_t<T>;
+    using RG = RfGeom<T, D, NTAPS, K>;
+    RfTaps<T, NTAPS> tp;
+    const double* gh = static_cast<const double*>(gnat_host);   // fp64 natural-order taps (re, im pairs)
+    for (int t = 0; t < NTAPS; ++t) {
+        tp.g[t].x = (T)gh[2 * t];
+        tp.g[t].y = (T)gh[2 * t + 1];
+    }
+    constexpr int EU = RG::EU;
+    const size_t smem = (NTAPS * sizeof(C) + 15) / 16 * 16 +
+                        (size_t)SKG_RFIR_WARPS * rf_nbuf<T>() * (RG::BUF + (NTAPS - 1 + EU - 1) / EU * EU) * sizeof(T);
+    auto kern = k_zoom_rfir<T, D, NTAPS, K>;
+    cudaError_t e = prep_smem(kern, smem);
+    if (e != cudaSuccess) return e;
+    const long long parts = (a.nout + RG::PART - 1) / RG::PART;
+    if (batch * parts >= (1LL << 31)) return cudaErrorNotSupported;
+    // 16-byte copies need aligned rows (and, for the wrap tail, U a whole number of units); otherwise the
+    // same kernel copies element by element — the route, and so the bits, do not depend on the alignment
+    const int aligned = reinterpret_cast<uintptr_t>(x) % 16 == 0 && xs % EU == 0 && a.U % EU == 0;
+    const unsigned grid = persistent_grid(kern, SKG_RFIR_WARPS * 32, smem, (batch * parts + SKG_RFIR_WARPS - 1) / SKG_RFIR_WARPS);
+    kern<<<grid, SKG_RFIR_WARPS * 32, smem, st>>>(x, xs, (unsigned)batch, aligned, a, tp, (const C*)S, (C*)zb, z_stride);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+// raw-window whole-output FIR: specialised (D, T)
+bool zoom_rfir_fits(const ZoomArgs& a, bool f32, const void* x, long long x_stride) {
+    const bool off = std::getenv("SKG_ZOOM_NO_RFIR") != nullptr;   // read per call: tests switch routes in-process
+    if (off || a.trim != 0 || a.T != 101 || (a.D != 16 && a.D != 4)) return false;
+    (void)f32, (void)x, (void)x_stride;
+    return a.U <= a.n && a.U >= a.T;
+}
+
+cudaError_t launch_zoom_rfir(const ZoomArgs& a, bool f32, const void* x, long long xs, long long batch,
+                             const void* gnat_host, const void* gnat, const void* S, void* zb, long long z_stride,
+                             cudaStream_t st) {
+    auto go = [&](auto tag) -> cudaError_t {
+        using T = decltype(tag);
+        const T* xt = static_cast<const T*>(x);
+        if (a.D == 16) return run_rfir<T, 16, 101, 2>(a, xt, xs, batch, gnat_host, S, zb, z_stride, st);
+        if (a.D == 4) return run_rfir<T, 4, 101, 8>(a, xt, xs, batch, gnat_host, S, zb, z_stride, st);
+        return cudaErrorNotSupported;
+    };
+    return f32 ? go(float{}) : go(double{});
+}
+
+}  // namespace skg

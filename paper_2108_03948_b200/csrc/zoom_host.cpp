@@ -243,8 +243,10 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
     }
     // split route FIR: the TMA-fed phase-lane FIR where it fits (fp64 cfg3 n_fft 2048: 0.111 ms against
     // 0.120 for the whole-output FIR + separate transform), else the whole-output FIR
-    const bool tfir = zoom_tfir_fits(a, f32, x, x_stride);
-    const bool pcfir = !tfir && zoom_pcfir_fits(a, f32);
+    // D in {4, 16} with 101 taps: whole outputs per lane from a raw shared-memory window (kernels_zoom_rfir.cu)
+    const bool rfir = zoom_rfir_fits(a, f32, x, x_stride);
+    const bool tfir = !rfir && zoom_tfir_fits(a, f32, x, x_stride);
+    const bool pcfir = !rfir && !tfir && zoom_pcfir_fits(a, f32);
     if (!force && !split_only && zoom_pcfir_fused_fits(a, f32, lg)) {
         // whole-output FIR + 512-point transform + band in one launch (kernels_zoom_pcfir.cu)
         check(launch_zoom_pcfir(a, f32, x, x_stride, batch, d.gnh.data(), d.sdec.p, nullptr, 0, true,
@@ -253,7 +255,7 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
         count_launch();
         return;
     }
-    if (single && pfir && !tfir && !pcfir && !force && !split_only) {
+    if (single && pfir && !rfir && !tfir && !pcfir && !force && !split_only) {
         // FIR and short FFT in one kernel where instantiated (configs[2] geometry)
         const cudaError_t e = launch_zoom_pfir_fft(a, zoom_pfir_lh(a), lg, f32, x, x_stride, batch, d.g.p, d.gn.p,
                                                    d.sdec.p, stockham_twiddles(lg, f32), (int)k_lo, (int)bins(),
@@ -264,7 +266,7 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
             return;
         }
     }
-    if (single && (pcfir || tfir || wfir || pfir || cfir) && !force) {
+    if (single && (rfir || pcfir || tfir || wfir || pfir || cfir) && !force) {
         // warp-chunk FIR -> work rows (L2-resident chunk of records) -> FFT + band gather
         const size_t cs = f32 ? 8 : 16, es = f32 ? 4 : 8;
         const long long zrow = a.nout;
@@ -279,7 +281,9 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
             // phase-lane FIR where it exists (power-of-two D <= 16), else the constant-bank FIR for the
             // specialised (D, T) pairs, else the warp-window FIR (all three measured within a few
             // percent of each other on cfg3)
-            if (pcfir)
+            if (rfir)
+                check(launch_zoom_rfir(a, f32, xb, x_stride, nb, d.gnh.data(), d.gn.p, d.sdec.p, zb, zrow, st), "zoom fir");
+            else if (pcfir)
                 check(launch_zoom_pcfir(a, f32, xb, x_stride, nb, d.gnh.data(), d.sdec.p, zb, zrow, false, nullptr,
                                         nullptr, nullptr, 0, st),
                       "zoom fir");

@@ -225,3 +225,40 @@ def test_zoom_decimation_sweep(prec, D):
         assert rel_max_rows(got, want) <= TOL_F64
     else:
         assert rel_l2_rows(got, want) <= TOL_F32
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("D", [4, 16])
+@pytest.mark.parametrize("n", [1000, 1024, 3000, 4096, 16384, 2000, 517])
+def test_raw_window_fir_route(prec, D, n, monkeypatch):
+    """configs[4] zoom geometry (101 taps, D in {4, 16}, circular): the whole-output FIR over a raw
+    shared-memory window (kernels_zoom_rfir.cu) against the oracle on every row of a ragged batch — items
+    whose windows start before the record, end past its usable length, a ragged last item, the circular
+    wrap terms — and against the phase-lane / constant-bank routes it replaces (SKG_ZOOM_NO_RFIR=1),
+    including strided rows and a circular=0 plan of the same geometry."""
+    P = sk.SKG_F64 if prec == "f64" else sk.SKG_F32
+    b = 77
+    x = W.sample_traces(b, n)
+    xd = _dev(x, prec)
+    xin = xd.cpu().double().numpy()
+    for circ in (1, 0):
+        plan = sk.ZoomPlanGPU(n, 0.4e12, 1.2e12, W.FS, P, decimation=D, circular=circ)
+        ref = O.ZoomPlan(n, 0.4e12, 1.2e12, W.FS, decimation=D, circular=circ)
+        want = [ref(r)[0] for r in xin]
+        got = plan.execute(xd).cpu().numpy()
+        monkeypatch.setenv("SKG_ZOOM_NO_RFIR", "1")
+        old = plan.execute(xd).cpu().numpy()
+        monkeypatch.delenv("SKG_ZOOM_NO_RFIR")
+        xs = torch.zeros((b, n + 12), dtype=xd.dtype, device=DEV)   # strided rows, 16-byte aligned
+        xs[:, :n] = xd
+        got_s = plan.execute(xs[:, :n]).cpu().numpy()
+        xu = torch.zeros((b, n + 13), dtype=xd.dtype, device=DEV)   # odd stride: the element-copy fill
+        xu[:, :n] = xd
+        np.testing.assert_array_equal(plan.execute(xu[:, :n]).cpu().numpy(), got)
+        if prec == "f64":
+            assert rel_max_rows(got, want) <= TOL_F64, (n, D, circ)
+            assert rel_max_rows(old, want) <= TOL_F64
+        else:
+            assert rel_l2_rows(got, want) <= TOL_F32, (n, D, circ)
+            assert rel_l2_rows(old, want) <= TOL_F32
+        np.testing.assert_array_equal(got_s, got)
