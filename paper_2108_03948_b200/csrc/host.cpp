@@ -374,12 +374,12 @@ bool r2c_4step_fused(const FourStep& f, const void* in, long long in_stride, lon
     const char* e = std::getenv("SKG_4STEP_FUSED");
     if (e && e[0] == '0') return false;
     if (f.lR != f.lC || f.lR < 8 || f.lR > 9) return false;
-    const int ups = launch_4step_rfused_ups<T>(f.lR);
-    if (ups <= 0) return false;
-    int grid = 0;
+    int grid = 0, ups = 0;
     if (launch_4step_rfused<T>(f.lR, in, in_stride, N, nullptr, 1, 1, batch, f.twR, f.twL, out, out_stride, layout,
-                               nullptr, nullptr, &grid, st) != cudaSuccess || grid <= 0)
+                               nullptr, nullptr, &grid, &ups, st) != cudaSuccess || grid <= 0 || ups <= 0) {
+        cudaGetLastError();
         return false;
+    }
     const char* dx = std::getenv("SKG_4STEP_DELTA_X10");
     const long long x10 = dx ? std::max(1, std::atoi(dx)) : 25;
     const long long delta = std::max<long long>(2, (grid * x10 / 10 + ups - 1) / ups);
@@ -393,7 +393,7 @@ bool r2c_4step_fused(const FourStep& f, const void* in, long long in_stride, lon
     check(cudaMemsetAsync(cnt.p, 0, (size_t)batch * 2 * sizeof(unsigned), st), "4step fused counters");
     unsigned* col_done = static_cast<unsigned*>(cnt.p);
     check(launch_4step_rfused<T>(f.lR, in, in_stride, N, Y.p, (int)slots, (int)delta, batch, f.twR, f.twL, out,
-                                 out_stride, layout, col_done, col_done + batch, nullptr, st),
+                                 out_stride, layout, col_done, col_done + batch, nullptr, nullptr, st),
           "4step real fused");
     count_launch();
     return true;

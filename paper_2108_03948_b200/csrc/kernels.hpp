@@ -82,12 +82,12 @@ cudaError_t launch_4step_rowh(int log2C, const void* Y, int log2R, long long bat
                               long long out_stride, int half, cudaStream_t st);
 
 // both passes in one cooperative persistent launch, work rows in a ring of `slots` traces (square R = C = 2^lg);
-// grid_out != nullptr: only report the grid the launch would use. ups: units per trace step.
+// grid_out / ups_out != nullptr: only report the grid the launch would use and the units per trace step.
 template <typename T>
 cudaError_t launch_4step_rfused(int lg, const void* x, long long x_stride, long long N, void* Yring, int slots, int delta,
                                 long long batch, const void* tw, const void* twL, void* out, long long out_stride,
-                                int half, unsigned* col_done, unsigned* row_done, int* grid_out, cudaStream_t st);
-template <typename T> int launch_4step_rfused_ups(int lg);
+                                int half, unsigned* col_done, unsigned* row_done, int* grid_out, int* ups_out,
+                                cudaStream_t st);
 
 // multi-pass CZT in one cooperative persistent launch (kernels_4step_czt.cuh): forward column, row (Bluestein
 // middle) and inverse column units interleaved, work rows in a ring of `slots` traces; counters = 3 * batch

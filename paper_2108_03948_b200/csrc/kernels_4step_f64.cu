@@ -37,10 +37,9 @@ template <>
 cudaError_t launch_4step_rfused<double>(int lg, const void* x, long long x_stride, long long N, void* Yring, int slots,
                                      int delta, long long batch, const void* tw, const void* twL, void* out,
                                      long long out_stride, int half, unsigned* col_done, unsigned* row_done,
-                                     int* grid_out, cudaStream_t st) {
+                                     int* grid_out, int* ups_out, cudaStream_t st) {
     return launch_4step_rfused_impl<double>(lg, x, x_stride, N, Yring, slots, delta, batch, tw, twL, out, out_stride, half,
-                                         col_done, row_done, grid_out, st);
+                                         col_done, row_done, grid_out, ups_out, st);
 }
-template <> int launch_4step_rfused_ups<double>(int lg) { return fused_units_per_step<double>(lg); }
 
 }  // namespace skg

@@ -523,7 +523,7 @@ template <typename T>
 cudaError_t launch_4step_rfused_impl(int lg, const void* x, long long x_stride, long long N, void* Yring, int slots,
                                      int delta, long long batch, const void* tw, const void* twL, void* out,
                                      long long out_stride, int half, unsigned* col_done, unsigned* row_done,
-                                     int* grid_out, cudaStream_t st) {
+                                     int* grid_out, int* ups_out, cudaStream_t st) {
     using C = cx_t<T>;
     return dispatch_log2<8, 9>(lg, [&](auto lgc) {
         constexpr int LG = decltype(lgc)::value;
@@ -539,6 +539,7 @@ cudaError_t launch_4step_rfused_impl(int lg, const void* x, long long x_stride, 
                 const unsigned grid = persistent_grid(kern, F::BLOCK, F::SMEM, 1LL << 40);
                 if (grid_out) {   // sizing query: the grid the launch will use
                     *grid_out = (int)grid;
+                    if (ups_out) *ups_out = F::UPS;
                     return cudaSuccess;
                 }
                 const T* xp = (const T*)x;
@@ -556,15 +557,6 @@ cudaError_t launch_4step_rfused_impl(int lg, const void* x, long long x_stride, 
             return launch(k4_rfused<T, LG, 16>);
         }
     });
-}
-
-template <typename T> int fused_units_per_step(int lg) {
-    int v = 0;
-    dispatch_log2<8, 9>(lg, [&](auto lgc) {
-        v = FusedCfg<T, decltype(lgc)::value>::UPS;
-        return cudaSuccess;
-    });
-    return v;
 }
 
 }  // namespace skg
