@@ -317,7 +317,10 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
         void* zb = nullptr;
         zb = stream_alloc((size_t)batch * n_fft * cs, st);
         check(cudaMemsetAsync(zb, 0, (size_t)batch * n_fft * cs, st), "memset");
-        if (wfir)
+        if (rfir)
+            check(launch_zoom_rfir(a, f32, x, x_stride, batch, d.gnh.data(), d.gn.p, d.sdec.p, zb, (long long)n_fft, st),
+                  "zoom fir");
+        else if (wfir)
             check(launch_zoom_wfir(a, f32, x, x_stride, batch, d.g.p, d.sdec.p, zb, (long long)n_fft, st), "zoom fir");
         else
             check(launch_zoom_fir(c, f32, x, x_stride, batch, d.g.p, d.sdec.p, zb, (long long)n_fft, st), "zoom fir");

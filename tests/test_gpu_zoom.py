@@ -100,7 +100,7 @@ def test_even_tap_extension_vs_oracle():
 
 @pytest.mark.parametrize("prec", ["f64", "f32"])
 @pytest.mark.parametrize("n,D", [(1000, 4), (1000, 16), (1024, 4), (1024, 16), (3000, 4), (3000, 16), (4096, 4),
-                                 (4096, 16), (16384, 16)])
+                                 (4096, 16), (16384, 4), (16384, 16), (65536, 4), (65536, 16)])
 def test_cfg5_zoom_rows(prec, n, D):
     """configs[4] zoom rows: band [0.4, 1.2] THz (§9 D3), default 101 taps and cutoff."""
     x = W.sample_traces(4, n)
