@@ -247,7 +247,9 @@ cudaError_t run_rfir(const ZoomArgs& a, const T* x, long long xs, long long batc
 // raw-window whole-output FIR: specialised (D, T)
 bool zoom_rfir_fits(const ZoomArgs& a, bool f32, const void* x, long long x_stride) {
     const bool off = std::getenv("SKG_ZOOM_NO_RFIR") != nullptr;   // read per call: tests switch routes in-process
-    if (off || a.trim != 0 || a.T != 101 || (a.D != 16 && a.D != 4)) return false;
+    if (off || a.trim != 0) return false;
+    const int key = a.D * 1000 + a.T;
+    if (key != 16101 && key != 4101 && key != 8065 && key != 8101) return false;
     (void)f32, (void)x, (void)x_stride;
     return a.U <= a.n && a.U >= a.T;
 }
@@ -258,9 +260,13 @@ cudaError_t launch_zoom_rfir(const ZoomArgs& a, bool f32, const void* x, long lo
     auto go = [&](auto tag) -> cudaError_t {
         using T = decltype(tag);
         const T* xt = static_cast<const T*>(x);
-        if (a.D == 16) return run_rfir<T, 16, 101, 2>(a, xt, xs, batch, gnat_host, S, zb, z_stride, st);
-        if (a.D == 4) return run_rfir<T, 4, 101, 8>(a, xt, xs, batch, gnat_host, S, zb, z_stride, st);
-        return cudaErrorNotSupported;
+        switch (a.D * 1000 + a.T) {
+            case 16101: return run_rfir<T, 16, 101, 2>(a, xt, xs, batch, gnat_host, S, zb, z_stride, st);
+            case 4101: return run_rfir<T, 4, 101, 8>(a, xt, xs, batch, gnat_host, S, zb, z_stride, st);
+            case 8065: return run_rfir<T, 8, 65, 4>(a, xt, xs, batch, gnat_host, S, zb, z_stride, st);
+            case 8101: return run_rfir<T, 8, 101, 4>(a, xt, xs, batch, gnat_host, S, zb, z_stride, st);
+            default: return cudaErrorNotSupported;
+        }
     };
     return f32 ? go(float{}) : go(double{});
 }

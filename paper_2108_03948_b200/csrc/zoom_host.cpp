@@ -316,7 +316,11 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
         const size_t cs = f32 ? 8 : 16;
         void* zb = nullptr;
         zb = stream_alloc((size_t)batch * n_fft * cs, st);
-        check(cudaMemsetAsync(zb, 0, (size_t)batch * n_fft * cs, st), "memset");
+        // the FIR writes the first nout values of every row: only the zero padding behind them is cleared
+        if ((size_t)a.nout < n_fft)
+            check(cudaMemset2DAsync(static_cast<char*>(zb) + (size_t)a.nout * cs, n_fft * cs, 0,
+                                    (n_fft - (size_t)a.nout) * cs, (size_t)batch, st),
+                  "memset");
         if (rfir)
             check(launch_zoom_rfir(a, f32, x, x_stride, batch, d.gnh.data(), d.gn.p, d.sdec.p, zb, (long long)n_fft, st),
                   "zoom fir");
