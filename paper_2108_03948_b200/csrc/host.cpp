@@ -392,9 +392,11 @@ bool r2c_4step_fused(const FourStep& f, const void* in, long long in_stride, lon
     Scratch cnt((size_t)batch * 2 * sizeof(unsigned), st);
     check(cudaMemsetAsync(cnt.p, 0, (size_t)batch * 2 * sizeof(unsigned), st), "4step fused counters");
     unsigned* col_done = static_cast<unsigned*>(cnt.p);
-    check(launch_4step_rfused<T>(f.lR, in, in_stride, N, Y.p, (int)slots, (int)delta, batch, f.twR, f.twL, out,
-                                 out_stride, layout, col_done, col_done + batch, nullptr, nullptr, st),
-          "4step real fused");
+    if (launch_4step_rfused<T>(f.lR, in, in_stride, N, Y.p, (int)slots, (int)delta, batch, f.twR, f.twL, out, out_stride,
+                               layout, col_done, col_done + batch, nullptr, nullptr, st) != cudaSuccess) {
+        cudaGetLastError();   // no cooperative launch here (e.g. the grid cannot be co-resident): the two launches
+        return false;
+    }
     count_launch();
     return true;
 }
@@ -617,8 +619,12 @@ bool CztPlanG::czt_4step_fused(const FourStepRef& fr, bool f32, const void* x, b
         void* dst = static_cast<char*>(out) + sg * seg_ * cs;
         const void* cinp = static_cast<const char*>(d.cin.p) + sg * n_ * cs;
         const long long mh = (long long)std::min(seg_, m_ - sg * seg_);
-        check(call(cinp, Y.p, (int)slots, (int)delta, dst, mh, static_cast<unsigned*>(cnt.p), nullptr, nullptr),
-              "czt 4step fused");
+        if (call(cinp, Y.p, (int)slots, (int)delta, dst, mh, static_cast<unsigned*>(cnt.p), nullptr, nullptr) !=
+            cudaSuccess) {
+            cudaGetLastError();
+            if (sg == 0) return false;   // no cooperative launch here: the three launches
+            throw std::runtime_error("czt 4step fused: launch failed");
+        }
         count_launch();
     }
     return true;

@@ -182,6 +182,14 @@ def test_real_fourstep_fused_ring(prec, L, b, variant, monkeypatch):
         torch.cuda.synchronize()
     assert torch.equal(one, two)
     assert torch.equal(one_half, two_half)
+    # strided output rows with a canary in the gaps, strided (odd: unaligned pairs) input rows with poison
+    canary = complex(7.5, -3.25)
+    buf = torch.full((b, L + 5), canary, dtype=one.dtype, device=DEV)
+    xs = torch.full((b, n + 3), float("nan"), dtype=dt, device=DEV)
+    xs[:, :n] = xd
+    sk.fft_spectrum_batch(xs[:, :n], L, out=buf[:, :L])
+    torch.cuda.synchronize()
+    assert torch.equal(buf[:, :L], two) and bool((buf[:, L:] == canary).all())
     got = one.cpu().numpy()
     for i in (0, b // 2, b - 1):
         want = O.fft_spectrum_batch(xin[i:i + 1], L)
@@ -221,6 +229,13 @@ def test_czt_fourstep_fused_ring(prec, n, m, b, variant, monkeypatch):
         assert 3 * (sk.launch_count() - n0) == n3, "the fused path did not run"
         torch.cuda.synchronize()
     assert torch.equal(one, three)
+    canary = complex(7.5, -3.25)
+    buf = torch.full((b, m + 3), canary, dtype=one.dtype, device=DEV)
+    xs = torch.full((b, n + 3), float("nan"), dtype=dt, device=DEV)
+    xs[:, :n] = xd
+    plan.execute(xs[:, :n], out=buf[:, :m])
+    torch.cuda.synchronize()
+    assert torch.equal(buf[:, :m], three) and bool((buf[:, m:] == canary).all())
     got = one.cpu().numpy()
     oplan = O.CztPlan(n, a, w, m)
     for i in (0, b // 2, b - 1):

@@ -1,4 +1,2 @@
-SKG_ZOOM_NO_FUSE=1 python tools/zoom_time.py 30
-M=gpu__time_duration.sum
-SKG_ZOOM_NO_FUSE=1 ncu --metrics $M --clock-control none -k regex:zoom --csv --log-file gpurun_out/r12_zoom_nofuse.csv python tools/zoom_time.py 2 > /dev/null 2>&1
-grep -v "^==" gpurun_out/r12_zoom_nofuse.csv | awk -F'","' '{print $5, $(NF)}' | tail -16
+timeout 1800 python -m pytest tests -x -q -m gpu 2>&1 | tail -4
+python bench.py > gpurun_out/r2_bench_late2.json 2> gpurun_out/r2_bench_late2.err; tail -c 300 gpurun_out/r2_bench_late2.err
