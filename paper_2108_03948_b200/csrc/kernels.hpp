@@ -159,6 +159,10 @@ bool zoom_rfir_fits(const ZoomArgs& a, bool f32, const void* x, long long x_stri
 cudaError_t launch_zoom_rfir(const ZoomArgs& a, bool f32, const void* x, long long xs, long long batch,
                              const void* gnat_host, const void* gnat, const void* S, void* zb, long long z_stride,
                              cudaStream_t st);
+bool zoom_rfir_fft_fits(const ZoomArgs& a, bool f32, int log2n);
+cudaError_t launch_zoom_rfir_fft(const ZoomArgs& a, bool f32, int log2n, const void* x, long long xs, long long batch,
+                                 const void* gnat_host, const void* S, const void* tw, const void* band, void* out,
+                                 long long out_stride, cudaStream_t st);
 bool zoom_pcfir_fits(const ZoomArgs& a, bool f32);
 bool zoom_pcfir_fused_fits(const ZoomArgs& a, bool f32, int log2n);
 cudaError_t launch_zoom_pcfir(const ZoomArgs& a, bool f32, const void* x, long long xs, long long batch,

@@ -255,6 +255,14 @@ void ZoomPlanG::execute(const void* x, long long x_stride, long long batch, void
         count_launch();
         return;
     }
+    if (!force && !split_only && rfir && zoom_rfir_fft_fits(a, f32, lg)) {
+        // raw-window FIR + n_fft 2048 transform + band in one launch (kernels_zoom_rfir.cu)
+        check(launch_zoom_rfir_fft(a, f32, lg, x, x_stride, batch, d.gnh.data(), d.sdec.p, stockham_twiddles(lg, f32),
+                                   d.band.p, out, out_stride, st),
+              "zoom fir+fft");
+        count_launch();
+        return;
+    }
     if (single && pfir && !rfir && !tfir && !pcfir && !force && !split_only) {
         // FIR and short FFT in one kernel where instantiated (configs[2] geometry)
         const cudaError_t e = launch_zoom_pfir_fft(a, zoom_pfir_lh(a), lg, f32, x, x_stride, batch, d.g.p, d.gn.p,

@@ -262,3 +262,43 @@ def test_raw_window_fir_route(prec, D, n, monkeypatch):
             assert rel_l2_rows(got, want) <= TOL_F32, (n, D, circ)
             assert rel_l2_rows(old, want) <= TOL_F32
         np.testing.assert_array_equal(got_s, got)
+
+
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+@pytest.mark.parametrize("n", [4096, 4000, 2048])
+def test_raw_window_fir_fft_fused(prec, n, monkeypatch):
+    """configs[2] as written (D = 8, 65 taps, n_fft 2048): raw-window FIR + 2048-point transform + band in one
+    launch (k_zoom_rfir_fft) against the oracle on every row of a batch larger than the grid's first wave is
+    not needed here (persistent loop: 700 records on <= 592 CTAs), against the two-launch route, with
+    unaligned strided rows, and with output rows whose gaps hold a canary."""
+    P = sk.SKG_F64 if prec == "f64" else sk.SKG_F32
+    b = 700
+    x = W.cfg3_batch(b, 4096)[:, :n] if n <= 4096 else W.sample_traces(b, n)
+    xd = _dev(x, prec)
+    xin = xd.cpu().double().numpy()
+    plan = sk.ZoomPlanGPU(n, 0.4e12, 1.2e12, W.FS, P, n_fft=2048, decimation=8, num_taps=65)
+    ref = O.ZoomPlan(n, 0.4e12, 1.2e12, W.FS, decimation=8, num_taps=65, n_fft=2048)
+    n0 = sk.launch_count()
+    got_t = plan.execute(xd)
+    assert sk.launch_count() - n0 == 1, "the one-launch route did not run"
+    got = got_t.cpu().numpy()
+    rows = [0, 1, 147, 148, 349, 591, 592, 699]
+    want = [ref(xin[i])[0] for i in rows]
+    if prec == "f64":
+        assert rel_max_rows(got[rows], want) <= TOL_F64
+    else:
+        assert rel_l2_rows(got[rows], want) <= TOL_F32
+    monkeypatch.setenv("SKG_ZOOM_NO_RFIR_FFT", "1")
+    two = plan.execute(xd).cpu().numpy()
+    monkeypatch.delenv("SKG_ZOOM_NO_RFIR_FFT")
+    if prec == "f64":
+        assert rel_max_rows(got, two) <= TOL_F64
+    else:
+        assert rel_l2_rows(got, two) <= TOL_F32
+    xu = torch.full((b, n + 13), float("nan"), dtype=xd.dtype, device=DEV)
+    xu[:, :n] = xd
+    canary = complex(7.5, -3.25)
+    buf = torch.full((b, plan.bins + 3), canary, dtype=got_t.dtype, device=DEV)
+    plan.execute(xu[:, :n], out=buf[:, : plan.bins])
+    torch.cuda.synchronize()
+    assert torch.equal(buf[:, : plan.bins], got_t) and bool((buf[:, plan.bins:] == canary).all())
