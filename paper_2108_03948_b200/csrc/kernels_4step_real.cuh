@@ -390,6 +390,12 @@ template <int LOG2L, typename C> __device__ __forceinline__ void pass_read(C (&v
     for (int q = 0; q < 16; ++q) v[q] = sm[pad16(tid + FftGeom<LOG2L>::NT * q)];
 }
 
+#ifndef SKG_RFUSED_W_F32
+#define SKG_RFUSED_W_F32 16
+#endif
+#ifndef SKG_RFUSED_W_F64
+#define SKG_RFUSED_W_F64 8
+#endif
 #ifndef SKG_RFUSED_MINB_F32_256
 #define SKG_RFUSED_MINB_F32_256 3
 #endif
@@ -401,7 +407,7 @@ template <int LOG2L, typename C> __device__ __forceinline__ void pass_read(C (&v
 #endif
 template <typename T, int LG> struct FusedCfg {
     using G = FftGeom<LG>;
-    static constexpr int W = Tile<T>::W;
+    static constexpr int W = sizeof(T) == 8 ? SKG_RFUSED_W_F64 : SKG_RFUSED_W_F32;   // rows / column pairs per unit
     static constexpr int BLOCK = G::NT * W;
     static constexpr int NCOL = G::L / (2 * W);        // column units per trace
     static constexpr int ROWS = G::L / 2 + 1;          // work rows per trace
@@ -413,7 +419,9 @@ template <typename T, int LG> struct FusedCfg {
     static constexpr size_t SMEM = ((size_t)W * (G::SMEM + 1) + G::TW_ALLOC + (size_t)W * (G::L / 2 + 1)) * sizeof(cx_t<T>);
     static constexpr bool OK = G::L >= 2 * W && G::P >= 2 && G::P <= 3 && BLOCK % 32 == 0;
     // registers: fp64 holds 16 complex = 64 registers of data (128 per thread); fp32 runs at 85 / 128
-    static constexpr int MINB = sizeof(T) == 8 ? SKG_RFUSED_THREADS_F64 / BLOCK : (BLOCK >= 512 ? SKG_RFUSED_MINB_F32_512 : SKG_RFUSED_MINB_F32_256);
+    // fp32: 768 resident threads (85 registers) for 256-point transforms, 1024 (64 registers) for 512-point ones
+    static constexpr int MINB = sizeof(T) == 8 ? SKG_RFUSED_THREADS_F64 / BLOCK
+                                               : (LG >= 9 ? SKG_RFUSED_MINB_F32_512 * 512 : SKG_RFUSED_MINB_F32_256 * 256) / BLOCK;
 };
 
 #ifndef SKG_RFUSED_CS
