@@ -302,6 +302,10 @@ def ref_runners(x_czt=None, czt=None, x_zoom=None, zoom=None, x_px=None, px=None
     return runs, kind
 
 
+def dt_name(prec):
+    return "double" if prec == "f64" else "float"
+
+
 def roofline_entry(bytes_per, flops_per, units, kern_s, hbm_gbs, fp_tflops, fp_name, kernel, traffic_prefix):
     """roof time = max(bytes / HBM, flops / FP peak); frac = roof time / measured time,
     reported in the bound's units."""
@@ -492,6 +496,23 @@ def bench_extras(args, sk, W, dev, world, pk, fp64_peak):
                                              "(reference FFT, fp64)", args.cpu_seconds / 2, kind, unit="pixels/s")
     res["cfg4_cube_H_f32"] = e
     del cd, mag, ph
+    # cfg5 long zero-padded spectra (N = 16384 -> 65536 bins, full layout): the Hermitian-half four-step in
+    # one cooperative launch, work rows in an L2-resident ring (0.5 GiB of traces in, 4 GiB of spectra out)
+    n5, L5 = 16384, 65536
+    for prec, dt, s in (("f64", torch.float64, 8), ("f32", torch.float32, 4)):
+        b5 = (1 << 29) // (n5 * s)
+        x5 = torch.from_numpy(W.sample_traces(64, n5)).to(dt).to(dev).repeat(b5 // 64, 1)
+        out = torch.empty((b5, L5), dtype=torch.complex128 if prec == "f64" else torch.complex64, device=dev)
+        l0 = sk.launch_count()
+        sk.fft_spectrum_batch(x5, L5, out=out)
+        nl = sk.launch_count() - l0
+        t, per = time_device(lambda: sk.fft_spectrum_batch(x5, L5, out=out), K, Wm, world)
+        ks = float(np.mean(per))
+        res[f"cfg5_fft65536_{prec}"] = {
+            "traces_per_s": b5 * K / t, "launches_per_call": nl,
+            "roofline": roofline_entry(n5 * s + L5 * 2 * s, 2.5 * L5 * math.log2(L5), b5, ks, pk["hbm_gbs"],
+                                       peak_of[prec][0], peak_of[prec][1], f"k4_rfused<{dt_name(prec)}, 8", None)}
+        del x5, out
     # SURVEY §8f rows 1-2, files -> files: 1024 cfg2 traces (N=1024 fp64) as reference-format CSV
     # (written once, untimed); a step = batched ingest -> fused band FFT 4096 (0.1-3 THz) -> batched
     # reference-format CSV writer. Host wall clock (file I/O and parsing are the work here).

@@ -1,2 +1,6 @@
-timeout 900 python -m pytest tests/test_gpu_multipass.py -x -q -k "real_fourstep" 2>&1 | tail -2
-timeout 300 python tools/fft4_time.py
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 1800 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
+python bench.py > gpurun_out/r2_bench_final.json 2> gpurun_out/r2_bench_final.err; tail -c 400 gpurun_out/r2_bench_final.err
+python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/r2_bench_ref.json 2>&1; head -c 400 gpurun_out/r2_bench_ref.json
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r2_launches_bench.csv python bench.py --steps 2 --warmup 1 --no-cpu > /dev/null 2>&1
+wc -l gpurun_out/r2_launches_bench.csv
