@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include "bulk_copy.cuh"
 #include "fft_device.cuh"
 #include "kernels.hpp"
 #include "kernels_czt_tm.cuh"
@@ -101,6 +102,7 @@ template <typename T, int LOG2M> struct R2cCfg {
                                 : (sizeof(T) == 4 && KCfg<T, LOG2M>::BLOCK == 512) ? SKG_R2C_MINB_F32_512
                                                                                    : KCfg<T, LOG2M>::MINB;
 };
+constexpr size_t kR2cTmaBytes = 8192;   // longest trace staged by TMA in k_fft_r2c
 template <typename T, int LOG2M, int NZ, int MODE>
 __global__ void __launch_bounds__(KCfg<T, LOG2M>::BLOCK, R2cCfg<T, LOG2M>::MINB)
 k_fft_r2c(const T* __restrict__ x, long long x_stride, long long N, int vec, long long batch,
@@ -111,11 +113,52 @@ k_fft_r2c(const T* __restrict__ x, long long x_stride, long long N, int vec, lon
     constexpr int M = G::L;
     constexpr long long L = 2LL * M;
     const long long half = N >> 1;
+#ifndef SKG_R2C_NO_TMA
+    // One transform per CTA, rows of whole 16-byte units, traces of at most 8 KB: the NEXT unit's trace
+    // arrives by one TMA bulk copy (cp.async.bulk + mbarrier) while this one is transformed, and the first
+    // pass reads its samples from shared memory instead of global memory. Measured against the L2-prefetch +
+    // LDG path (-DSKG_R2C_NO_TMA): cube 1.068 -> 1.034 ms, 1024 -> 4096 fp32 0.217 -> 0.214 ms, fp64
+    // at par; 16 KB traces (L = 16384 fp32) measured 1% slower, so they keep the LDG path.
+    __shared__ __align__(8) uint64_t stg_bar;
+    const bool tma = K::GROUPS == 1 && vec && (N * sizeof(T)) % 16 == 0 && N * sizeof(T) <= kR2cTmaBytes &&
+                     (x_stride * sizeof(T)) % 16 == 0 && (reinterpret_cast<uintptr_t>(x) % 16) == 0;
+    T* stg = reinterpret_cast<T*>((reinterpret_cast<uintptr_t>(tws + G::TW_ALLOC) + 15) & ~static_cast<uintptr_t>(15));
+    uint32_t parity = 0;
+    auto issue = [&](long long bb) {
+        if (threadIdx.x != 0 || bb >= batch) return;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&stg_bar, (uint32_t)(N * sizeof(T)));
+        bulk_g2s(stg, x + bb * x_stride, (uint32_t)(N * sizeof(T)), &stg_bar);
+    };
+    if (tma) {
+        if (threadIdx.x == 0) {
+            mbar_init(&stg_bar, 1);
+            mbar_fence_init();
+        }
+        __syncthreads();
+        issue((long long)blockIdx.x);
+    }
+#endif
     for (long long base = (long long)blockIdx.x * K::GROUPS; base < batch; base += (long long)gridDim.x * K::GROUPS) {
         const long long b = base + gid;
         const bool active = b < batch;
         C v[G::EPT];
         const T* xs = x + b * x_stride;
+#ifndef SKG_R2C_NO_TMA
+        if (tma) {
+            mbar_wait(&stg_bar, parity);
+            parity ^= 1u;
+#pragma unroll
+            for (int q = 0; q < G::EPT; ++q) {
+                v[q] = czero<C>();
+                const long long pos = tid + (long long)G::NT * q;
+                if (q < NZ && pos < half) v[q] = reinterpret_cast<const C*>(stg)[pos];
+            }
+            __syncthreads();                          // every sample read out of the staging buffer
+            issue(base + (long long)gridDim.x);       // the next trace streams in during this transform
+        } else
+#endif
+        {
         {
             const long long bn = b + (long long)gridDim.x * K::GROUPS;
             if (bn < batch) {
@@ -140,6 +183,7 @@ k_fft_r2c(const T* __restrict__ x, long long x_stride, long long N, int vec, lon
                     if (2 * pos + 1 < N) v[q].y = xs[2 * pos + 1];
                 }
             }
+        }
         }
         block_fft<false, LOG2M, NZ>(v, sm, tws, tid);
         // pair Z[k] with Z[M-k]
@@ -523,10 +567,16 @@ cudaError_t run_r2c(long long N, const T* x, long long x_stride, long long batch
     using K = KCfg<T, LOG2M>;
     using C = cx_t<T>;
     auto kern = k_fft_r2c<T, LOG2M, NZ, MODE>;
-    cudaError_t e = prep_smem(kern, K::SMEM_BYTES);
+#ifndef SKG_R2C_NO_TMA
+    const size_t smem_bytes =
+        K::SMEM_BYTES + (K::GROUPS == 1 && (size_t)N * sizeof(T) <= kR2cTmaBytes ? 16 + (size_t)N * sizeof(T) : 0);
+#else
+    const size_t smem_bytes = K::SMEM_BYTES;
+#endif
+    cudaError_t e = prep_smem(kern, smem_bytes);
     if (e != cudaSuccess) return e;
     const int vec = ((N & 1) == 0 && (x_stride & 1) == 0 && ((uintptr_t)x % (2 * sizeof(T))) == 0) ? 1 : 0;
-    kern<<<persistent_grid(kern, K::BLOCK, K::SMEM_BYTES, grid_for(batch, K::GROUPS)), K::BLOCK, K::SMEM_BYTES, st>>>(
+    kern<<<persistent_grid(kern, K::BLOCK, smem_bytes, grid_for(batch, K::GROUPS)), K::BLOCK, smem_bytes, st>>>(
         x, x_stride, N, vec, batch, (const C*)tw, (const C*)post, (C*)out, out_stride, (const C*)rtab,
         mag, phase, mp_stride, klo, khi);
     return cudaGetLastError();
