@@ -10,7 +10,8 @@
 //     z = x[., n2] + i x[., n2 + 1]; the split A = (Z[k1] + conj Z[R-k1]) / 2, B = (Z[k1] - conj Z[R-k1]) / 2i
 //     reads the partner through shared memory; A W_L^{n2 k1}, B W_L^{(n2+1) k1} go to Y[k1][n2], Y[k1][n2+1]
 //     for k1 <= R/2 as one 16 / 32-byte store — half the column transforms, half the work rows;
-//   * row unit (rowh_unit): a C-point transform per row k1 <= R/2; each result is stored at
+//   * row unit (k4_rowh, the row branch of k4_rfused; store: rowh_store): a C-point transform per row k1 <= R/2;
+//     each result is stored at
 //     k1 + R k2 and, conjugated, at the mirror (R - k1) + R (C - 1 - k2) (rows 0 and R/2 mirror onto
 //     themselves and skip it); the half layout (L/2 + 1 bins) keeps whichever of the two is <= L/2.
 // HBM traffic per trace: N s + 2 L 2s (work rows written and read once at half size, output once)
