@@ -244,3 +244,17 @@ def test_czt_fourstep_fused_ring(prec, n, m, b, variant, monkeypatch):
             assert rel_max_rows(got[i:i + 1], want) <= TOL_F64
         else:
             assert rel_l2_rows(got[i:i + 1], want) <= TOL_F32
+
+
+def test_fused_paths_stress():
+    """tools/fused_stress.py: 450 (grid size, look-ahead, shape, precision) variants of the one-launch
+    four-step spectrum and CZT, each bit-identical to the multi-launch path; a dependency cycle or a lost
+    release would show as the timeout."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "fused_stress.py")], capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "all ok: 450" in r.stdout
