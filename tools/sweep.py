@@ -2,8 +2,8 @@
 4*next_pow2(N), CZT with M in {N/4, N, 4N} over 0.1-3 THz ((M-1) W step), Zoom FFT with D in {4, 16}
 over 0.4-1.2 THz — in fp64 and fp32, batch sized to ~1 GiB of input (capped so one
 row stays within a few seconds). Each row: traces/s, achieved GB/s and TFLOP/s on the algorithmic
-counts, fraction of the roof max(bytes/HBM, flops/FP peak), and a parity spot check of
-the first two traces against the CPU oracle. Inputs are generated on the GPU (seeded pulse + noise)
+counts, fraction of the roof max(bytes/HBM, flops/FP peak), and a parity check of the
+first, a middle and the last trace of the batch against the CPU oracle. Inputs are generated on the GPU (seeded pulse + noise)
 and copied back for the check.
 
 usage: python tools/sweep.py [--out profiles/r1_cfg5_sweep.json] [--quick]
