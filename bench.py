@@ -472,7 +472,8 @@ def bench_extras(args, sk, W, dev, world, pk, fp64_peak):
             cc = zoom_counts(4096, 8, 65, zp.n_fft, zp.bins, s)
             e = {"traces_per_s": 4096 * K / t, "launches_per_call": nl,
                  "roofline": roofline_entry(cc["bytes"], cc["flops"], 4096, ks, pk["hbm_gbs"], peak_of[prec][0],
-                                            peak_of[prec][1], "zoom call", None)}
+                                            peak_of[prec][1], "zoom call",
+                                            f"unnamed>::k_zoom_{'rfir_fft' if nf else 'pcfir'}<{dt_name(prec)}, 8, 65")}
             if nf in cpu:
                 e["cpu_baseline"] = cpu[nf]
             res[f"cfg3_zoom_nfft{zp.n_fft}_{prec}"] = e
@@ -511,7 +512,8 @@ def bench_extras(args, sk, W, dev, world, pk, fp64_peak):
         res[f"cfg5_fft65536_{prec}"] = {
             "traces_per_s": b5 * K / t, "launches_per_call": nl,
             "roofline": roofline_entry(n5 * s + L5 * 2 * s, 2.5 * L5 * math.log2(L5), b5, ks, pk["hbm_gbs"],
-                                       peak_of[prec][0], peak_of[prec][1], f"k4_rfused<{dt_name(prec)}, 8", None)}
+                                       peak_of[prec][0], peak_of[prec][1], f"k4_rfused<{dt_name(prec)}, 8",
+                                       f"k4_rfused<{dt_name(prec)}, 8")}
         del x5, out
     # SURVEY §8f rows 1-2, files -> files: 1024 cfg2 traces (N=1024 fp64) as reference-format CSV
     # (written once, untimed); a step = batched ingest -> fused band FFT 4096 (0.1-3 THz) -> batched
