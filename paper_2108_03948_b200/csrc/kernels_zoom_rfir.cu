@@ -59,10 +59,17 @@ __device__ __forceinline__ void unit_elems(const double2& v, double (&e)[2]) { e
 #ifndef SKG_RFIR_WARPS
 #define SKG_RFIR_WARPS 4
 #endif
-template <typename T> __host__ __device__ constexpr int rf_nbuf() { return sizeof(T) == 8 ? 1 : 2; }
+#ifndef SKG_RFIR_NBUF_F64
+#define SKG_RFIR_NBUF_F64 1
+#endif
+#ifndef SKG_RFIR_WARPS_F64
+#define SKG_RFIR_WARPS_F64 SKG_RFIR_WARPS
+#endif
+template <typename T> __host__ __device__ constexpr int rf_nbuf() { return sizeof(T) == 8 ? SKG_RFIR_NBUF_F64 : 2; }
+template <typename T> __host__ __device__ constexpr int rf_warps() { return sizeof(T) == 8 ? SKG_RFIR_WARPS_F64 : SKG_RFIR_WARPS; }
 
 template <typename T, int D, int NTAPS, int K>
-__global__ void __launch_bounds__(SKG_RFIR_WARPS * 32)
+__global__ void __launch_bounds__(rf_warps<T>() * 32)
 k_zoom_rfir(const T* __restrict__ x, long long x_stride, unsigned batch, int aligned, ZoomArgs a,
             const __grid_constant__ RfTaps<T, NTAPS> tp, const cx_t<T>* __restrict__ S, cx_t<T>* __restrict__ zb,
             long long z_stride) {
@@ -85,7 +92,7 @@ k_zoom_rfir(const T* __restrict__ x, long long x_stride, unsigned batch, int ali
     const int U = (int)a.U;
     const unsigned parts = (unsigned)(a.nout + RG::PART - 1) / RG::PART;
     const unsigned nitem = batch * parts;   // < 2^31 (checked by the launcher)
-    const unsigned w0 = blockIdx.x * SKG_RFIR_WARPS + warp, wstride = gridDim.x * SKG_RFIR_WARPS;
+    const unsigned w0 = blockIdx.x * rf_warps<T>() + warp, wstride = gridDim.x * rf_warps<T>();
     const bool wrap = a.circular && a.mwrap > 0;
     // fill: unit un of the item covers samples i0 + un EU .. + EU - 1, i0 = p PART D - PADL
     auto fill = [&](unsigned item, int slot) {
@@ -453,7 +460,7 @@ cudaError_t run_rfir(const ZoomArgs& a, const T* x, long long xs, long long batc
     }
     constexpr int EU = RG::EU;
     const size_t smem = (NTAPS * sizeof(C) + 15) / 16 * 16 +
-                        (size_t)SKG_RFIR_WARPS * rf_nbuf<T>() * (RG::BUF + (NTAPS - 1 + EU - 1) / EU * EU) * sizeof(T);
+                        (size_t)rf_warps<T>() * rf_nbuf<T>() * (RG::BUF + (NTAPS - 1 + EU - 1) / EU * EU) * sizeof(T);
     auto kern = k_zoom_rfir<T, D, NTAPS, K>;
     cudaError_t e = prep_smem(kern, smem);
     if (e != cudaSuccess) return e;
@@ -462,8 +469,9 @@ cudaError_t run_rfir(const ZoomArgs& a, const T* x, long long xs, long long batc
     // 16-byte copies need aligned rows (and, for the wrap tail, U a whole number of units); otherwise the
     // same kernel copies element by element — the route, and so the bits, do not depend on the alignment
     const int aligned = reinterpret_cast<uintptr_t>(x) % 16 == 0 && xs % EU == 0 && a.U % EU == 0;
-    const unsigned grid = persistent_grid(kern, SKG_RFIR_WARPS * 32, smem, (batch * parts + SKG_RFIR_WARPS - 1) / SKG_RFIR_WARPS);
-    kern<<<grid, SKG_RFIR_WARPS * 32, smem, st>>>(x, xs, (unsigned)batch, aligned, a, tp, (const C*)S, (C*)zb, z_stride);
+    constexpr int NW = rf_warps<T>();
+    const unsigned grid = persistent_grid(kern, NW * 32, smem, (batch * parts + NW - 1) / NW);
+    kern<<<grid, NW * 32, smem, st>>>(x, xs, (unsigned)batch, aligned, a, tp, (const C*)S, (C*)zb, z_stride);
     return cudaGetLastError();
 }
 
