@@ -23,7 +23,7 @@ namespace skg {
 #define SKG_CZTF_THREADS_F64 512   // resident threads per SM the fp64 register cap targets
 #endif
 #ifndef SKG_CZTF_MINB_F32
-#define SKG_CZTF_MINB_F32 3
+#define SKG_CZTF_MINB_F32 4   // 64 registers, 4 CTAs of 256 threads per SM: L = 2^15 rows 5.9 -> 5.2 ms (3: 80 registers; 2: 7.0 ms)
 #endif
 // exchange barrier of a row transform under the row-major mapping: the NT threads of a row are a warp or
 // part of one (NT <= 32: __syncwarp), else a named barrier per row (ids 1.., 0 is __syncthreads)

@@ -14,7 +14,9 @@ from paper_2108_03948_b200 import workloads as W  # noqa: E402
 tag = f"fused={os.environ.get('SKG_4STEP_FUSED', '1')}"
 rows = [(3000, 12000), (4096, 16384), (16384, 4096), (16384, 16384), (16384, 65536), (65536, 16384), (65536, 65536),
         (65536, 262144)]
-for prec, dt, s in (("f64", torch.float64, 8), ("f32", torch.float32, 4)):
+import os as _os
+PRECS = [p for p in (("f64", torch.float64, 8), ("f32", torch.float32, 4)) if p[0] in _os.environ.get("SKG_PRECS", "f64,f32")]
+for prec, dt, s in PRECS:
     for n, m in rows:
         batch = max(64, ((1 << 30) // (n * s)) // 64 * 64)
         x = torch.from_numpy(W.sample_traces(64, n)).to(dt).cuda().repeat(batch // 64, 1)
