@@ -154,7 +154,7 @@ def test_real_fourstep_paths(prec, L, real_path, monkeypatch):
 
 
 @pytest.mark.parametrize("variant", ["default", "short-lookahead", "small-grid"])
-@pytest.mark.parametrize("prec,L,b", [("f32", 65536, 260), ("f64", 65536, 200), ("f32", 262144, 64), ("f64", 262144, 64)])
+@pytest.mark.parametrize("prec,L,b", [("f32", 65536, 330), ("f64", 65536, 200), ("f32", 262144, 64), ("f64", 262144, 64)])
 def test_real_fourstep_fused_ring(prec, L, b, variant, monkeypatch):
     """The one-launch Hermitian four-step (k4_rfused: column and row units interleaved in one persistent
     cooperative grid, work rows in an L2-resident ring reused every `slots` traces, release/acquire
