@@ -65,7 +65,10 @@ __device__ __forceinline__ void unit_elems(const double2& v, double (&e)[2]) { e
 #ifndef SKG_RFIR_WARPS_F64
 #define SKG_RFIR_WARPS_F64 SKG_RFIR_WARPS
 #endif
-template <typename T> __host__ __device__ constexpr int rf_nbuf() { return sizeof(T) == 8 ? SKG_RFIR_NBUF_F64 : 2; }
+#ifndef SKG_RFIR_NBUF_F32
+#define SKG_RFIR_NBUF_F32 2
+#endif
+template <typename T> __host__ __device__ constexpr int rf_nbuf() { return sizeof(T) == 8 ? SKG_RFIR_NBUF_F64 : SKG_RFIR_NBUF_F32; }
 template <typename T> __host__ __device__ constexpr int rf_warps() { return sizeof(T) == 8 ? SKG_RFIR_WARPS_F64 : SKG_RFIR_WARPS; }
 
 template <typename T, int D, int NTAPS, int K>
